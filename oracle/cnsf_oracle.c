@@ -1,0 +1,498 @@
+/*
+ * cnsf_oracle.c -- plain, slow, FP64 CPU oracle of the CNSF fan-beam forward
+ * projection y = A c and its adjoint c = A^T y (Zhang & Entezari, arXiv
+ * 1907.10526).  Every function follows the paper's construction step by step
+ * (explicit points, lines and planes), NOT the closed forms the CUDA path
+ * uses, so a reader can check it against the paper by eye.
+ *
+ * TEST INFRASTRUCTURE ONLY (see cnsf_oracle.h).  Only tests/, the graft
+ * smoke() check and bench.py's cpu_baseline / --impl reference legs may load
+ * this library.
+ *
+ * Parity pins: every exported function is pinned by tests/test_oracle_*.py
+ * against values fixed by the paper, SPEC worked examples or mathematics
+ * (chord lengths, dense convolutions, exact bin integrals, adjointness).
+ * Absolute curve values of Figs. 5-7 are "parity unpinned" (figures lost).
+ *
+ * Rounding: FP64, round to nearest, compiled with -ffp-contract=off and no
+ * fast-math (ledger #16).
+ */
+#include "cnsf_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_PI 3.14159265358979323846
+
+/* Degenerate-direction threshold, ledger #7: a projected direction with
+ * |zeta| < 1e-6 h is a delta ("reduces to a delta function ... gets
+ * eliminated in the convolutions"). */
+#define ORC_EPS_REL 1e-6
+
+static double dot2(const double a[2], const double b[2]) { return a[0] * b[0] + a[1] * b[1]; }
+
+/* theta_v = 2 pi v / N_v, counter-clockwise from +x (ledger #9). */
+double orc_view_angle(const orc_geometry* g, int32_t v)
+{
+    return 2.0 * ORC_PI * (double)v / (double)g->n_views;
+}
+
+/* s_j = (j - (N_s - 1)/2) Delta_s (ledger #10). */
+double orc_bin_center(const orc_geometry* g, int32_t j)
+{
+    return ((double)j - 0.5 * (double)(g->n_det - 1)) * g->det_pitch;
+}
+
+/* Pixel centre k_n of Eq. 5: row-major grid centred on the rotation centre,
+ * row 0 at +y (ledger #13). */
+void orc_pixel_center(const orc_geometry* g, int32_t row, int32_t col, double k[2])
+{
+    const double c = 0.5 * (double)(g->n - 1);
+    k[0] = ((double)col - c) * g->pixel;
+    k[1] = (c - (double)row) * g->pixel;
+}
+
+/* Sec. II-A: viewing direction u, source p = D_po u, detector axis
+ * e spanning u^perp with the fixed orientation e = (-u_y, u_x). */
+void orc_view_frame(const orc_geometry* g, double theta, double u[2], double e[2], double p[2])
+{
+    u[0] = cos(theta);
+    u[1] = sin(theta);
+    e[0] = -u[1];
+    e[1] = u[0];
+    p[0] = g->sid * u[0];
+    p[1] = g->sid * u[1];
+}
+
+/* Physical detector line through d = -D_so u, coordinate s along e
+ * (ledger #6). */
+static void detector_point_f(const orc_geometry* g, const double u[2], const double e[2],
+                             double s, double q[2])
+{
+    const double d_so = g->sdd - g->sid;
+    q[0] = -d_so * u[0] + s * e[0];
+    q[1] = -d_so * u[1] + s * e[1];
+}
+
+void orc_detector_point(const orc_geometry* g, double theta, double s, double q[2])
+{
+    double u[2], e[2], p[2];
+    orc_view_frame(g, theta, u, e, p);
+    detector_point_f(g, u, e, s, q);
+}
+
+/* Eq. 11: the ray of detector coordinate s has unit direction
+ * v(s) from the source to the detector point (ledger #5), and R_{v(s)^perp}
+ * is the unit row r perpendicular to v, oriented so that r.e > 0. */
+static void ray_frame_f(const orc_geometry* g, const double u[2], const double e[2],
+                        const double p[2], double s, double v[2], double r[2])
+{
+    double q[2];
+    detector_point_f(g, u, e, s, q);
+    const double dx = q[0] - p[0], dy = q[1] - p[1];
+    const double len = sqrt(dx * dx + dy * dy);
+    v[0] = dx / len;
+    v[1] = dy / len;
+    r[0] = -v[1];
+    r[1] = v[0];
+    if (dot2(r, e) < 0.0) {
+        r[0] = -r[0];
+        r[1] = -r[1];
+    }
+}
+
+void orc_ray_frame(const orc_geometry* g, double theta, double s, double v[2], double r[2])
+{
+    double u[2], e[2], p[2];
+    orc_view_frame(g, theta, u, e, p);
+    ray_frame_f(g, u, e, p, s, v, r);
+}
+
+/* Eq. 4: perspective projection P(x) of an image point onto the detector:
+ * the line from p through x meets the detector line at
+ * s = D_ps (x - p).e / ((p - x).u)  (similar triangles). */
+static double perspective_f(const orc_geometry* g, const double u[2], const double e[2],
+                            const double p[2], const double x[2])
+{
+    const double xp[2] = {x[0] - p[0], x[1] - p[1]};
+    const double depth = -dot2(xp, u); /* (p - x).u */
+    return g->sdd * dot2(xp, e) / depth;
+}
+
+double orc_perspective_project(const orc_geometry* g, double theta, const double x[2])
+{
+    double u[2], e[2], p[2];
+    orc_view_frame(g, theta, u, e, p);
+    return perspective_f(g, u, e, p, x);
+}
+
+/* Eq. 13: tau' is the perspective image of the bin
+ * [s - tau/2, s + tau/2] on the plane v(s)^perp.  Ledger #1: the plane passes
+ * through the pixel centre k (the basis function sits at the origin of the
+ * derivation).  Each bin edge q+- is projected from the source p
+ * onto that plane by an explicit line-plane intersection, and tau' is the
+ * distance between the two images measured along r (perspective division =
+ * the parameter t+-). */
+static double effective_blur_f(const orc_geometry* g, const double u[2], const double e[2],
+                               const double p[2], double s, const double v[2],
+                               const double r[2], const double k[2])
+{
+    const double tau = g->det_width;
+    double qp[2], qm[2];
+    detector_point_f(g, u, e, s + 0.5 * tau, qp);
+    detector_point_f(g, u, e, s - 0.5 * tau, qm);
+    const double kp[2] = {k[0] - p[0], k[1] - p[1]};
+    const double dp[2] = {qp[0] - p[0], qp[1] - p[1]};
+    const double dm[2] = {qm[0] - p[0], qm[1] - p[1]};
+    /* plane {X : (X - k).v = 0}; line X = p + t (q - p) */
+    const double tp = dot2(kp, v) / dot2(dp, v);
+    const double tm = dot2(kp, v) / dot2(dm, v);
+    const double xp[2] = {p[0] + tp * dp[0], p[1] + tp * dp[1]};
+    const double xm[2] = {p[0] + tm * dm[0], p[1] + tm * dm[1]};
+    return fabs(dot2(xp, r) - dot2(xm, r));
+}
+
+double orc_effective_blur(const orc_geometry* g, double theta, double s, const double k[2])
+{
+    double u[2], e[2], p[2], v[2], r[2];
+    orc_view_frame(g, theta, u, e, p);
+    ray_frame_f(g, u, e, p, s, v, r);
+    return effective_blur_f(g, u, e, p, s, v, r, k);
+}
+
+/* centred box splines are symmetric, so take |zeta|;
+ * a direction below eps is a delta function and is eliminated. */
+int orc_canonicalize(int32_t m, const double* raw, double eps, double* out)
+{
+    int cnt = 0;
+    for (int i = 0; i < m; ++i) {
+        const double a = fabs(raw[i]);
+        if (a >= eps) out[cnt++] = a;
+    }
+    return cnt;
+}
+
+/* one-sided power (x)_+^d, with the step convention (0)_+^0 = 1 */
+static double truncated_power(double x, int d)
+{
+    if (d == 0) return x >= 0.0 ? 1.0 : 0.0;
+    if (x <= 0.0) return 0.0;
+    double y = 1.0;
+    for (int i = 0; i < d; ++i) y *= x;
+    return y;
+}
+
+/* Centred univariate box spline with directions a_1..a_m > 0 (P:195-206 by
+ * convolution; evaluated as in Eq. 12 / Eq. 14 by forward differences of the
+ * one-sided power):
+ *   M(x) = 1/((m-1)! prod a_i) sum_{S subset {1..m}} (-1)^{|S|} (x + sigma - sum_{i in S} a_i)_+^{m-1}
+ * with sigma = sum a_i / 2 (centring).  Zero outside the open
+ * support |x| < sigma (ledger #15), where it is not evaluated. */
+double orc_box_spline(int32_t m, const double* a, double x)
+{
+    if (m < 1 || m > 8) return 0.0;
+    double sigma = 0.0, prod = 1.0, fact = 1.0;
+    for (int i = 0; i < m; ++i) {
+        sigma += a[i];
+        prod *= a[i];
+    }
+    sigma *= 0.5;
+    if (!(fabs(x) < sigma)) return 0.0;
+    for (int i = 2; i <= m - 1; ++i) fact *= (double)i;
+    double sum = 0.0;
+    for (int mask = 0; mask < (1 << m); ++mask) {
+        double shift = 0.0;
+        int bits = 0;
+        for (int i = 0; i < m; ++i)
+            if (mask & (1 << i)) {
+                shift += a[i];
+                ++bits;
+            }
+        const double t = truncated_power(x + sigma - shift, m - 1);
+        sum += (bits & 1) ? -t : t;
+    }
+    return sum / (fact * prod);
+}
+
+/* Eq. 12: P_u{M_Xi}(s) = Delta_zeta1 Delta_zeta2 (R_{v(s)^perp} p)_+
+ * with the pixel moved to the origin (Eq. 4): the argument is
+ * s' = r.(p - k), and Z(s) = R_{v(s)^perp} Xi with Xi = h I, i.e.
+ * zeta1 = r.(h,0), zeta2 = r.(0,h).  M_Xi with Xi = h I has
+ * density 1/h^2; the indicator pixel is h^2 M_Xi (ledger #4). */
+static double footprint_f(const orc_geometry* g, const double p[2], const double r[2],
+                          const double k[2])
+{
+    const double h = g->pixel;
+    const double pk[2] = {p[0] - k[0], p[1] - k[1]};
+    const double x = dot2(r, pk);
+    const double raw[2] = {h * r[0], h * r[1]};
+    double a[2];
+    const int m = orc_canonicalize(2, raw, ORC_EPS_REL * h, a);
+    return h * h * orc_box_spline(m, a, x);
+}
+
+double orc_footprint(const orc_geometry* g, double theta, double s, const double k[2])
+{
+    double u[2], e[2], p[2], v[2], r[2];
+    orc_view_frame(g, theta, u, e, p);
+    ray_frame_f(g, u, e, p, s, v, r);
+    return footprint_f(g, p, r, k);
+}
+
+/* Eq. 14: the blurred fan-beam footprint
+ *   Delta_zeta1 Delta_zeta2 Delta_tau' (R_{v(s)^perp} p)_+^2 / 2!
+ * i.e. the 3-direction box spline M_{[zeta1, zeta2, tau']} at s' = r.(p - k),
+ * with tau' from Eq. 13.  Unit-mass blur (averaging over the bin, ledger #3)
+ * and the h^2 indicator factor (ledger #4). */
+static double weight_f(const orc_geometry* g, const double u[2], const double e[2],
+                       const double p[2], double s, const double v[2], const double r[2],
+                       const double k[2])
+{
+    const double h = g->pixel;
+    const double pk[2] = {p[0] - k[0], p[1] - k[1]};
+    const double x = dot2(r, pk);
+    const double tau_eff = effective_blur_f(g, u, e, p, s, v, r, k);
+    const double raw[3] = {h * r[0], h * r[1], tau_eff};
+    double a[3];
+    const int m = orc_canonicalize(3, raw, ORC_EPS_REL * h, a);
+    return h * h * orc_box_spline(m, a, x);
+}
+
+double orc_weight(const orc_geometry* g, double theta, double s, const double k[2])
+{
+    double u[2], e[2], p[2], v[2], r[2];
+    orc_view_frame(g, theta, u, e, p);
+    ray_frame_f(g, u, e, p, s, v, r);
+    return weight_f(g, u, e, p, s, v, r, k);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Projectors (Eq. 6 and its adjoint).                                       */
+
+static int geometry_ok(const orc_geometry* g)
+{
+    if (!g || g->n < 1 || !(g->pixel > 0) || g->n_views < 1 || g->n_det < 1) return 0;
+    if (!(g->det_pitch > 0) || !(g->det_width > 0)) return 0;
+    if (!(g->sid > 0) || !(g->sdd >= g->sid)) return 0;
+    /* S:249/S:251 (ledger #14): every pixel strictly between source and
+     * detector for every view, i.e. the FOV's circumscribed circle strictly
+     * inside the source orbit. */
+    const double radius = 0.5 * (double)g->n * g->pixel * sqrt(2.0);
+    if (!(radius < g->sid)) return 0;
+    return 1;
+}
+
+typedef struct {
+    double u[2], e[2], p[2];
+    double* v; /* [n_det][2] */
+    double* r; /* [n_det][2] */
+} view_t;
+
+static void view_build(const orc_geometry* g, int32_t vglob, view_t* V)
+{
+    orc_view_frame(g, orc_view_angle(g, vglob), V->u, V->e, V->p);
+    for (int32_t j = 0; j < g->n_det; ++j)
+        ray_frame_f(g, V->u, V->e, V->p, orc_bin_center(g, j), V->v + 2 * j, V->r + 2 * j);
+}
+
+/* Candidate bins of pixel k in one view: the perspective images of the four
+ * pixel corners (Eq. 4) bound the unblurred support; the blurred support is
+ * wider by about tau/2 on each side.  A margin of tau + Delta_s covers it; the
+ * exact support test inside orc_box_spline decides, so any
+ * superset gives the same result (pinned by a test that widens the margin). */
+static double g_candidate_margin_scale = 1.0;
+
+static void candidate_bins(const orc_geometry* g, const view_t* V, const double k[2],
+                           int32_t* jlo, int32_t* jhi)
+{
+    const double hh = 0.5 * g->pixel;
+    double smin = 1e300, smax = -1e300;
+    for (int c = 0; c < 4; ++c) {
+        const double corner[2] = {k[0] + ((c & 1) ? hh : -hh), k[1] + ((c & 2) ? hh : -hh)};
+        const double s = perspective_f(g, V->u, V->e, V->p, corner);
+        if (s < smin) smin = s;
+        if (s > smax) smax = s;
+    }
+    const double margin = g_candidate_margin_scale * (g->det_width + g->det_pitch);
+    const double c0 = 0.5 * (double)(g->n_det - 1);
+    double lo = ceil((smin - margin) / g->det_pitch + c0);
+    double hi = floor((smax + margin) / g->det_pitch + c0);
+    if (lo < 0) lo = 0;
+    if (hi > g->n_det - 1) hi = g->n_det - 1;
+    *jlo = (int32_t)lo;
+    *jhi = (int32_t)hi;
+}
+
+void orc_set_candidate_margin_scale(double s) { g_candidate_margin_scale = s; }
+
+static int nthreads_of(int32_t threads)
+{
+#ifdef _OPENMP
+    return threads > 0 ? threads : omp_get_max_threads();
+#else
+    (void)threads;
+    return 1;
+#endif
+}
+
+int orc_forward(const orc_geometry* g, const double* image, double* sino, int32_t batch,
+                int32_t v0, int32_t nv, int32_t threads)
+{
+    if (!geometry_ok(g) || !image || !sino || batch < 1 || v0 < 0 || nv < 0 ||
+        v0 + nv > g->n_views)
+        return -1;
+    const int32_t n = g->n, ns = g->n_det;
+    const int nt = nthreads_of(threads);
+    const int64_t tasks = (int64_t)batch * nv;
+    int64_t task;
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1)
+    for (task = 0; task < tasks; ++task) {
+        const int32_t b = (int32_t)(task / nv), vl = (int32_t)(task % nv);
+        view_t V;
+        V.v = (double*)malloc(sizeof(double) * 2 * ns);
+        V.r = (double*)malloc(sizeof(double) * 2 * ns);
+        view_build(g, v0 + vl, &V);
+        double* y = sino + ((int64_t)b * nv + vl) * ns;
+        for (int32_t j = 0; j < ns; ++j) y[j] = 0.0;
+        const double* c = image + (int64_t)b * n * n;
+        /* y_j = sum_n c_n P_{u,tau}{phi}(s_j - P(k_n))  (Eq. 6) */
+        for (int32_t row = 0; row < n; ++row)
+            for (int32_t col = 0; col < n; ++col) {
+                double k[2];
+                orc_pixel_center(g, row, col, k);
+                int32_t jlo, jhi;
+                candidate_bins(g, &V, k, &jlo, &jhi);
+                const double cv = c[(int64_t)row * n + col];
+                for (int32_t j = jlo; j <= jhi; ++j) {
+                    const double w = weight_f(g, V.u, V.e, V.p, orc_bin_center(g, j),
+                                              V.v + 2 * j, V.r + 2 * j, k);
+                    y[j] += cv * w;
+                }
+            }
+        free(V.v);
+        free(V.r);
+    }
+    return 0;
+}
+
+static view_t* views_build_all(const orc_geometry* g, int32_t v0, int32_t nv, int nt)
+{
+    view_t* Vs = (view_t*)calloc((size_t)(nv > 0 ? nv : 1), sizeof(view_t));
+    int32_t vl;
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (vl = 0; vl < nv; ++vl) {
+        Vs[vl].v = (double*)malloc(sizeof(double) * 2 * g->n_det);
+        Vs[vl].r = (double*)malloc(sizeof(double) * 2 * g->n_det);
+        view_build(g, v0 + vl, &Vs[vl]);
+    }
+    return Vs;
+}
+
+static void views_free(view_t* Vs, int32_t nv)
+{
+    for (int32_t i = 0; i < nv; ++i) {
+        free(Vs[i].v);
+        free(Vs[i].r);
+    }
+    free(Vs);
+}
+
+/* c_k = sum_{v,j} y[v][j] W(v, j, k): the adjoint with the identical weight
+ * function ("exact algebraic adjoint"). */
+static double back_one(const orc_geometry* g, const view_t* Vs, const double* y, int32_t nv,
+                       int32_t row, int32_t col)
+{
+    const int32_t ns = g->n_det;
+    double k[2];
+    orc_pixel_center(g, row, col, k);
+    double acc = 0.0;
+    for (int32_t vl = 0; vl < nv; ++vl) {
+        const view_t* V = &Vs[vl];
+        int32_t jlo, jhi;
+        candidate_bins(g, V, k, &jlo, &jhi);
+        for (int32_t j = jlo; j <= jhi; ++j) {
+            const double w = weight_f(g, V->u, V->e, V->p, orc_bin_center(g, j), V->v + 2 * j,
+                                      V->r + 2 * j, k);
+            acc += y[(int64_t)vl * ns + j] * w;
+        }
+    }
+    return acc;
+}
+
+int orc_back(const orc_geometry* g, const double* sino, double* image, int32_t batch,
+             int32_t v0, int32_t nv, int32_t threads)
+{
+    if (!geometry_ok(g) || !image || !sino || batch < 1 || v0 < 0 || nv < 0 ||
+        v0 + nv > g->n_views)
+        return -1;
+    const int32_t n = g->n, ns = g->n_det;
+    const int nt = nthreads_of(threads);
+    view_t* Vs = views_build_all(g, v0, nv, nt);
+    const int64_t tasks = (int64_t)batch * n;
+    int64_t task;
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1)
+    for (task = 0; task < tasks; ++task) {
+        const int32_t b = (int32_t)(task / n), row = (int32_t)(task % n);
+        const double* y = sino + (int64_t)b * nv * ns;
+        double* out = image + ((int64_t)b * n + row) * n;
+        for (int32_t col = 0; col < n; ++col) out[col] = back_one(g, Vs, y, nv, row, col);
+    }
+    views_free(Vs, nv);
+    return 0;
+}
+
+int orc_back_pixels(const orc_geometry* g, const double* sino, int32_t batch, int32_t v0,
+                    int32_t nv, const int32_t* rows, const int32_t* cols, int32_t npix,
+                    double* out, int32_t threads)
+{
+    if (!geometry_ok(g) || !sino || !out || batch < 1 || v0 < 0 || nv < 0 ||
+        v0 + nv > g->n_views || npix < 0)
+        return -1;
+    for (int32_t i = 0; i < npix; ++i)
+        if (rows[i] < 0 || rows[i] >= g->n || cols[i] < 0 || cols[i] >= g->n) return -1;
+    const int nt = nthreads_of(threads);
+    view_t* Vs = views_build_all(g, v0, nv, nt);
+    const int64_t tasks = (int64_t)batch * npix;
+    int64_t task;
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1)
+    for (task = 0; task < tasks; ++task) {
+        const int32_t b = (int32_t)(task / npix), i = (int32_t)(task % npix);
+        out[task] = back_one(g, Vs, sino + (int64_t)b * nv * g->n_det, nv, rows[i], cols[i]);
+    }
+    views_free(Vs, nv);
+    return 0;
+}
+
+int64_t orc_count_weights(const orc_geometry* g, int32_t v0, int32_t nv, int32_t threads)
+{
+    if (!geometry_ok(g) || v0 < 0 || nv < 0 || v0 + nv > g->n_views) return -1;
+    const int nt = nthreads_of(threads);
+    const int32_t n = g->n;
+    int64_t total = 0;
+    int32_t vl;
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1) reduction(+ : total)
+    for (vl = 0; vl < nv; ++vl) {
+        view_t V;
+        V.v = (double*)malloc(sizeof(double) * 2 * g->n_det);
+        V.r = (double*)malloc(sizeof(double) * 2 * g->n_det);
+        view_build(g, v0 + vl, &V);
+        for (int32_t row = 0; row < n; ++row)
+            for (int32_t col = 0; col < n; ++col) {
+                double k[2];
+                orc_pixel_center(g, row, col, k);
+                int32_t jlo, jhi;
+                candidate_bins(g, &V, k, &jlo, &jhi);
+                for (int32_t j = jlo; j <= jhi; ++j)
+                    if (weight_f(g, V.u, V.e, V.p, orc_bin_center(g, j), V.v + 2 * j,
+                                 V.r + 2 * j, k) != 0.0)
+                        ++total;
+            }
+        free(V.v);
+        free(V.r);
+    }
+    return total;
+}
