@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark: CNSF fan-beam forward + back-projection pairs per second.
+
+One step = one FP+BP pair over one image of the configured workload (default
+config 2: 512^2 Shepp-Logan, 720 views, 1024 bins, SID 500 / SDD 1000 mm):
+  y_g = A_g c            (cbp_forward over this rank's view shard)
+  c'  = sum_g A_g^T y_g  (cbp_back over the shard, then NCCL all_reduce)
+With N GPUs the views are sharded (strong scaling: the pair's work is fixed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2]
+  python bench.py --impl reference ...   # the FP64 CPU oracle arm
+
+Prints ONE JSON line on rank 0.  Timing: CUDA events on the launching stream,
+per step, L2 flushed (256 MiB write) between steps outside the events, max
+over ranks.  See DESIGN.md section 6 for the roofline arithmetic.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+METRIC = "fwd+back projection pairs/sec at 512²×720 views×1024 dets; % FP32/HBM roofline"
+FLOPS_PER_WEIGHT = 32  # canonical FP32 flops per nonzero weight
+WORKLOADS = {
+    "1": "config1: 64x64 Shepp-Logan, 90 views, 128 bins, SID 500 / SDD 1000 mm",
+    "2": "config2: 512x512 Shepp-Logan, 720 views, 1024 bins, SID 500 / SDD 1000 mm",
+    "3": "config3: 1024x1024 Shepp-Logan, 1440 views, 2048 bins, SID 500 / SDD 1000 mm",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="cnsf", choices=["cnsf", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def shard(n_views: int, rank: int, world: int):
+    """contiguous view block of this rank."""
+    base, rem = divmod(n_views, world)
+    v0 = rank * base + min(rank, rem)
+    return v0, base + (1 if rank < rem else 0)
+
+
+def weight_counts(cfg: str):
+    path = os.path.join(ROOT, "tests", "golden", "weight_counts.json")
+    try:
+        return json.load(open(path))[cfg]["per_view"]
+    except (OSError, KeyError):
+        return None
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        return {}
+
+
+def traffic_table():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/cbp_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.1)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+                pw.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        busy = [s for s in sm if s > 0]
+        return {"sm_mhz": statistics.median(busy) if busy else 0.0, "sm_max_mhz": max(mx),
+                "power_w_max": max(pw), "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """The FP64 CPU oracle as it stands, on a bounded view sample per step."""
+    if rank != 0:
+        return
+    import oracle as O
+    g = W.geometry(args.config)
+    img = W.shepp_logan(g["n"]).astype(np.float64)
+    cores = os.cpu_count() or 1
+    O.build()
+    # size each step so the whole run takes about a minute
+    t0 = time.perf_counter()
+    y = O.forward(g, img, view_begin=0, view_count=1, threads=cores)
+    O.back(g, y, view_begin=0, threads=cores)
+    per_view = time.perf_counter() - t0
+    budget = 60.0 / max(1, args.steps + args.warmup)
+    nvs = int(max(1, min(g["n_views"], budget / max(per_view, 1e-6))))
+    times = []
+    for k in range(args.warmup + args.steps):
+        v0 = (k * 37) % (g["n_views"] - nvs + 1)
+        t0 = time.perf_counter()
+        y = O.forward(g, img, view_begin=v0, view_count=nvs, threads=cores)
+        O.back(g, y, view_begin=v0, threads=cores)
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t_pair = sum(times) / len(times) * g["n_views"] / nvs  # extrapolated full pair
+    value = 1.0 / t_pair
+    sample = (f"{nvs} of {g['n_views']} views per step (FP+BP, views rotated), "
+              f"extrapolated x{g['n_views'] / nvs:.1f} to one pair")
+    line = {
+        "metric": METRIC, "value": value, "unit": "pairs/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_pair * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "n": g["n"], "n_views": g["n_views"],
+                   "n_det": g["n_det"], "parallelism": "cpu-openmp"},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg: str, target_s: float = 12.0):
+    """oracle FP+BP on a bounded view sample of the same workload (rank 0, N=1)."""
+    import oracle as O
+    g = W.geometry(cfg)
+    img = W.shepp_logan(g["n"]).astype(np.float64)
+    cores = os.cpu_count() or 1
+    O.build()
+    t0 = time.perf_counter()
+    y = O.forward(g, img, view_begin=0, view_count=2, threads=cores)
+    O.back(g, y, view_begin=0, threads=cores)
+    per_view = (time.perf_counter() - t0) / 2
+    nvs = int(max(2, min(g["n_views"], target_s / max(per_view, 1e-6))))
+    t0 = time.perf_counter()
+    y = O.forward(g, img, view_begin=0, view_count=nvs, threads=cores)
+    O.back(g, y, view_begin=0, threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": nvs / (dt * g["n_views"]), "unit": "pairs/s", "cores": cores,
+            "kind": "oracle",
+            "sample": f"FP+BP over views 0..{nvs - 1} of {g['n_views']} ({dt:.1f} s wall), "
+                      f"scaled to one full pair"}
+
+
+# -------------------------------------------------------------------- CUDA arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1907_10526_b200 as cbp
+
+    assert args.warmup >= 3, "at least 3 warm-up steps"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    g = W.geometry(args.config)
+    v0, nv = shard(g["n_views"], rank, world)
+    n, ns = g["n"], g["n_det"]
+
+    img = torch.from_numpy(W.shepp_logan(n)).to(dev)
+    sino = torch.empty((nv, ns), dtype=torch.float32, device=dev)
+    out = torch.empty((n, n), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        cbp.forward(g, img, sino, view_begin=v0, view_count=nv, stream=stream)
+        if ev:
+            ev[1].record(stream)
+        cbp.back(g, sino, out, view_begin=v0, stream=stream)
+        if ev:
+            ev[2].record(stream)
+        if world > 1:
+            dist.all_reduce(out)
+        if ev:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = cbp.launch_count()
+    for k in range(args.steps):
+        flush.zero_()  # L2 flush, outside the timed events
+        step(evs[k])
+    torch.cuda.synchronize()
+    launches = cbp.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if clocks else None
+
+    fp_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    bp_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    ar_ms = [e[2].elapsed_time(e[3]) for e in evs]
+    step_ms = [e[0].elapsed_time(e[3]) for e in evs]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    value = args.steps / (total_ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (ALU / FP32-pipe bound)
+    counts = weight_counts(args.config)
+    nw = int(sum(counts[v0:v0 + nv])) if counts else None
+    props = torch.cuda.get_device_properties(dev)
+    peaks = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz") or (clk or {}).get("sm_max_mhz") or 1965.0)
+    peak_tflops = props.multi_processor_count * 128 * 2 * sm_max * 1e6 / 1e12
+    fp_avg, bp_avg = statistics.mean(fp_ms), statistics.mean(bp_ms)
+    kernels = {}
+    for name, ms in (("fp", fp_avg), ("bp", bp_avg)):
+        ach = nw * FLOPS_PER_WEIGHT / (ms * 1e-3) / 1e12 if nw else None
+        kernels[name] = {"ms": ms, "tflops": ach, "frac": ach / peak_tflops if ach else None,
+                         "weights_per_launch": nw}
+    dom = "bp" if bp_avg >= fp_avg else "fp"
+    traffic = traffic_table().get(args.config, {}).get(dom)
+    roof = {"bound": "alu", "kernel": f"cbp_{dom}_kernel", "achieved": kernels[dom]["tflops"],
+            "peak": peak_tflops, "unit": "TFLOP/s", "frac": kernels[dom]["frac"],
+            "traffic": traffic,
+            "peak_basis": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 flop x "
+                          f"{sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+            "work": f"{nw} nonzero weights x {FLOPS_PER_WEIGHT} flop per launch",
+            "hbm_gbs_algorithmic": 4 * (n * n + nv * ns) / (ms_to_s(statistics.mean(step_ms))) / 1e9}
+
+    # ---- end to end through the C ABI with host buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        h_img = torch.from_numpy(W.shepp_logan(n)).pin_memory()
+        h_sino = torch.empty((nv, ns), dtype=torch.float32).pin_memory()
+        h_out = torch.empty((n, n), dtype=torch.float32).pin_memory()
+        d_out = torch.empty((n, n), dtype=torch.float32, device=dev)
+        ke = max(3, min(args.steps, 50))
+
+        def e2e_step():
+            cbp.forward(g, h_img, h_sino, view_begin=v0, view_count=nv)  # H2D img, D2H sino
+            if world > 1:
+                cbp.back(g, h_sino, d_out, view_begin=v0)  # H2D sino
+                torch.cuda.synchronize()
+                dist.all_reduce(d_out)
+                h_out.copy_(d_out)  # D2H image
+            else:
+                cbp.back(g, h_sino, h_out, view_begin=v0)  # H2D sino, D2H image
+
+        for _ in range(3):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(ke):
+            e2e_step()
+        e1.record()
+        e1.synchronize()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": ke / (float(et.item()) * 1e-3), "unit": "pairs/s",
+               "h2d_bytes_per_step": 4 * (n * n + nv * ns),
+               "d2h_bytes_per_step": 4 * (nv * ns + n * n),
+               "path": "cbp_forward/cbp_back with pinned host buffers (library staging)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "n": n, "n_views": g["n_views"],
+                       "n_det": ns, "pixel_mm": g["pixel"], "det_pitch_mm": g["det_pitch"],
+                       "sid_mm": g["sid"], "sdd_mm": g["sdd"], "batch": 1,
+                       "parallelism": f"views/{world}" if world > 1 else "single",
+                       "l2": "flushed between steps (256 MiB write, outside the timed events)"},
+            "roofline": roof,
+            "kernels": kernels,
+            "allreduce_ms": statistics.mean(ar_ms) if world > 1 else 0.0,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ms_to_s(ms: float) -> float:
+    return ms * 1e-3
+
+
+if __name__ == "__main__":
+    main()

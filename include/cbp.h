@@ -1,0 +1,113 @@
+/*
+ * cbp.h -- C ABI of the B200-native CNSF fan-beam projector
+ * (Zhang & Entezari, "A Convolutional Forward and Back-Projection Model for
+ * Fan-Beam Geometry", arXiv 1907.10526).
+ *
+ * Citations: "P:n" is line n of the paper text, "S:n" line n of
+ * SPEC.md, "ledger #k" reading k of DESIGN.md section 3.
+ *
+ * The library computes, matrix-free and on the fly,
+ *   forward   y = A c       (Eq. 6)
+ *   back      c = A^T y     (the exact adjoint with the same weights)
+ * where A[(v, j), k] = W(v, j, k) = h^2 M_{zeta1, zeta2, tau'}(s'), the
+ * blurred fan-beam footprint of Eq. 14 of the indicator pixel k
+ * on detector bin j of view v: zeta1, zeta2 from Eq. 12, the
+ * effective blur tau' from Eq. 13 on the plane through the pixel centre
+ * (ledger #1), s' = R_{v(s_j)^perp}(p - k) (Eq. 11).
+ *
+ * Conventions:
+ *   views   theta_v = 2 pi v / n_views, counter-clockwise from +x (ledger #9)
+ *   source  p = sid * (cos theta, sin theta); detector line through
+ *           -(sdd - sid) * (cos theta, sin theta) along e = (-sin, cos) (ledger #6)
+ *   bins    s_j = (j - (n_det - 1)/2) * det_pitch (ledger #10)
+ *   pixels  k(row, col) = ((col - (n-1)/2) h, ((n-1)/2 - row) h) (ledger #13)
+ *   blur    unit-mass average over [s_j - tau/2, s_j + tau/2] (ledger #3)
+ *
+ * Data layout (FP32, contiguous, row-major):
+ *   image  [batch][n][n]
+ *   sino   [batch][view_count][n_det]   (views view_begin .. view_begin+view_count-1)
+ *
+ * Memory: every data pointer may be device memory (cudaMalloc / torch CUDA
+ * tensors) or host memory (pageable or pinned).  Device pointers must be on
+ * the current device.  Host pointers are staged through an internal device
+ * workspace with cudaMemcpyAsync on `stream`, and the call then synchronises
+ * `stream` before returning so the host result is ready.  The caller owns
+ * every buffer; the library never retains a data pointer.  Per-geometry
+ * tables (a few KB) are cached per device, guarded by a mutex.
+ *
+ * Streams: `stream` is a cudaStream_t (0 = legacy default stream).  With
+ * device pointers all work is stream-ordered and asynchronous: execution
+ * errors surface at the caller's next synchronisation, not in the return
+ * value.  No call except cbp_adjoint_check synchronises the device.
+ *
+ * Errors: functions return CBP_OK (0) or a negative code; arguments are
+ * validated before any CUDA call ("geometry violation -> error before
+ * computation").
+ */
+#ifndef CBP_H
+#define CBP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CBP_OK      0
+#define CBP_EINVAL -1  /* invalid geometry or argument (see cbp_validate)         */
+#define CBP_ECUDA  -2  /* CUDA error at launch / copy / allocation of workspace   */
+#define CBP_ENOMEM -3  /* host allocation failure                                 */
+
+/* Scanner and grid (P:96-106 geometry; P:157-159 image; P:124 and P:416
+ * detector).  All lengths in mm.                                            */
+typedef struct cbp_geometry {
+    int32_t n;          /* image is n x n pixels, n >= 1                               */
+    double  pixel;      /* pixel side h > 0                                            */
+    int32_t n_views;    /* views over [0, 2 pi): theta_v = 2 pi v / n_views, >= 1      */
+    int32_t n_det;      /* detector bins N_s >= 1                                      */
+    double  det_pitch;  /* bin spacing Delta_s > 0                                     */
+    double  det_width;  /* bin width tau > 0 (the detector blur, Eq. 2)                */
+    double  sid;        /* D_po, source to rotation centre; n h / sqrt(2) < sid        */
+    double  sdd;        /* D_ps, source to detector; sdd >= sid (D_so = sdd - sid)     */
+} cbp_geometry_t;
+
+/* Validate a geometry (no CUDA call).  CBP_EINVAL if n < 1, pixel <= 0,
+ * n_views < 1, n_det < 1, det_pitch <= 0, det_width <= 0, sid <= 0,
+ * sdd < sid, det_width >= 2 sdd, any value non-finite, or the field of view's
+ * circumscribed circle n h / sqrt(2) is not strictly inside the source orbit
+ * (every pixel must lie strictly in front of the source). */
+int cbp_validate(const cbp_geometry_t* g);
+
+/* Forward projection y = A c (Eq. 6) for views [view_begin,
+ * view_begin + view_count) of `batch` images.  Overwrites sino.
+ * CBP_EINVAL: invalid geometry, null pointer, batch < 1, view range outside
+ * [0, n_views), view_count < 1, device pointer not 4-byte aligned. */
+int cbp_forward(const cbp_geometry_t* g, const float* image, float* sino, int32_t batch,
+                int32_t view_begin, int32_t view_count, void* stream);
+
+/* Back-projection c = A^T y over views [view_begin, view_begin + view_count)
+ * (the partial adjoint when the range is a shard of the views).  Overwrites
+ * image, or adds to it when accumulate != 0.  Errors as cbp_forward. */
+int cbp_back(const cbp_geometry_t* g, const float* sino, float* image, int32_t batch,
+             int32_t view_begin, int32_t view_count, int32_t accumulate, void* stream);
+
+/* Adjoint identity check on the current device (synchronous): draws seeded
+ * c, y ~ U[0,1) (splitmix64), runs cbp_forward and cbp_back over all views,
+ * and returns |<Ac,y> - <c,A^T y>| / |<Ac,y>| with FP64 inner products in
+ * *rel_defect.  CBP_EINVAL for an invalid geometry or null rel_defect. */
+int cbp_adjoint_check(const cbp_geometry_t* g, uint64_t seed, double* rel_defect);
+
+/* Static description of an error code (never NULL). */
+const char* cbp_strerror(int code);
+
+/* ABI version (major * 10000 + minor * 100 + patch). */
+int cbp_version(void);
+
+/* Number of CUDA kernels this library has launched in this process (all
+ * devices, all threads); instrumentation for the benchmark's launch count. */
+uint64_t cbp_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CBP_H */

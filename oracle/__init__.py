@@ -89,6 +89,9 @@ def lib():
                 "orc_set_candidate_margin_scale": (None, [ctypes.c_double]),
                 "orc_count_weights": (ctypes.c_int64, [G, ctypes.c_int32, ctypes.c_int32,
                                                        ctypes.c_int32]),
+                "orc_count_weights_per_view": (ctypes.c_int, [G, ctypes.c_int32, ctypes.c_int32,
+                                                              ctypes.POINTER(ctypes.c_int64),
+                                                              ctypes.c_int32]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -226,3 +229,15 @@ def count_weights(geom, view_begin=0, view_count=None, threads=0) -> int:
     g = _g(geom)
     nv = g.n_views - view_begin if view_count is None else view_count
     return int(lib().orc_count_weights(ctypes.byref(g), view_begin, nv, threads))
+
+
+def count_weights_per_view(geom, view_begin=0, view_count=None, threads=0) -> np.ndarray:
+    g = _g(geom)
+    nv = g.n_views - view_begin if view_count is None else view_count
+    out = np.zeros(nv, dtype=np.int64)
+    rc = lib().orc_count_weights_per_view(ctypes.byref(g), view_begin, nv,
+                                          out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                          threads)
+    if rc != 0:
+        raise ValueError("orc_count_weights_per_view: invalid arguments")
+    return out

@@ -467,19 +467,20 @@ int orc_back_pixels(const orc_geometry* g, const double* sino, int32_t batch, in
     return 0;
 }
 
-int64_t orc_count_weights(const orc_geometry* g, int32_t v0, int32_t nv, int32_t threads)
+int orc_count_weights_per_view(const orc_geometry* g, int32_t v0, int32_t nv, int64_t* out,
+                               int32_t threads)
 {
-    if (!geometry_ok(g) || v0 < 0 || nv < 0 || v0 + nv > g->n_views) return -1;
+    if (!geometry_ok(g) || !out || v0 < 0 || nv < 0 || v0 + nv > g->n_views) return -1;
     const int nt = nthreads_of(threads);
     const int32_t n = g->n;
-    int64_t total = 0;
     int32_t vl;
-#pragma omp parallel for num_threads(nt) schedule(dynamic, 1) reduction(+ : total)
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1)
     for (vl = 0; vl < nv; ++vl) {
         view_t V;
         V.v = (double*)malloc(sizeof(double) * 2 * g->n_det);
         V.r = (double*)malloc(sizeof(double) * 2 * g->n_det);
         view_build(g, v0 + vl, &V);
+        int64_t cnt = 0;
         for (int32_t row = 0; row < n; ++row)
             for (int32_t col = 0; col < n; ++col) {
                 double k[2];
@@ -489,10 +490,23 @@ int64_t orc_count_weights(const orc_geometry* g, int32_t v0, int32_t nv, int32_t
                 for (int32_t j = jlo; j <= jhi; ++j)
                     if (weight_f(g, V.u, V.e, V.p, orc_bin_center(g, j), V.v + 2 * j,
                                  V.r + 2 * j, k) != 0.0)
-                        ++total;
+                        ++cnt;
             }
+        out[vl] = cnt;
         free(V.v);
         free(V.r);
     }
+    return 0;
+}
+
+int64_t orc_count_weights(const orc_geometry* g, int32_t v0, int32_t nv, int32_t threads)
+{
+    if (!geometry_ok(g) || v0 < 0 || nv < 0 || v0 + nv > g->n_views) return -1;
+    int64_t* per = (int64_t*)calloc((size_t)(nv > 0 ? nv : 1), sizeof(int64_t));
+    int64_t total = 0;
+    if (orc_count_weights_per_view(g, v0, nv, per, threads) != 0) total = -1;
+    else
+        for (int32_t i = 0; i < nv; ++i) total += per[i];
+    free(per);
     return total;
 }

@@ -75,6 +75,8 @@ int orc_back_pixels(const orc_geometry* g, const double* sino, int32_t batch,
 void orc_set_candidate_margin_scale(double s);
 /* number of nonzero weights (support test of Eq. 14) over views [v0, v0+nv) */
 int64_t orc_count_weights(const orc_geometry* g, int32_t v0, int32_t nv, int32_t threads);
+int orc_count_weights_per_view(const orc_geometry* g, int32_t v0, int32_t nv, int64_t* out,
+                               int32_t threads);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,216 @@
+"""B200-native CNSF fan-beam projector (arXiv 1907.10526): thin Python binding
+of the C ABI in ``include/cbp.h`` (``libcbp.so``, built in-tree for sm_100a).
+
+Argument marshalling only: every step of forward / back-projection runs in
+the library's CUDA kernels.  There is no CPU fallback: if ``libcbp.so`` is
+missing or fails to load, every call raises.
+
+Tensors: ``torch.float32``, contiguous; CUDA tensors on the current device
+run asynchronously on ``torch.cuda.current_stream()`` (or the given stream);
+CPU tensors / numpy arrays go through the library's host-staging path
+(synchronous).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, asdict
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcbp.so")
+
+CBP_OK, CBP_EINVAL, CBP_ECUDA, CBP_ENOMEM = 0, -1, -2, -3
+
+# names declared in include/cbp.h
+ABI_FUNCTIONS = ("cbp_validate", "cbp_forward", "cbp_back", "cbp_adjoint_check",
+                 "cbp_strerror", "cbp_version", "cbp_launch_count")
+
+
+class CbpError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        super().__init__(f"{where}: {strerror(code)} ({code})")
+        self.code = code
+
+
+class cbp_geometry_t(ctypes.Structure):
+    """mirror of ``cbp_geometry_t`` (include/cbp.h)."""
+    _fields_ = [("n", ctypes.c_int32), ("pixel", ctypes.c_double),
+                ("n_views", ctypes.c_int32), ("n_det", ctypes.c_int32),
+                ("det_pitch", ctypes.c_double), ("det_width", ctypes.c_double),
+                ("sid", ctypes.c_double), ("sdd", ctypes.c_double)]
+
+
+@dataclass(frozen=True)
+class Geometry:
+    """Scanner and grid, mm: see include/cbp.h."""
+    n: int
+    pixel: float
+    n_views: int
+    n_det: int
+    det_pitch: float
+    det_width: float
+    sid: float
+    sdd: float
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "Geometry":
+        return cls(**{k: d[k] for k in cls.__dataclass_fields__})
+
+    def c_struct(self) -> cbp_geometry_t:
+        return cbp_geometry_t(int(self.n), float(self.pixel), int(self.n_views), int(self.n_det),
+                              float(self.det_pitch), float(self.det_width), float(self.sid),
+                              float(self.sdd))
+
+    def as_dict(self) -> dict:
+        return asdict(self)
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libcbp.so (raises if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing; run `python -m paper_1907_10526_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        G = ctypes.POINTER(cbp_geometry_t)
+        vp, fp = ctypes.c_void_p, ctypes.c_void_p
+        i32 = ctypes.c_int32
+        L.cbp_validate.argtypes = [G]
+        L.cbp_validate.restype = ctypes.c_int
+        L.cbp_forward.argtypes = [G, fp, fp, i32, i32, i32, vp]
+        L.cbp_forward.restype = ctypes.c_int
+        L.cbp_back.argtypes = [G, fp, fp, i32, i32, i32, i32, vp]
+        L.cbp_back.restype = ctypes.c_int
+        L.cbp_adjoint_check.argtypes = [G, ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]
+        L.cbp_adjoint_check.restype = ctypes.c_int
+        L.cbp_strerror.argtypes = [ctypes.c_int]
+        L.cbp_strerror.restype = ctypes.c_char_p
+        L.cbp_version.argtypes = []
+        L.cbp_version.restype = ctypes.c_int
+        L.cbp_launch_count.argtypes = []
+        L.cbp_launch_count.restype = ctypes.c_uint64
+        _lib = L
+    return _lib
+
+
+def _geom(geom) -> cbp_geometry_t:
+    if isinstance(geom, cbp_geometry_t):
+        return geom
+    if isinstance(geom, Geometry):
+        return geom.c_struct()
+    return Geometry.from_dict(geom).c_struct()
+
+
+def _checked(geom) -> cbp_geometry_t:
+    g = _geom(geom)
+    rc = lib().cbp_validate(ctypes.byref(g))
+    if rc != CBP_OK:
+        raise CbpError(rc, "cbp_validate")
+    return g
+
+
+def strerror(code: int) -> str:
+    return lib().cbp_strerror(code).decode()
+
+
+def version() -> int:
+    return lib().cbp_version()
+
+
+def launch_count() -> int:
+    return int(lib().cbp_launch_count())
+
+
+def validate(geom) -> int:
+    return lib().cbp_validate(ctypes.byref(_geom(geom)))
+
+
+def _ptr_and_stream(t, stream):
+    """(data pointer, stream handle) of a torch tensor or numpy array."""
+    import numpy as np
+    if isinstance(t, np.ndarray):
+        if t.dtype != np.float32 or not t.flags["C_CONTIGUOUS"]:
+            raise ValueError("expected a C-contiguous float32 array")
+        return t.ctypes.data, 0
+    import torch
+    if t.dtype != torch.float32 or not t.is_contiguous():
+        raise ValueError("expected a contiguous float32 tensor")
+    if t.is_cuda:
+        if stream is None:
+            stream = torch.cuda.current_stream(t.device)
+        return t.data_ptr(), int(stream.cuda_stream if hasattr(stream, "cuda_stream") else stream)
+    return t.data_ptr(), int(stream or 0)
+
+
+def forward(geom, image, sino=None, view_begin: int = 0, view_count: int | None = None,
+            stream=None):
+    """y = A c (Eq. 6) for views [view_begin, view_begin + view_count).
+
+    image: [n, n] or [B, n, n] float32 (CUDA tensor, CPU tensor or numpy).
+    Returns sino [B?, view_count, n_det] (allocated like `image` if not given).
+    """
+    g = _checked(geom)
+    nv = g.n_views - view_begin if view_count is None else view_count
+    squeeze = image.ndim == 2
+    batch = 1 if squeeze else image.shape[0]
+    if tuple(image.shape[-2:]) != (g.n, g.n):
+        raise ValueError(f"image shape {tuple(image.shape)} does not match n={g.n}")
+    shape = (nv, g.n_det) if squeeze else (batch, nv, g.n_det)
+    if sino is None:
+        sino = _empty_like(image, shape)
+    elif tuple(sino.shape) != shape:
+        raise ValueError(f"sino shape {tuple(sino.shape)} != {shape}")
+    pi, st = _ptr_and_stream(image, stream)
+    ps, _ = _ptr_and_stream(sino, stream)
+    rc = lib().cbp_forward(ctypes.byref(g), pi, ps, batch, view_begin, nv, st)
+    if rc != CBP_OK:
+        raise CbpError(rc, "cbp_forward")
+    return sino
+
+
+def back(geom, sino, image=None, view_begin: int = 0, accumulate: bool = False, stream=None):
+    """c = A^T y over views [view_begin, view_begin + sino.shape[-2]).
+
+    sino: [V, n_det] or [B, V, n_det] float32.  Returns image [B?, n, n];
+    with accumulate=True adds into the given image.
+    """
+    g = _checked(geom)
+    squeeze = sino.ndim == 2
+    batch = 1 if squeeze else sino.shape[0]
+    nv = sino.shape[-2]
+    if sino.shape[-1] != g.n_det:
+        raise ValueError(f"sino shape {tuple(sino.shape)} does not match n_det={g.n_det}")
+    shape = (g.n, g.n) if squeeze else (batch, g.n, g.n)
+    if image is None:
+        if accumulate:
+            raise ValueError("accumulate=True needs an image to add into")
+        image = _empty_like(sino, shape)
+    elif tuple(image.shape) != shape:
+        raise ValueError(f"image shape {tuple(image.shape)} != {shape}")
+    ps, st = _ptr_and_stream(sino, stream)
+    pi, _ = _ptr_and_stream(image, stream)
+    rc = lib().cbp_back(ctypes.byref(g), ps, pi, batch, view_begin, nv, 1 if accumulate else 0, st)
+    if rc != CBP_OK:
+        raise CbpError(rc, "cbp_back")
+    return image
+
+
+def adjoint_check(geom, seed: int = 0) -> float:
+    """relative adjoint defect |<Ac,y> - <c,A^T y>| / |<Ac,y>| on the current device."""
+    out = ctypes.c_double()
+    rc = lib().cbp_adjoint_check(ctypes.byref(_geom(geom)), ctypes.c_uint64(seed),
+                                 ctypes.byref(out))
+    if rc != CBP_OK:
+        raise CbpError(rc, "cbp_adjoint_check")
+    return out.value
+
+
+def _empty_like(ref, shape):
+    import numpy as np
+    if isinstance(ref, np.ndarray):
+        return np.empty(shape, dtype=np.float32)
+    import torch
+    return torch.empty(shape, dtype=torch.float32, device=ref.device)

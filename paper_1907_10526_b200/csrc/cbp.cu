@@ -1,0 +1,331 @@
+// cbp.cu -- the C ABI of include/cbp.h: argument validation, per-geometry
+// table cache (row a1), host-buffer staging, kernel launches.
+//
+// Built with: nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3
+//             -Xcompiler -fPIC -shared  (see paper_1907_10526_b200/build.py)
+#include "cbp.h"
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "cbp_bp.cuh"
+#include "cbp_common.cuh"
+#include "cbp_fp.cuh"
+#include "cbp_tables.cuh"
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
+
+cbp::GeomDev to_dev(const cbp_geometry_t& g)
+{
+    cbp::GeomDev d;
+    d.n = g.n;
+    d.n_views = g.n_views;
+    d.n_det = g.n_det;
+    d.h = g.pixel;
+    d.pitch = g.det_pitch;
+    d.tau = g.det_width;
+    d.sid = g.sid;
+    d.sdd = g.sdd;
+    d.c0 = 0.5 * (double)(g.n - 1);
+    d.cs = 0.5 * (double)(g.n_det - 1);
+    return d;
+}
+
+// ---- per-(geometry, device) tables --------------------------------------
+struct TableKey {
+    int device;
+    int32_t n_views, n_det;
+    double pitch, tau, sdd;
+    bool operator<(const TableKey& o) const
+    {
+        return std::memcmp(this, &o, sizeof(TableKey)) < 0;
+    }
+};
+
+struct TableSet {
+    double2* view_cs = nullptr;
+    double2* bin_d = nullptr;
+    float4* bin_f = nullptr;
+};
+
+std::mutex g_table_mu;
+std::map<TableKey, TableSet> g_tables;
+
+int get_tables(const cbp_geometry_t& g, cudaStream_t stream, cbp::Tables& out)
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return CBP_ECUDA;
+    TableKey key;
+    std::memset(&key, 0, sizeof(key));
+    key.device = dev;
+    key.n_views = g.n_views;
+    key.n_det = g.n_det;
+    key.pitch = g.det_pitch;
+    key.tau = g.det_width;
+    key.sdd = g.sdd;
+    std::lock_guard<std::mutex> lock(g_table_mu);
+    auto it = g_tables.find(key);
+    if (it == g_tables.end()) {
+        TableSet ts;
+        if (cudaMalloc(&ts.view_cs, sizeof(double2) * g.n_views) != cudaSuccess ||
+            cudaMalloc(&ts.bin_d, sizeof(double2) * g.n_det) != cudaSuccess ||
+            cudaMalloc(&ts.bin_f, sizeof(float4) * g.n_det) != cudaSuccess) {
+            cudaFree(ts.view_cs);
+            cudaFree(ts.bin_d);
+            cudaFree(ts.bin_f);
+            cudaGetLastError();
+            return CBP_ECUDA;
+        }
+        const int m = g.n_views > g.n_det ? g.n_views : g.n_det;
+        cbp::cbp_tables_kernel<<<(m + 127) / 128, 128, 0, stream>>>(to_dev(g), ts.view_cs,
+                                                                    ts.bin_d, ts.bin_f);
+        ++g_launches;
+        if (cudaGetLastError() != cudaSuccess) return CBP_ECUDA;
+        // tables are shared across streams: finish building before publishing
+        if (cudaStreamSynchronize(stream) != cudaSuccess) return CBP_ECUDA;
+        it = g_tables.emplace(key, ts).first;
+    }
+    out.view_cs = it->second.view_cs;
+    out.bin_d = it->second.bin_d;
+    out.bin_f = it->second.bin_f;
+    return CBP_OK;
+}
+
+// ---- host-buffer staging workspace --------------------------------------
+struct Workspace {
+    void* buf[2] = {nullptr, nullptr};
+    size_t cap[2] = {0, 0};
+};
+std::mutex g_ws_mu;
+std::map<int, Workspace> g_ws;
+
+int ws_get(Workspace& w, int slot, size_t bytes, void** p)
+{
+    if (w.cap[slot] < bytes) {
+        cudaFree(w.buf[slot]);
+        w.buf[slot] = nullptr;
+        w.cap[slot] = 0;
+        if (cudaMalloc(&w.buf[slot], bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return CBP_ECUDA;
+        }
+        w.cap[slot] = bytes;
+    }
+    *p = w.buf[slot];
+    return CBP_OK;
+}
+
+// 1 = device (or managed) memory on the current device, 0 = host, -1 = error
+int pointer_kind(const void* p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;  // unknown to CUDA: plain host memory
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        return a.device == dev ? 1 : -1;
+    }
+    return 0;
+}
+
+int check_common(const cbp_geometry_t* g, const void* a, const void* b, int32_t batch,
+                 int32_t view_begin, int32_t view_count)
+{
+    if (cbp_validate(g) != CBP_OK) return CBP_EINVAL;
+    if (!a || !b || batch < 1 || view_count < 1 || view_begin < 0 ||
+        (int64_t)view_begin + view_count > g->n_views)
+        return CBP_EINVAL;
+    if (((uintptr_t)a & 3) || ((uintptr_t)b & 3)) return CBP_EINVAL;
+    return CBP_OK;
+}
+
+int launch_fp(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
+              int32_t batch, int32_t v0, int32_t nv, cudaStream_t stream)
+{
+    cbp::FPParams P;
+    P.g = to_dev(g);
+    P.t = t;
+    P.image = img;
+    P.sino = sino;
+    P.view_begin = v0;
+    P.view_count = nv;
+    dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, nv, batch);
+    cbp::cbp_fp_kernel<<<grid, cbp::FP_BLOCK, 0, stream>>>(P);
+    ++g_launches;
+    return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+}
+
+int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
+              int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream)
+{
+    cbp::BPParams P;
+    P.g = to_dev(g);
+    P.t = t;
+    P.sino = sino;
+    P.image = img;
+    P.view_begin = v0;
+    P.view_count = nv;
+    P.accumulate = accumulate ? 1 : 0;
+    const int tiles = (g.n + cbp::BP_TILE - 1) / cbp::BP_TILE;
+    dim3 grid(tiles, tiles, batch);
+    cbp::cbp_bp_kernel<<<grid, cbp::BP_THREADS, 0, stream>>>(P);
+    ++g_launches;
+    return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cbp_validate(const cbp_geometry_t* g)
+{
+    if (!g) return CBP_EINVAL;
+    if (g->n < 1 || g->n_views < 1 || g->n_det < 1) return CBP_EINVAL;
+    if (!finite_pos(g->pixel) || !finite_pos(g->det_pitch) || !finite_pos(g->det_width) ||
+        !finite_pos(g->sid) || !finite_pos(g->sdd))
+        return CBP_EINVAL;
+    if (g->sdd < g->sid) return CBP_EINVAL;
+    if (g->det_width >= 2.0 * g->sdd) return CBP_EINVAL;
+    const double radius = 0.5 * (double)g->n * g->pixel * std::sqrt(2.0);
+    if (!(radius < g->sid)) return CBP_EINVAL;
+    return CBP_OK;
+}
+
+int cbp_forward(const cbp_geometry_t* g, const float* image, float* sino, int32_t batch,
+                int32_t view_begin, int32_t view_count, void* stream_)
+{
+    int rc = check_common(g, image, sino, batch, view_begin, view_count);
+    if (rc != CBP_OK) return rc;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    cbp::Tables t;
+    if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    const int ki = pointer_kind(image), ks = pointer_kind(sino);
+    if (ki < 0 || ks < 0) return CBP_EINVAL;
+    if (ki == 1 && ks == 1) return launch_fp(*g, t, image, sino, batch, view_begin, view_count, stream);
+
+    // host buffers: stage through the device workspace, then synchronise
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    Workspace& w = g_ws[dev];
+    const size_t ib = sizeof(float) * (size_t)batch * g->n * g->n;
+    const size_t sb = sizeof(float) * (size_t)batch * view_count * g->n_det;
+    void *di = (void*)image, *ds = (void*)sino;
+    if (ki == 0 && (rc = ws_get(w, 0, ib, &di)) != CBP_OK) return rc;
+    if (ks == 0 && (rc = ws_get(w, 1, sb, &ds)) != CBP_OK) return rc;
+    if (ki == 0 && cudaMemcpyAsync(di, image, ib, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+        return CBP_ECUDA;
+    if ((rc = launch_fp(*g, t, (const float*)di, (float*)ds, batch, view_begin, view_count,
+                        stream)) != CBP_OK)
+        return rc;
+    if (ks == 0 && cudaMemcpyAsync(sino, ds, sb, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+        return CBP_ECUDA;
+    return cudaStreamSynchronize(stream) == cudaSuccess ? CBP_OK : CBP_ECUDA;
+}
+
+int cbp_back(const cbp_geometry_t* g, const float* sino, float* image, int32_t batch,
+             int32_t view_begin, int32_t view_count, int32_t accumulate, void* stream_)
+{
+    int rc = check_common(g, sino, image, batch, view_begin, view_count);
+    if (rc != CBP_OK) return rc;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    cbp::Tables t;
+    if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    const int ks = pointer_kind(sino), ki = pointer_kind(image);
+    if (ki < 0 || ks < 0) return CBP_EINVAL;
+    if (ki == 1 && ks == 1)
+        return launch_bp(*g, t, sino, image, batch, view_begin, view_count, accumulate, stream);
+
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_ws_mu);
+    Workspace& w = g_ws[dev];
+    const size_t ib = sizeof(float) * (size_t)batch * g->n * g->n;
+    const size_t sb = sizeof(float) * (size_t)batch * view_count * g->n_det;
+    void *di = (void*)image, *ds = (void*)sino;
+    if (ks == 0 && (rc = ws_get(w, 1, sb, &ds)) != CBP_OK) return rc;
+    if (ki == 0 && (rc = ws_get(w, 0, ib, &di)) != CBP_OK) return rc;
+    if (ks == 0 && cudaMemcpyAsync(ds, sino, sb, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+        return CBP_ECUDA;
+    if (ki == 0 && accumulate &&
+        cudaMemcpyAsync(di, image, ib, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+        return CBP_ECUDA;
+    if ((rc = launch_bp(*g, t, (const float*)ds, (float*)di, batch, view_begin, view_count,
+                        accumulate, stream)) != CBP_OK)
+        return rc;
+    if (ki == 0 && cudaMemcpyAsync(image, di, ib, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+        return CBP_ECUDA;
+    return cudaStreamSynchronize(stream) == cudaSuccess ? CBP_OK : CBP_ECUDA;
+}
+
+static uint64_t splitmix64(uint64_t& x)
+{
+    uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+int cbp_adjoint_check(const cbp_geometry_t* g, uint64_t seed, double* rel_defect)
+{
+    if (cbp_validate(g) != CBP_OK || !rel_defect) return CBP_EINVAL;
+    const size_t ni = (size_t)g->n * g->n, ns = (size_t)g->n_views * g->n_det;
+    std::vector<float> c(ni), y(ns), Ac(ns), Aty(ni);
+    uint64_t st = seed;
+    for (auto& x : c) x = (float)((splitmix64(st) >> 40) * 0x1p-24);
+    for (auto& x : y) x = (float)((splitmix64(st) >> 40) * 0x1p-24);
+    float *dc = nullptr, *dy = nullptr, *dAc = nullptr, *dAty = nullptr;
+    int rc = CBP_ECUDA;
+    if (cudaMalloc(&dc, ni * 4) == cudaSuccess && cudaMalloc(&dy, ns * 4) == cudaSuccess &&
+        cudaMalloc(&dAc, ns * 4) == cudaSuccess && cudaMalloc(&dAty, ni * 4) == cudaSuccess &&
+        cudaMemcpy(dc, c.data(), ni * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+        cudaMemcpy(dy, y.data(), ns * 4, cudaMemcpyHostToDevice) == cudaSuccess) {
+        rc = cbp_forward(g, dc, dAc, 1, 0, g->n_views, nullptr);
+        if (rc == CBP_OK) rc = cbp_back(g, dy, dAty, 1, 0, g->n_views, 0, nullptr);
+        if (rc == CBP_OK) {
+            if (cudaMemcpy(Ac.data(), dAc, ns * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+                cudaMemcpy(Aty.data(), dAty, ni * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+                rc = CBP_ECUDA;
+        }
+    }
+    cudaFree(dc);
+    cudaFree(dy);
+    cudaFree(dAc);
+    cudaFree(dAty);
+    cudaGetLastError();
+    if (rc != CBP_OK) return rc;
+    double lhs = 0.0, rhs = 0.0;
+    for (size_t i = 0; i < ns; ++i) lhs += (double)Ac[i] * (double)y[i];
+    for (size_t i = 0; i < ni; ++i) rhs += (double)c[i] * (double)Aty[i];
+    *rel_defect = lhs != 0.0 ? std::fabs(lhs - rhs) / std::fabs(lhs) : std::fabs(rhs);
+    return CBP_OK;
+}
+
+const char* cbp_strerror(int code)
+{
+    switch (code) {
+        case CBP_OK: return "ok";
+        case CBP_EINVAL: return "invalid geometry or argument";
+        case CBP_ECUDA: return "CUDA error";
+        case CBP_ENOMEM: return "out of host memory";
+        default: return "unknown error";
+    }
+}
+
+int cbp_version(void) { return 100; }
+
+uint64_t cbp_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through the C ABI) against the FP64 oracle on
+identical seeded inputs.
+
+Bar (BASELINE.json north_star; DESIGN.md ledger #18):
+  relL2  = |y_gpu - y_ref|_2 / |y_ref|_2        <= 1e-5
+  maxrel = max|y_gpu - y_ref| / max|y_ref|       <= 1e-4
+  adjoint defect |<Ac,y> - <c,A^T y>| / |<Ac,y>| <= 1e-5
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1907_10526_b200 as cbp
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+REL_L2 = 1e-5
+MAX_REL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _metrics(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    d = got - ref
+    return (float(np.linalg.norm(d) / max(np.linalg.norm(ref), 1e-300)),
+            float(np.abs(d).max() / max(np.abs(ref).max(), 1e-300)))
+
+
+def _assert_parity(got, ref, what=""):
+    rl2, mr = _metrics(got, ref)
+    assert rl2 <= REL_L2 and mr <= MAX_REL, f"{what}: relL2={rl2:.3e} maxrel={mr:.3e}"
+
+
+def _fp(torch, g, img, view_begin=0, view_count=None):
+    t = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).cuda()
+    out = cbp.forward(g, t, view_begin=view_begin, view_count=view_count)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _bp(torch, g, sino, view_begin=0):
+    t = torch.from_numpy(np.ascontiguousarray(sino, dtype=np.float32)).cuda()
+    out = cbp.back(g, t, view_begin=view_begin)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+# ---------------------------------------------------------------- config 1
+CFG1_IMAGES = {
+    "shepp": lambda n: W.shepp_logan(n),
+    "rand1": lambda n: W.random_image(n, 1),
+    "rand2": lambda n: W.random_image(n, 2),
+    "rand3": lambda n: W.random_image(n, 3),
+    "ones": lambda n: W.ones(n),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CFG1_IMAGES))
+def test_forward_config1(torch_cuda, name):
+    g = W.geometry("1")
+    img = CFG1_IMAGES[name](g["n"])
+    _assert_parity(_fp(torch_cuda, g, img), O.forward(g, img), f"FP cfg1 {name}")
+
+
+@pytest.mark.parametrize("seed", [101, 102, 103])
+def test_back_config1(torch_cuda, seed):
+    g = W.geometry("1")
+    y = W.random_sino(g["n_views"], g["n_det"], seed)
+    _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), f"BP cfg1 seed {seed}")
+
+
+def test_back_of_forward_config1(torch_cuda):
+    g = W.geometry("1")
+    y = O.forward(g, W.shepp_logan(g["n"])).astype(np.float32)
+    _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), "BP(FP(shepp)) cfg1")
+
+
+def test_adjoint_config1(torch_cuda):
+    g = W.geometry("1")
+    assert cbp.adjoint_check(g, seed=1) <= 1e-5
+    c = W.random_image(g["n"], 1)
+    y = W.random_sino(g["n_views"], g["n_det"], 101)
+    lhs = float(np.sum(_fp(torch_cuda, g, c).astype(np.float64) * y))
+    rhs = float(np.sum(c.astype(np.float64) * _bp(torch_cuda, g, y)))
+    assert abs(lhs - rhs) / abs(lhs) <= 1e-5
+
+
+# ---------------------------------------------- full sizes (sampled oracle)
+@pytest.mark.parametrize("cfg,stride", [("2", 45), ("3", 180)])
+def test_forward_full_size_sampled_views(torch_cuda, cfg, stride):
+    g = W.geometry(cfg)
+    img = W.shepp_logan(g["n"])
+    y = _fp(torch_cuda, g, img)  # all views, the launch bench.py times
+    for v in range(0, g["n_views"], stride):
+        _assert_parity(y[v], O.forward(g, img, view_begin=v, view_count=1)[0], f"FP cfg{cfg} v{v}")
+    img_r = W.random_image(g["n"], 2)
+    y = _fp(torch_cuda, g, img_r)
+    for v in range(7, g["n_views"], stride * 2):
+        _assert_parity(y[v], O.forward(g, img_r, view_begin=v, view_count=1)[0],
+                       f"FP cfg{cfg} rand v{v}")
+
+
+@pytest.mark.parametrize("cfg,npix", [("2", 96), ("3", 24)])
+def test_back_full_size_sampled_pixels(torch_cuda, cfg, npix):
+    g = W.geometry(cfg)
+    y = W.random_sino(g["n_views"], g["n_det"], 103)
+    c = _bp(torch_cuda, g, y)
+    rng = np.random.default_rng(11)
+    n = g["n"]
+    rows = np.concatenate([[0, n - 1, n // 2, 0], rng.integers(0, n, npix)])
+    cols = np.concatenate([[0, n - 1, n // 2, n - 1], rng.integers(0, n, npix)])
+    ref = O.back_pixels(g, y, rows, cols)
+    _assert_parity(c[rows, cols], ref, f"BP cfg{cfg} sampled")
+    # invariant at any size: BP is nonnegative for a nonnegative sinogram
+    assert c.min() >= 0.0
+
+
+def test_adjoint_config2(torch_cuda):
+    assert cbp.adjoint_check(W.geometry("2"), seed=7) <= 1e-5
+
+
+# ------------------------------------------------------------- edge cases
+EDGE = {
+    # single pixel and the paper's accuracy set-ups
+    "fig5": dict(W.FIG5),
+    "fig6_origin": dict(W.FIG6, n_det=41),
+    "fig7": dict(W.FIG7),
+    "paper64": dict(W.PAPER_TIMING[64]),
+    # ragged tiles and detector blocks
+    "ragged": dict(n=37, pixel=1.3, n_views=17, n_det=97, det_pitch=1.1, det_width=0.9,
+                   sid=120.0, sdd=260.0),
+    # one view, one bin
+    "one_view": dict(n=20, pixel=1.0, n_views=1, n_det=50, det_pitch=1.0, det_width=1.0,
+                     sid=60.0, sdd=100.0),
+    "one_bin": dict(n=8, pixel=1.0, n_views=12, n_det=1, det_pitch=4.0, det_width=4.0,
+                    sid=60.0, sdd=100.0),
+    # detector at the rotation centre (D_so = 0) and bins much wider than pixels
+    "dso0_wide": dict(n=24, pixel=0.5, n_views=30, n_det=9, det_pitch=3.0, det_width=3.0,
+                      sid=40.0, sdd=40.0),
+    # large tau / pitch ratio and many bins per pixel (BP multi-pass)
+    "fine_bins": dict(n=6, pixel=2.0, n_views=10, n_det=900, det_pitch=0.05, det_width=0.2,
+                      sid=30.0, sdd=55.0),
+}
+
+
+@pytest.mark.parametrize("name", sorted(EDGE))
+def test_edge_geometries(torch_cuda, name):
+    g = EDGE[name]
+    img = W.random_image(g["n"], 5)
+    _assert_parity(_fp(torch_cuda, g, img), O.forward(g, img), f"FP {name}")
+    y = W.random_sino(g["n_views"], g["n_det"], 105)
+    _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), f"BP {name}")
+
+
+def test_single_pixel_image(torch_cuda):
+    g = W.geometry("1")
+    img = W.single_pixel(g["n"], 10, 50)
+    _assert_parity(_fp(torch_cuda, g, img), O.forward(g, img), "FP single pixel")
+
+
+def test_zero_inputs(torch_cuda):
+    g = W.geometry("1")
+    assert not _fp(torch_cuda, g, np.zeros((64, 64), np.float32)).any()
+    assert not _bp(torch_cuda, g, np.zeros((90, 128), np.float32)).any()
+
+
+def test_batch_and_view_ranges(torch_cuda):
+    torch = torch_cuda
+    g = W.geometry("1")
+    imgs = W.random_image(g["n"], 3, batch=3)
+    y = _fp(torch, g, imgs, view_begin=10, view_count=25)
+    assert y.shape == (3, 25, g["n_det"])
+    ref = O.forward(g, imgs, view_begin=10, view_count=25)
+    for b in range(3):
+        _assert_parity(y[b], ref[b], f"FP batch {b}")
+    ys = W.random_sino(25, g["n_det"], 101, batch=2)
+    c = _bp(torch, g, ys, view_begin=10)
+    refc = O.back(g, ys, view_begin=10)
+    for b in range(2):
+        _assert_parity(c[b], refc[b], f"BP batch {b}")
+
+
+def test_accumulate_and_shards(torch_cuda):
+    torch = torch_cuda
+    g = W.geometry("1")
+    y = torch.from_numpy(W.random_sino(g["n_views"], g["n_det"], 102)).cuda()
+    full = cbp.back(g, y)
+    acc = cbp.back(g, y[:40].contiguous(), view_begin=0)
+    cbp.back(g, y[40:].contiguous(), image=acc, view_begin=40, accumulate=True)
+    torch.cuda.synchronize()
+    _assert_parity(acc.cpu().numpy(), full.cpu().numpy(), "BP shards")
+
+
+def test_deterministic(torch_cuda):
+    torch = torch_cuda
+    g = W.geometry("2")
+    img = torch.from_numpy(W.shepp_logan(g["n"])).cuda()
+    y1 = cbp.forward(g, img)
+    y2 = cbp.forward(g, img)
+    c1 = cbp.back(g, y1)
+    c2 = cbp.back(g, y1)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2) and torch.equal(c1, c2)
+
+
+def test_host_buffers_match_device(torch_cuda):
+    torch = torch_cuda
+    g = W.geometry("1")
+    img = W.random_image(g["n"], 1)
+    y_host = cbp.forward(g, img)  # numpy in, numpy out (staged)
+    y_dev = cbp.forward(g, torch.from_numpy(img).cuda()).cpu().numpy()
+    assert np.array_equal(y_host, y_dev)
+    c_host = cbp.back(g, y_host)
+    c_dev = cbp.back(g, torch.from_numpy(y_host).cuda()).cpu().numpy()
+    assert np.array_equal(c_host, c_dev)
+    assert np.isfinite(c_host).all()
