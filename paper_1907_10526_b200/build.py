@@ -28,6 +28,14 @@ def sources() -> list[str]:
                   if f.endswith((".cu", ".cuh", ".h")))
 
 
+def build_debug() -> str:
+    """libcbp_debug.so: the same library with device-side index checks (CBP_DEBUG_CHECKS)."""
+    out = os.path.join(PKG, "libcbp_debug.so")
+    cmd = [NVCC, *NVCC_FLAGS, "-DCBP_DEBUG_CHECKS", "-o", out, os.path.join(CSRC, "cbp.cu")]
+    subprocess.run(cmd, check=True, capture_output=True)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     deps = sources() + [os.path.join(ROOT, "include", "cbp.h"), os.path.abspath(__file__)]
     stale = (not os.path.exists(LIB)) or any(os.path.getmtime(d) > os.path.getmtime(LIB)

@@ -5,9 +5,11 @@
 //             -Xcompiler -fPIC -shared  (see paper_1907_10526_b200/build.py)
 #include "cbp.h"
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -89,6 +91,9 @@ int get_tables(const cbp_geometry_t& g, cudaStream_t stream, cbp::Tables& out)
         cbp::cbp_tables_kernel<<<(m + 127) / 128, 128, 0, stream>>>(to_dev(g), ts.view_cs,
                                                                     ts.bin_d, ts.bin_f);
         ++g_launches;
+#ifdef CBP_DEBUG_CHECKS
+        fprintf(stderr, "tables kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
+#endif
         if (cudaGetLastError() != cudaSuccess) return CBP_ECUDA;
         // tables are shared across streams: finish building before publishing
         if (cudaStreamSynchronize(stream) != cudaSuccess) return CBP_ECUDA;
@@ -151,37 +156,129 @@ int check_common(const cbp_geometry_t* g, const void* a, const void* b, int32_t 
     return CBP_OK;
 }
 
+// stream-ordered scratch from the device's default pool (kept, not released)
+int scratch_alloc(void** p, size_t bytes, cudaStream_t stream)
+{
+    static std::once_flag once[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::call_once(once[dev & 63], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+    if (cudaMallocAsync(p, bytes, stream) != cudaSuccess) {
+        cudaGetLastError();
+        return CBP_ECUDA;
+    }
+    return CBP_OK;
+}
+
+// width of the zero border around the image for the FP kernel: the largest
+// per-line candidate count K = floor(2 sigma_q) + 1 any ray can have, with
+// sigma_q = (A + C + tau') / (2 A) <= 1 + tau'_max / (sqrt(2) h) and
+// tau'_max <= (tau / D_ps) (D_po + n h / sqrt(2))
+int fp_pad_width(const cbp_geometry_t& g)
+{
+    const double taumax = g.det_width / g.sdd * (g.sid + g.n * g.pixel / std::sqrt(2.0));
+    const double sigq = 1.0 + taumax / (std::sqrt(2.0) * g.pixel);
+    return (int)std::floor(2.0 * sigq) + 2;
+}
+
 int launch_fp(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
               int32_t batch, int32_t v0, int32_t nv, cudaStream_t stream)
 {
-    cbp::FPParams P;
-    P.g = to_dev(g);
-    P.t = t;
-    P.image = img;
-    P.sino = sino;
-    P.view_begin = v0;
-    P.view_count = nv;
-    dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, nv, batch);
-    cbp::cbp_fp_kernel<<<grid, cbp::FP_BLOCK, 0, stream>>>(P);
+    const int P = fp_pad_width(g);
+    const int np = g.n + 2 * P;
+    const size_t plane = (size_t)np * np;
+    float* pad = nullptr;
+    int rc = scratch_alloc((void**)&pad, sizeof(float) * 2 * plane * batch, stream);
+    if (rc != CBP_OK) return rc;
+    float* padT = pad + plane * batch;
+    dim3 pgrid((np + cbp::PAD_TILE - 1) / cbp::PAD_TILE, (np + cbp::PAD_TILE - 1) / cbp::PAD_TILE,
+               batch);
+    cbp::cbp_pad_kernel<<<pgrid, dim3(cbp::PAD_TILE, 8), 0, stream>>>(img, pad, padT, g.n, P, np);
     ++g_launches;
-    return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+    cbp::FPParams Pm;
+    Pm.g = to_dev(g);
+    Pm.t = t;
+    Pm.pad = pad;
+    Pm.padT = padT;
+    Pm.np = np;
+    Pm.P = P;
+    Pm.sino = sino;
+    Pm.view_begin = v0;
+    Pm.view_count = nv;
+    dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, nv, batch);
+    cbp::cbp_fp_kernel<<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
+    ++g_launches;
+    rc = cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+    cudaFreeAsync(pad, stream);
+    return rc;
+}
+
+// number of view groups the BP splits the views into (one CTA per tile and
+// group): about 6 waves of 2 CTAs per SM, at least 8 views per group.
+int bp_groups(const cbp_geometry_t& g, int32_t batch, int32_t nv, int sms)
+{
+    const int tiles = ((g.n + cbp::BP_TILE - 1) / cbp::BP_TILE) * ((g.n + cbp::BP_TILE - 1) / cbp::BP_TILE);
+    const double target = 12.0 * sms;
+    int G = (int)std::lround(target / ((double)tiles * batch));
+    G = std::max(1, std::min(G, std::max(1, nv / 8)));
+    const int vpg = (nv + G - 1) / G;
+    return (nv + vpg - 1) / vpg;
 }
 
 int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
               int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream)
 {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int G = bp_groups(g, batch, nv, sms);
+    const int vpg = (nv + G - 1) / G;
+    const size_t plane = (size_t)g.n * g.n;
+    float* part = nullptr;
+    if (G > 1) {
+        int rc = scratch_alloc((void**)&part, sizeof(float) * plane * batch * G, stream);
+        if (rc != CBP_OK) return rc;
+    }
     cbp::BPParams P;
     P.g = to_dev(g);
     P.t = t;
     P.sino = sino;
-    P.image = img;
+    P.out = G > 1 ? part : img;
     P.view_begin = v0;
     P.view_count = nv;
+    P.groups = G;
+    P.views_per_group = vpg;
+    P.batch = batch;
     P.accumulate = accumulate ? 1 : 0;
     const int tiles = (g.n + cbp::BP_TILE - 1) / cbp::BP_TILE;
-    dim3 grid(tiles, tiles, batch);
+    dim3 grid(tiles, tiles, G * batch);
+#ifdef CBP_DEBUG_CHECKS
+    const char* skip = getenv("CBP_DEBUG_SKIP");
+    fprintf(stderr, "launch_bp G=%d vpg=%d grid=%d,%d,%d part=%p img=%p sino=%p\n", G, vpg, grid.x,
+            grid.y, grid.z, (void*)part, (void*)img, (const void*)sino);
+    if (!(skip && skip[0] == '1'))
+#endif
     cbp::cbp_bp_kernel<<<grid, cbp::BP_THREADS, 0, stream>>>(P);
     ++g_launches;
+#ifdef CBP_DEBUG_CHECKS
+    fprintf(stderr, "bp kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
+#endif
+    if (G > 1) {
+        const size_t count = plane * batch;
+        const int blocks = (int)std::min<size_t>((count + 255) / 256, (size_t)sms * 8);
+        cbp::cbp_reduce_kernel<<<blocks, 256, 0, stream>>>(part, img, count, G, accumulate ? 1 : 0);
+        ++g_launches;
+#ifdef CBP_DEBUG_CHECKS
+        fprintf(stderr, "reduce kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
+#endif
+        cudaFreeAsync(part, stream);
+    }
     return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
 }
 

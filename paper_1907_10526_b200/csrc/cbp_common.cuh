@@ -26,21 +26,23 @@ struct Tables {
 };
 
 // ---------------------------------------------------------------------------
-// Eq. 14 in a form that is stable in FP32.
+// Eq. 14 in a form that is stable in FP32 and cheap on the FP32 pipe
+// (pinned on CPU by tests/test_weight_form.py).
 //
 // M_{A,B,C}(x) = box_A * box_B * box_C (x) with A = max|zeta|, B = tau',
-// C = min|zeta|, is evaluated as nested antiderivative differences:
-//   R_C(z) = int_{-inf}^{z} H_C,  H_C the CDF of the centred box of width C
-//          = max(z', 0) + (C/2) sat(z'/C + 1)^2,        z' = z - C/2
-//   G(y)   = [R_C(y + B/2) - R_C(y - B/2)] / B           (CDF of box_B * box_C)
-//   M(x)   = [G(x + A/2) - G(x - A/2)] / A
-// which is algebraically Delta_A Delta_B Delta_C (x + sigma)_+^2 / (2! A B C)
-// (Eq. 14) but never divides by the possibly vanishing C: C = 0 gives
-// invC = +inf, sat() maps +-inf to {0, 1} and NaN to +0, and (C/2) t^2 = 0,
-// i.e. the delta direction is eliminated exactly as P:347 prescribes.
-//
-// cnsf_num returns A B M(x) = R(z11) - R(z12) - R(z21) + R(z22); the caller
-// multiplies by h^2 / A (per bin) and 1 / B.
+// C = min|zeta| (Eq. 12-14) is evaluated as nested antiderivative differences
+// of R_C(z) = int_{-inf}^z H_C (H_C the CDF of the centred box of width C):
+//   A B M(x) = sum_{a = +-A/2, b = +-B/2} +- R_C(x + a + b)
+// With z' = z - C/2, R_C = max(z', 0) + (C/2) sat(z'/C + 1)^2, and since the
+// four shifted knots pair up as z11 - z12 = z21 - z22 = B:
+//   sum +- max(z', 0) = clamp(z11, 0, B) - clamp(z21, 0, B)
+//                     = max(0, min(z11, A, B, A + B - z11))   (a trapezoid in z11)
+//   sum +- (C/2) t^2  = (C/2) (t11^2 - t12^2 - t21^2 + t22^2)
+// where z11 = x + (A - C)/2 + B/2, z21 = z11 - A, t1. = sat(z11/C + {1, w1}),
+// t2. = sat(z21/C + {1, w1}), w1 = 1 - B/C.  Never divides by a vanishing C:
+// C = 0 gives 1/C = +inf, sat() maps +-inf to {0, 1} and NaN to +0, and
+// (C/2) T = 0 -- the delta direction is eliminated exactly as P:347 says.
+// W = h^2 M = (h^2 / A) * num / B.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float sat_fma(float a, float b, float c)
 {
@@ -56,21 +58,37 @@ __device__ __forceinline__ float rcp_approx(float x)
     return y;
 }
 
-// hAmC = (A - C)/2, hApC = (A + C)/2, invC = 1/C, hC = C/2
-__device__ __forceinline__ float cnsf_num(float x, float B, float hAmC, float hApC, float invC,
-                                          float hC)
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+
+// 3-input minimum (FMNMX3 on sm_100a)
+__device__ __forceinline__ float fmin3(float a, float b, float c)
 {
-    const float hb = 0.5f * B;
-    const float y1 = x + hAmC;  // (x + A/2) - C/2
-    const float y2 = x - hApC;  // (x - A/2) - C/2
-    const float z11 = y1 + hb, z12 = y1 - hb, z21 = y2 + hb, z22 = y2 - hb;
-    const float t11 = sat_fma(z11, invC, 1.0f);
-    const float t12 = sat_fma(z12, invC, 1.0f);
-    const float t21 = sat_fma(z21, invC, 1.0f);
-    const float t22 = sat_fma(z22, invC, 1.0f);
-    const float m = (fmaxf(z11, 0.0f) - fmaxf(z12, 0.0f)) - (fmaxf(z21, 0.0f) - fmaxf(z22, 0.0f));
-    const float T = fmaf(t11, t11, -t12 * t12) - fmaf(t21, t21, -t22 * t22);
-    return fmaf(hC, T, m);
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
 }
+
+// Two weights at once (packed FFMA2 / FADD2 / FMUL2 on sm_100a): lanes share
+// the per-bin constants A, invC and hC = C/2.  Returns num = A B M for both.
+// The trapezoid part clamp(z11,0,B) - clamp(z21,0,B) is written as
+// max(0, min(z11, min(A, B), B - z21)), one 3-input min and two 2-input ops.
+__device__ __forceinline__ float2 cnsf_num2(float2 z11, float2 z21, float2 B, float2 w1, float A,
+                                            float invC, float hC)
+{
+    const float2 t11 = make_float2(sat_fma(z11.x, invC, 1.0f), sat_fma(z11.y, invC, 1.0f));
+    const float2 t12 = make_float2(sat_fma(z11.x, invC, w1.x), sat_fma(z11.y, invC, w1.y));
+    const float2 t21 = make_float2(sat_fma(z21.x, invC, 1.0f), sat_fma(z21.y, invC, 1.0f));
+    const float2 t22 = make_float2(sat_fma(z21.x, invC, w1.x), sat_fma(z21.y, invC, w1.y));
+    float2 T = __fmul2_rn(t11, t11);
+    T = __ffma2_rn(neg2(t12), t12, T);
+    T = __ffma2_rn(neg2(t21), t21, T);
+    T = __ffma2_rn(t22, t22, T);
+    const float2 r = __fadd2_rn(B, neg2(z21));  // A + B - z11
+    const float2 M2 = make_float2(fmaxf(fmin3(z11.x, fminf(A, B.x), r.x), 0.0f),
+                                  fmaxf(fmin3(z11.y, fminf(A, B.y), r.y), 0.0f));
+    return __ffma2_rn(make_float2(hC, hC), T, M2);
+}
+
+__device__ __forceinline__ float2 rcp2(float2 b) { return make_float2(rcp_approx(b.x), rcp_approx(b.y)); }
 
 }  // namespace cbp

@@ -6,15 +6,22 @@
 // the ray frame r_j, v_j, the projected pixel directions zeta1 = h r_x,
 // zeta2 = h r_y (Eq. 12) and the effective-blur gain g_j.  The
 // pixel-dependent quantities are affine in (row, col):
-//   s'(k)  = r_j . (p - k)       (Eq. 11 with the pixel moved to the origin, Eq. 4)
-//   tau'(k)= g_j (k - p) . v_j    (Eq. 13 on the plane through k, ledger #1)
+//   s'(k)   = r_j . (p - k)       (Eq. 11 with the pixel moved to the origin, Eq. 4)
+//   tau'(k) = g_j (k - p) . v_j   (Eq. 13 on the plane through k, ledger #1)
 // so the thread walks the image along the axis most parallel to the ray
 // ("lines" i) and, on each line, visits the K pixels q whose blurred support
-// can contain the ray: |s'| < (A + B + C)/2.  The crossing position q*(i) of
-// the ray on line i is carried in 32.32 fixed point, which keeps s' exact to
-// ~1e-7 h at any image size (an FP32 absolute coordinate would lose
-// log2(n) bits).  Each output is written once (no atomics,
-// deterministic; the paper's FP used atomic adds).
+// can contain the ray, |s'| < (A + B + C)/2.  The crossing of the ray's
+// support edge with line i is carried in 32.32 fixed point, which keeps s'
+// exact to ~1e-7 h at any image size (an FP32 absolute coordinate would lose
+// log2(n) bits).
+//
+// Layout: the image is read from a zero-padded copy (rows-major rays) or a
+// zero-padded transposed copy (column-major rays) built by cbp_pad_kernel,
+// so the K candidates of a line are always K consecutive floats (coalesced
+// across the warp's adjacent bins, no bounds checks).  Two lines are
+// evaluated together in packed f32x2 arithmetic (FFMA2), K is warp-uniform
+// and unrolled.  Each output is written once (no atomics, deterministic; the
+// paper's FP used atomic adds).
 #pragma once
 
 #include "cbp_common.cuh"
@@ -24,20 +31,163 @@ namespace cbp {
 struct FPParams {
     GeomDev g;
     Tables t;
-    const float* image;  // [batch][n][n]
-    float* sino;         // [batch][view_count][n_det]
+    const float* pad;   // [batch][np][np] zero-padded image, pixel (r, c) at (r + P, c + P)
+    const float* padT;  // [batch][np][np] its transpose
+    int np, P;          // padded side, pad width (>= max K)
+    float* sino;        // [batch][view_count][n_det]
     int view_begin, view_count;
 };
 
-constexpr int FP_BLOCK = 64;
+constexpr int FP_BLOCK = 128;
+constexpr int FP_KMAX_UNROLLED = 6;
+
+// ---- zero-padded (and transposed) image copies ----------------------------
+constexpr int PAD_TILE = 32;
+
+__global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_kernel(const float* __restrict__ img,
+                                                               float* __restrict__ pad,
+                                                               float* __restrict__ padT, int n,
+                                                               int P, int np)
+{
+    __shared__ float tile[PAD_TILE][PAD_TILE + 1];
+    const int b = blockIdx.z;
+    const int r0 = blockIdx.y * PAD_TILE, c0 = blockIdx.x * PAD_TILE;
+    const float* src = img + (size_t)b * n * n;
+    float* dst = pad + (size_t)b * np * np;
+    float* dstT = padT + (size_t)b * np * np;
+    for (int rr = threadIdx.y; rr < PAD_TILE; rr += 8) {
+        const int r = r0 + rr, c = c0 + threadIdx.x;
+        const int sr = r - P, sc = c - P;
+        float v = 0.0f;
+        if (sr >= 0 && sr < n && sc >= 0 && sc < n) v = src[(size_t)sr * n + sc];
+        tile[rr][threadIdx.x] = v;
+        if (r < np && c < np) dst[(size_t)r * np + c] = v;
+    }
+    __syncthreads();
+    for (int cc = threadIdx.y; cc < PAD_TILE; cc += 8) {
+        const int c = c0 + cc, r = r0 + threadIdx.x;
+        if (r < np && c < np) dstT[(size_t)c * np + r] = tile[threadIdx.x][cc];
+    }
+}
+
+// ---- per-ray constants -----------------------------------------------------
+// On line i the first candidate is q_lo = floor(e(i)) + 1, where e(i) is the
+// lower support edge in 32.32 fixed point; with f = frac(e(i)):
+//   s'(q_lo)   = b_q (1 - sigma_q - f)
+//   tau'(q_lo) = Be0 + i dB - tq f           (affine in i and f)
+//   z11(q_lo)  = z0c + bqs f + tau'/2
+// and the k-th candidate adds k dz to z11 (and z21), k tq to tau', k mtqc to w1.
+struct FPRay {
+    float z0c, bqs;       // z11 = z0c + bqs f_u + tau'/2   (f_u = f 2^32)
+    float Be0, dB, btq;   // tau' = Be0 + i dB + btq f_u
+    float dz, tq, mtqc;   // per-candidate increments of z11 (and z21), tau', w1
+    float A, invC, hC;
+    uint32_t flo, mlo;    // 32.32 fixed point: support lower edge on the first line, step
+    int32_t fhi, mhi;
+    const float* base;    // padded image of this ray's orientation (row / column major)
+};
+
+template <int K>
+__device__ __forceinline__ double fp_walk(const FPRay& R, int i0, int i1, int n, int np, int P)
+{
+    double dacc = 0.0;
+    float2 acc = make_float2(0.0f, 0.0f);
+    uint32_t flo = R.flo;
+    int32_t fhi = R.fhi;
+    const int qmax = n + P - K;
+    const float* row = R.base + (size_t)(i0 + P) * np + P;  // line i0, column 0
+    float2 fi = make_float2((float)i0, (float)i0 + 1.0f);
+    int iter = 0;
+    for (int i = i0; i <= i1; i += 2) {
+        // line a = i, line b = i + 1
+        const uint32_t fla = flo;
+        const int32_t ha = fhi;
+        uint32_t flb;
+        int32_t hb;
+        asm("add.cc.u32 %0, %2, %3;\n\taddc.s32 %1, %4, %5;"
+            : "=r"(flb), "=r"(hb) : "r"(flo), "r"(R.mlo), "r"(fhi), "r"(R.mhi));
+        asm("add.cc.u32 %0, %2, %3;\n\taddc.s32 %1, %4, %5;"
+            : "=r"(flo), "=r"(fhi) : "r"(flb), "r"(R.mlo), "r"(hb), "r"(R.mhi));
+        // first candidate (clamped into the zero border when the ray misses the line)
+        const int qa = min(max(ha + 1, -P), qmax), qb = min(max(hb + 1, -P), qmax);
+        const float* pa = row + qa;
+        const float* pb = row + np + qb;
+        row += 2 * (size_t)np;
+        const float2 f = make_float2((float)fla, (float)flb);
+        float2 B0 = __ffma2_rn(f, make_float2(R.btq, R.btq),
+                               __ffma2_rn(fi, make_float2(R.dB, R.dB), make_float2(R.Be0, R.Be0)));
+        B0 = make_float2(fmaxf(B0.x, 1e-30f), fmaxf(B0.y, 1e-30f));  // rays that miss: keep finite
+        fi = __fadd2_rn(fi, make_float2(2.0f, 2.0f));
+        float2 z11 = __ffma2_rn(f, make_float2(R.bqs, R.bqs), make_float2(R.z0c, R.z0c));
+        z11 = __ffma2_rn(make_float2(0.5f, 0.5f), B0, z11);
+        const float2 z21_0 = __fadd2_rn(z11, make_float2(-R.A, -R.A));
+        const float2 w1_0 = __ffma2_rn(neg2(B0), make_float2(R.invC, R.invC), make_float2(1.0f, 1.0f));
+        float ca[K], cb[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            ca[k] = __ldg(pa + k);
+            cb[k] = __ldg(pb + k);
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const float2 kk = make_float2((float)k, (float)k);
+            const float2 zz11 = k ? __ffma2_rn(kk, make_float2(R.dz, R.dz), z11) : z11;
+            const float2 zz21 = k ? __ffma2_rn(kk, make_float2(R.dz, R.dz), z21_0) : z21_0;
+            const float2 B = k ? __ffma2_rn(kk, make_float2(R.tq, R.tq), B0) : B0;
+            const float2 w1 = k ? __ffma2_rn(kk, make_float2(R.mtqc, R.mtqc), w1_0) : w1_0;
+            const float2 num = cnsf_num2(zz11, zz21, B, w1, R.A, R.invC, R.hC);
+            const float2 cw = __fmul2_rn(make_float2(ca[k], cb[k]), rcp2(B));
+            acc = __ffma2_rn(cw, num, acc);
+        }
+        if (++iter == 16) {  // two-level accumulation: FP32 partials, FP64 total
+            dacc += (double)acc.x + (double)acc.y;
+            acc = make_float2(0.0f, 0.0f);
+            iter = 0;
+        }
+    }
+    return dacc + (double)acc.x + (double)acc.y;
+}
+
+// generic K (wide bins relative to pixels): same arithmetic, runtime trip count
+__device__ double fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, int np, int P)
+{
+    double dacc = 0.0;
+    uint32_t flo = R.flo;
+    int32_t fhi = R.fhi;
+    const int qmax = n + P - K;
+    for (int i = i0; i <= i1; ++i) {
+        const uint32_t fl = flo;
+        const int q = min(max(fhi + 1, -P), qmax);
+        asm("add.cc.u32 %0, %0, %2;\n\taddc.s32 %1, %1, %3;"
+            : "+r"(flo), "+r"(fhi) : "r"(R.mlo), "r"(R.mhi));
+        const float* p = R.base + (size_t)(i + P) * np + (q + P);
+        const float ff = (float)fl;
+        const float B0 = fmaxf(fmaf(ff, R.btq, fmaf((float)i, R.dB, R.Be0)), 1e-30f);
+        const float z0 = fmaf(0.5f, B0, fmaf(ff, R.bqs, R.z0c));
+        float part = 0.0f;
+        for (int k = 0; k < K; ++k) {
+            const float kf = (float)k;
+            const float z11 = fmaf(kf, R.dz, z0);
+            const float z21 = z11 - R.A;
+            const float B = fmaf(kf, R.tq, B0);
+            const float w1 = fmaf(-B, R.invC, 1.0f);
+            const float2 num = cnsf_num2(make_float2(z11, z11), make_float2(z21, z21),
+                                         make_float2(B, B), make_float2(w1, w1), R.A, R.invC, R.hC);
+            part = fmaf(__ldg(p + k) * rcp_approx(B), num.x, part);
+        }
+        dacc += (double)part;
+    }
+    return dacc;
+}
 
 __global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
 {
     const GeomDev& g = P.g;
-    const int j = blockIdx.x * FP_BLOCK + threadIdx.x;
+    const int jr = blockIdx.x * FP_BLOCK + threadIdx.x;
+    const bool valid = jr < g.n_det;
+    const int j = valid ? jr : g.n_det - 1;
     const int vl = blockIdx.y;
     const int b = blockIdx.z;
-    if (j >= g.n_det) return;
     const int v = P.view_begin + vl;
     const int n = g.n;
 
@@ -63,24 +213,21 @@ __global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
     const double b_q = rows_major ? bcol : brow;  // step of s' along the line (|b_q| = A)
     const double t_i = gj * (rows_major ? drow : dcol);
     const double t_q = gj * (rows_major ? dcol : drow);
-    const size_t stride_i = rows_major ? (size_t)n : 1;
-    const size_t stride_q = rows_major ? 1 : (size_t)n;
-
     const double A = fabs(b_q), C = fabs(a_i);
     double dmax = D00;
     dmax = fmax(dmax, D00 + (n - 1) * dcol);
     dmax = fmax(dmax, D00 + (n - 1) * drow);
     dmax = fmax(dmax, D00 + (n - 1) * (dcol + drow));
     const double sig_q = 0.5 * (A + C + gj * dmax) / A;  // support half-width in pixels
-    const int K = (int)floor(2.0 * sig_q) + 1;          // max candidates per line
+    int K = (int)floor(2.0 * sig_q) + 1;                // candidates per line
 
-    // crossing of the ray with line i: q*(i) = Q0 + i m
+    // ray crossing of line i: q*(i) = Q0 + i m; lines whose window meets [0, n)
     const double Q0 = -X00 / b_q, m = -a_i / b_q;
-    double ilo, ihi;
+    int ilo, ihi;
     if (fabs(m) < 1e-15) {
         const bool hit = Q0 > -sig_q && Q0 < (n - 1) + sig_q;
-        ilo = hit ? 0.0 : 1.0;
-        ihi = hit ? (double)(n - 1) : 0.0;
+        ilo = hit ? 0 : n;
+        ihi = hit ? n - 1 : -1;
     } else {
         double a = (-sig_q - Q0) / m, c = ((n - 1) + sig_q - Q0) / m;
         if (a > c) {
@@ -88,48 +235,58 @@ __global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
             a = c;
             c = tmp;
         }
-        ilo = fmax(0.0, floor(a));
-        ihi = fmin((double)(n - 1), ceil(c));
+        a = fmax(-1.0, fmin((double)n, floor(a)));
+        c = fmax(-1.0, fmin((double)n, ceil(c)));
+        ilo = max(0, (int)a);
+        ihi = min(n - 1, (int)c);
     }
-
-    const float* img = P.image + (size_t)b * n * n;
-    const float bq_fx = (float)(b_q * 0x1p-32);
-    const float bq = (float)b_q, tq = (float)t_q, ti = (float)t_i;
-    const float T00 = (float)(gj * D00);
-    const float hA = (float)A, hC_ = (float)C;
-    const float hAmC = 0.5f * (hA - hC_), hApC = 0.5f * (hA + hC_);
-    const float invC = 1.0f / hC_;  // +inf when C == 0 (handled by sat)
-    const float hC = 0.5f * hC_;
-
-    const int64_t Q0fx = (int64_t)llrint(Q0 * 0x1p32);
-    const int64_t Mfx = (int64_t)llrint(m * 0x1p32);
-    const int64_t Sfx = (int64_t)llrint(sig_q * 0x1p32);
+    if (!valid) {
+        ilo = n;
+        ihi = -1;
+        K = 1;
+    }
+    const int wlo = __reduce_min_sync(0xffffffffu, ilo);
+    const int whi = __reduce_max_sync(0xffffffffu, ihi);
+    const int Kw = __reduce_max_sync(0xffffffffu, K);
 
     double acc = 0.0;
-    if (ilo <= ihi) {
-        const int i0 = (int)ilo, i1 = (int)ihi;
-        int64_t Qi = Q0fx + (int64_t)i0 * Mfx;
-        for (int i = i0; i <= i1; ++i, Qi += Mfx) {
-            const int q_lo = (int)((Qi - Sfx) >> 32) + 1;  // first pixel past q* - sigma
-            const int64_t dq = (int64_t)q_lo * 4294967296LL - Qi;  // (q_lo - q*) in 32.32
-            const float x0 = (float)dq * bq_fx;           // s' at pixel q_lo
-            const float tau0 = fmaf((float)q_lo, tq, fmaf((float)i, ti, T00));
-            const float* line = img + (size_t)i * stride_i;
-            float part = 0.0f;
-            for (int k = 0; k < K; ++k) {
-                const int q = q_lo + k;
-                const float x = fmaf((float)k, bq, x0);
-                const float B = fmaf((float)k, tq, tau0);
-                const float c = ((unsigned)q < (unsigned)n) ? __ldg(line + (size_t)q * stride_q) : 0.0f;
-                const float num = cnsf_num(x, B, hAmC, hApC, invC, hC);
-                const bool in = fabsf(x) < fmaf(0.5f, B, hApC);  // open support (ledger #15)
-                part = fmaf(in ? c : 0.0f, num * rcp_approx(B), part);
-            }
-            acc += (double)part;
+    if (Kw > P.P) acc = __longlong_as_double(0x7ff8000000000000ll);  // pad too thin: fail loudly (NaN)
+    if (wlo <= whi && Kw <= P.P) {
+        FPRay R;
+        // lower support edge on line i: q*(i) - sig_q, as 32.32 fixed point from line wlo
+        const int64_t E0 = (int64_t)llrint((Q0 + (double)wlo * m - sig_q) * 0x1p32);
+        const int64_t Mfx = (int64_t)llrint(m * 0x1p32);
+        R.flo = (uint32_t)(uint64_t)E0;
+        R.fhi = (int32_t)(E0 >> 32);
+        R.mlo = (uint32_t)(uint64_t)Mfx;
+        R.mhi = (int32_t)(Mfx >> 32);
+        // candidate q_lo = floor(e) + 1 has s' = b_q (q_lo - q*) = b_q (1 - sig_q - frac(e));
+        // z11 = s' + (A - C)/2 + B/2
+        R.z0c = (float)(b_q * (1.0 - sig_q) + 0.5 * (A - C));
+        R.bqs = (float)(-b_q * 0x1p-32);
+        R.Be0 = (float)(gj * D00 + (Q0 - sig_q + 1.0) * t_q);
+        R.dB = (float)(t_i + m * t_q);
+        R.btq = (float)(-t_q * 0x1p-32);
+        R.dz = (float)(b_q + 0.5 * t_q);
+        R.tq = (float)t_q;
+        R.A = (float)A;
+        const float Cf = (float)C;
+        R.invC = 1.0f / Cf;  // +inf for C == 0: handled by sat()
+        R.hC = 0.5f * Cf;
+        R.mtqc = -R.tq * R.invC;
+        R.base = (rows_major ? P.pad : P.padT) + (size_t)b * P.np * P.np;
+        switch (Kw) {
+            case 1: acc = fp_walk<1>(R, wlo, whi, n, P.np, P.P); break;
+            case 2: acc = fp_walk<2>(R, wlo, whi, n, P.np, P.P); break;
+            case 3: acc = fp_walk<3>(R, wlo, whi, n, P.np, P.P); break;
+            case 4: acc = fp_walk<4>(R, wlo, whi, n, P.np, P.P); break;
+            case 5: acc = fp_walk<5>(R, wlo, whi, n, P.np, P.P); break;
+            case 6: acc = fp_walk<6>(R, wlo, whi, n, P.np, P.P); break;
+            default: acc = fp_walk_generic(R, Kw, wlo, whi, n, P.np, P.P); break;
         }
+        acc *= h * h / A;  // W = (h^2 / A) num / B
     }
-    // W = h^2 M = (h^2 / A) * num / B
-    P.sino[((size_t)b * P.view_count + vl) * g.n_det + j] = (float)(acc * (h * h / A));
+    if (valid) P.sino[((size_t)b * P.view_count + vl) * g.n_det + j] = (float)acc;
 }
 
 }  // namespace cbp

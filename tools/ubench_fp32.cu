@@ -23,7 +23,7 @@ __global__ void kern(float* out, float s)
             if (MODE == 2) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p[i]) : "l"(S), "l"(T));       // FFMA2
             if (MODE == 3) asm volatile("fma.rn.sat.f32 %0, %0, %1, %2;" : "+f"(a[i]) : "f"(s), "f"(a[(i+1)&7])); // FFMA.SAT
             if (MODE == 4) asm volatile("max.f32 %0, %0, %1;" : "+f"(a[i]) : "f"(a[(i+3)&7]));             // FMNMX
-            if (MODE == 5) asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(a[i]));                         // MUFU.RCP
+            if (MODE == 5) { float r; asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a[i])); a[i] = r + 1.0f; }  // MUFU.RCP (+FADD)
             if (MODE == 6) { // mix: 2 FFMA2 + 1 FFMA.SAT + 1 FMNMX
                 asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p[i]) : "l"(S), "l"(T));
                 asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p[(i+4)&7]) : "l"(S), "l"(T));
@@ -53,6 +53,7 @@ void run(const char* name, int ipi, float* d, int sms, int clk_khz)
     for (int r = 0; r < 5; ++r) kern<MODE><<<blocks, threads>>>(d, 0.999f);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
+    if (cudaGetLastError() != cudaSuccess) printf("launch error\n");
     double warp_instr = 5.0 * blocks * (threads / 32) * (double)ITERS * 8 * ipi;
     double per_s = warp_instr / (ms * 1e-3);
     printf("%-28s %8.2f ms  %7.3f warp-instr/clk/SM (at %d MHz)  %.1f Tinstr-lane/s\n", name, ms,
