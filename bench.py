@@ -52,13 +52,6 @@ def parse():
     return ap.parse_args()
 
 
-def shard(n_views: int, rank: int, world: int):
-    """contiguous view block of this rank."""
-    base, rem = divmod(n_views, world)
-    v0 = rank * base + min(rank, rem)
-    return v0, base + (1 if rank < rem else 0)
-
-
 def weight_counts(cfg: str):
     path = os.path.join(ROOT, "tests", "golden", "weight_counts.json")
     try:
@@ -141,13 +134,15 @@ def run_reference(args, rank, world):
     img = W.shepp_logan(g["n"]).astype(np.float64)
     cores = os.cpu_count() or 1
     O.build()
-    # size each step so the whole run takes about a minute
+    # size each step so the whole run takes about a minute; at least one view
+    # per core (the oracle's FP is parallel over views)
+    probe = min(g["n_views"], max(8, cores))
     t0 = time.perf_counter()
-    y = O.forward(g, img, view_begin=0, view_count=1, threads=cores)
+    y = O.forward(g, img, view_begin=0, view_count=probe, threads=cores)
     O.back(g, y, view_begin=0, threads=cores)
-    per_view = time.perf_counter() - t0
+    per_view = (time.perf_counter() - t0) / probe
     budget = 60.0 / max(1, args.steps + args.warmup)
-    nvs = int(max(1, min(g["n_views"], budget / max(per_view, 1e-6))))
+    nvs = int(max(min(g["n_views"], cores), min(g["n_views"], budget / max(per_view, 1e-6))))
     times = []
     for k in range(args.warmup + args.steps):
         v0 = (k * 37) % (g["n_views"] - nvs + 1)
@@ -182,11 +177,12 @@ def cpu_baseline(cfg: str, target_s: float = 12.0):
     img = W.shepp_logan(g["n"]).astype(np.float64)
     cores = os.cpu_count() or 1
     O.build()
+    probe = min(g["n_views"], max(8, cores))
     t0 = time.perf_counter()
-    y = O.forward(g, img, view_begin=0, view_count=2, threads=cores)
+    y = O.forward(g, img, view_begin=0, view_count=probe, threads=cores)
     O.back(g, y, view_begin=0, threads=cores)
-    per_view = (time.perf_counter() - t0) / 2
-    nvs = int(max(2, min(g["n_views"], target_s / max(per_view, 1e-6))))
+    per_view = (time.perf_counter() - t0) / probe
+    nvs = int(max(probe, min(g["n_views"], target_s / max(per_view, 1e-6))))
     t0 = time.perf_counter()
     y = O.forward(g, img, view_begin=0, view_count=nvs, threads=cores)
     O.back(g, y, view_begin=0, threads=cores)
@@ -211,6 +207,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1907_10526_b200 as cbp
+    from paper_1907_10526_b200.sharded import view_shard
 
     assert args.warmup >= 3, "at least 3 warm-up steps"
     torch.cuda.set_device(local)
@@ -218,7 +215,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     g = W.geometry(args.config)
-    v0, nv = shard(g["n_views"], rank, world)
+    v0, nv = view_shard(g["n_views"], rank, world)
     n, ns = g["n"], g["n_det"]
 
     img = torch.from_numpy(W.shepp_logan(n)).to(dev)
