@@ -105,6 +105,54 @@ int get_tables(const cbp_geometry_t& g, cudaStream_t stream, cbp::Tables& out)
     return CBP_OK;
 }
 
+// ---- BP pair order per ray-direction bucket (device-resident, per device) --
+// For bucket b (ray direction phi_b = (b + 1/2) pi / BP_BUCKETS, physical
+// angle) the 512 pixel pairs of a 32 x 32 tile -- horizontal pairs when the
+// rays are within 45 degrees of the x axis, else vertical -- sorted by the
+// lateral coordinate of their centre, col sin(phi) + row cos(phi) (row axis
+// pointing down = -y).  Entry = r * 32 + c of the pair's first pixel.
+std::mutex g_pairs_mu;
+std::map<int, uint16_t*> g_pairs;
+
+int get_pair_order(const uint16_t** out)
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return CBP_ECUDA;
+    std::lock_guard<std::mutex> lock(g_pairs_mu);
+    auto it = g_pairs.find(dev);
+    if (it == g_pairs.end()) {
+        const int NP = cbp::BP_PAIRS, T = cbp::BP_TILE;
+        std::vector<uint16_t> host((size_t)cbp::BP_BUCKETS * NP);
+        for (int b = 0; b < cbp::BP_BUCKETS; ++b) {
+            const double phi = (b + 0.5) * 3.14159265358979323846 / cbp::BP_BUCKETS;
+            const bool horiz = cbp::bucket_horiz(b);
+            std::vector<std::pair<double, int>> key;
+            for (int a = 0; a < T; ++a)
+                for (int q = 0; q < T / 2; ++q) {
+                    const int r = horiz ? a : 2 * q, c = horiz ? 2 * q : a;
+                    const double cc = c + (horiz ? 0.5 : 0.0), rr = r + (horiz ? 0.0 : 0.5);
+                    key.emplace_back(cc * std::sin(phi) + rr * std::cos(phi), r * T + c);
+                }
+            std::stable_sort(key.begin(), key.end(),
+                             [](const std::pair<double, int>& x, const std::pair<double, int>& y) {
+                                 return x.first < y.first;
+                             });
+            for (int i = 0; i < NP; ++i) host[(size_t)b * NP + i] = (uint16_t)key[i].second;
+        }
+        uint16_t* d = nullptr;
+        if (cudaMalloc(&d, host.size() * sizeof(uint16_t)) != cudaSuccess ||
+            cudaMemcpy(d, host.data(), host.size() * sizeof(uint16_t), cudaMemcpyHostToDevice) !=
+                cudaSuccess) {
+            cudaFree(d);
+            cudaGetLastError();
+            return CBP_ECUDA;
+        }
+        it = g_pairs.emplace(dev, d).first;
+    }
+    *out = it->second;
+    return CBP_OK;
+}
+
 // ---- host-buffer staging workspace --------------------------------------
 struct Workspace {
     void* buf[2] = {nullptr, nullptr};
@@ -246,6 +294,10 @@ int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, 
         if (rc != CBP_OK) return rc;
     }
     cbp::BPParams P;
+    if (get_pair_order(&P.pairs) != CBP_OK) {
+        if (part) cudaFreeAsync(part, stream);
+        return CBP_ECUDA;
+    }
     P.g = to_dev(g);
     P.t = t;
     P.sino = sino;

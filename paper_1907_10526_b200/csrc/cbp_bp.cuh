@@ -17,12 +17,15 @@
 //  3. every thread evaluates two pixel PAIRS, each pair two pixels adjacent
 //     along the image axis most parallel to this view's rays (they share
 //     bins), in packed f32x2 arithmetic over the union of their support
-//     intervals.  Which pixels a thread owns depends on that axis: a warp
-//     always covers 2 x 32 pixels of two tile lines along the rays, so its
-//     lanes read the same few entries (shared-memory broadcast) and have
+//     intervals.  Which pairs a thread owns depends on the rays' direction
+//     through the tile, quantised to BP_BUCKETS directions over [0, pi):
+//     for each direction the 512 pairs are sorted by their lateral
+//     coordinate (perpendicular to the rays) and dealt out in that order, so
+//     the 32 lanes of a warp hold a thin strip of pairs along the rays --
+//     they read the same few entries (shared-memory broadcast) and have
 //     nearly equal trip counts (little divergence).  Partial sums live in
-//     registers for a run of views with the same axis and are flushed to a
-//     per-tile FP64 accumulator in shared memory.
+//     registers for a run of views with the same direction bucket and are
+//     flushed to a per-tile FP64 accumulator in shared memory.
 // Views are split into groups across CTAs for occupancy; groups > 1 write
 // FP32 partial images that cbp_reduce_kernel sums in a fixed order.  No
 // atomics anywhere: the result is deterministic.
@@ -35,6 +38,7 @@ namespace cbp {
 struct BPParams {
     GeomDev g;
     Tables t;
+    const uint16_t* pairs;  // [BP_BUCKETS][512] tile pair order per ray direction (r * 32 + c)
     const float* sino;  // [batch][view_count][n_det]
     float* out;         // groups == 1: image [batch][n][n]; else partials [groups][batch][n][n]
     int view_begin, view_count;
@@ -46,6 +50,8 @@ constexpr int BP_TILE = 32;       // pixels per tile side
 constexpr int BP_THREADS = 256;   // 8 warps x 2 pairs x 2 pixels x 32 lanes = 32 x 32
 constexpr int BP_VC = 8;          // views per chunk
 constexpr int BP_NB = 80;         // bins per view per pass (a 32-pixel tile spans <= ~64)
+constexpr int BP_BUCKETS = 32;    // ray directions over [0, pi) for the pair order
+constexpr int BP_PAIRS = BP_TILE * BP_TILE / 2;
 
 struct __align__(16) BPEntry {
     float4 a;  // z11(k_a), dz11/dc, dz11/dr, tau'(k_a)
@@ -53,8 +59,8 @@ struct __align__(16) BPEntry {
     float4 c;  // A, 1/C, C/2, y[b][v][j] h^2 / A
 };
 
-struct BPHeader {
-    int ja, jlo, jhi, horiz;   // nearest bin of P(k_a); tile bin range; pair axis (1 = x)
+struct __align__(16) BPHeader {
+    int ja, jlo, jhi, bucket;  // nearest bin of P(k_a); tile bin range; ray-direction bucket
     float urel, nx, ny, cW;    // u(k) - ja = urel + (nx dc + ny dr) / den;  W(k) = cW / den
     float dena, dx, dy, npass_f;  // den = delta_k = dena + dx dc + dy dr
     double delta_a, f_a, cth, sth, kae;
@@ -119,7 +125,10 @@ __device__ void bp_view_header(const GeomDev& g, const Tables& t, int v, double 
     H.ja = (int)ja;
     H.jlo = (int)jl;
     H.jhi = (int)jh;
-    H.horiz = fabsf(nx) <= fabsf(ny);  // pair the pixels whose projections nearly coincide
+    // direction of the rays through the tile (source -> anchor), modulo pi
+    float phi = atan2f((float)(kay - g.sid * sth), (float)(kax - g.sid * cth));
+    if (phi < 0.0f) phi += 3.14159265f;
+    H.bucket = min(BP_BUCKETS - 1, max(0, (int)(phi * (BP_BUCKETS / 3.14159265f))));
     H.urel = urel;
     H.nx = nx;
     H.ny = ny;
@@ -134,6 +143,9 @@ __device__ void bp_view_header(const GeomDev& g, const Tables& t, int v, double 
     H.sth = sth;
     H.kae = kae;
 }
+
+// pairs along x for ray directions within 45 degrees of the x axis
+__host__ __device__ inline bool bucket_horiz(int b) { return b < BP_BUCKETS / 4 || b >= 3 * BP_BUCKETS / 4; }
 
 __device__ void bp_build_entry(const GeomDev& g, const Tables& t, const BPHeader& H, int j, float y,
                                BPEntry& E)
@@ -154,8 +166,23 @@ __device__ void bp_build_entry(const GeomDev& g, const Tables& t, const BPHeader
     const float tx = -gj * ry * h, ty = -gj * rx * h;  // dtau'/dc, dtau'/dr
     const float zsx = -rx * h + 0.5f * tx, zsy = ry * h + 0.5f * ty;
     E.a = make_float4((float)(xa + 0.5 * ((double)A - (double)C) + 0.5 * (double)Ba), zsx, zsy, Ba);
-    E.b = make_float4(tx, ty, H.horiz ? zsx : zsy, H.horiz ? tx : ty);
+    const bool horiz = bucket_horiz(H.bucket);
+    E.b = make_float4(tx, ty, horiz ? zsx : zsy, horiz ? tx : ty);
     E.c = make_float4(A, 1.0f / C, 0.5f * C, y * (h * h / A));
+}
+
+// one entry, one pixel pair (lane b = lane a + one pixel along the pair axis)
+__device__ __forceinline__ float2 bp_eval(const BPEntry* e, float dc, float dr, float2 acc)
+{
+    const float4 ea = e->a, eb = e->b, ec = e->c;
+    const float za = fmaf(dr, ea.z, fmaf(dc, ea.y, ea.x));
+    const float Ba = fmaf(dr, eb.y, fmaf(dc, eb.x, ea.w));
+    const float2 z11 = make_float2(za, za + eb.z);
+    const float2 B = make_float2(Ba, Ba + eb.w);
+    const float2 z21 = __fadd2_rn(z11, make_float2(-ec.x, -ec.x));
+    const float2 w1 = __ffma2_rn(neg2(B), make_float2(ec.y, ec.y), make_float2(1.0f, 1.0f));
+    const float2 num = cnsf_num2(z11, z21, B, w1, ec.x, ec.y, ec.z);
+    return __ffma2_rn(__fmul2_rn(make_float2(ec.w, ec.w), rcp2(B)), num, acc);
 }
 
 // entries row[jl - base .. jh - base]; empty when jh < jl (no pointer is
@@ -163,47 +190,25 @@ __device__ void bp_build_entry(const GeomDev& g, const Tables& t, const BPHeader
 __device__ __forceinline__ float2 bp_pair(const BPEntry* row, int jl, int jh, int base, float dc,
                                           float dr, float2 acc)
 {
+    if (jh < jl) return acc;
+    CBP_CHECK(jl >= base && jh - base < BP_NB, "bp_pair jl=%d jh=%d base=%d\n", jl, jh, base);
     const int cnt = jh - jl + 1;
-    if (cnt <= 0) return acc;
     const BPEntry* e = row + (jl - base);
-    for (int k = 0; k < cnt; ++k, ++e) {
-        const float4 ea = e->a, eb = e->b, ec = e->c;
-        const float za = fmaf(dr, ea.z, fmaf(dc, ea.y, ea.x));
-        const float Ba = fmaf(dr, eb.y, fmaf(dc, eb.x, ea.w));
-        const float2 z11 = make_float2(za, za + eb.z);
-        const float2 B = make_float2(Ba, Ba + eb.w);
-        const float2 z21 = __fadd2_rn(z11, make_float2(-ec.x, -ec.x));
-        const float2 w1 = __ffma2_rn(neg2(B), make_float2(ec.y, ec.y), make_float2(1.0f, 1.0f));
-        const float2 num = cnsf_num2(z11, z21, B, w1, ec.x, ec.y, ec.z);
-        acc = __ffma2_rn(__fmul2_rn(make_float2(ec.w, ec.w), rcp2(B)), num, acc);
-    }
+    for (int k = 0; k < cnt; ++k, ++e) acc = bp_eval(e, dc, dr, acc);
     return acc;
 }
 
-// Thread -> pixel pair map.  Pair p of thread (warp w, lane l): tile line
-// L = 4 w + 2 p + l / 16, position Q = 2 (l % 16); for horiz (pairs along x)
-// the pixels are (row L, cols Q, Q+1), else (rows Q, Q+1, col L).
-__device__ __forceinline__ void pair_pixel(int tid, int p, int horiz, int& r, int& c)
+__device__ __forceinline__ void bp_flush(double (*acc_s)[BP_TILE + 1], int horiz, int e0, int e1,
+                                         float2 a0, float2 a1)
 {
-    const int w = tid >> 5, l = tid & 31;
-    const int L = 4 * w + 2 * p + (l >> 4), Q = 2 * (l & 15);
-    r = horiz ? L : Q;
-    c = horiz ? Q : L;
+    const int r0 = e0 >> 5, c0 = e0 & 31, r1 = e1 >> 5, c1 = e1 & 31;
+    acc_s[r0][c0] += (double)a0.x;
+    acc_s[r0 + !horiz][c0 + horiz] += (double)a0.y;
+    acc_s[r1][c1] += (double)a1.x;
+    acc_s[r1 + !horiz][c1 + horiz] += (double)a1.y;
 }
 
-__device__ __forceinline__ void bp_flush(double (*acc_s)[BP_TILE + 1], int tid, int horiz, float2 a0,
-                                         float2 a1)
-{
-    int r, c;
-    pair_pixel(tid, 0, horiz, r, c);
-    acc_s[r][c] += (double)a0.x;
-    acc_s[r + !horiz][c + horiz] += (double)a0.y;
-    pair_pixel(tid, 1, horiz, r, c);
-    acc_s[r][c] += (double)a1.x;
-    acc_s[r + !horiz][c + horiz] += (double)a1.y;
-}
-
-__global__ void __launch_bounds__(BP_THREADS, 3) cbp_bp_kernel(const BPParams P)
+__global__ void __launch_bounds__(BP_THREADS, 4) cbp_bp_kernel(const BPParams P)
 {
     __shared__ BPEntry tab[BP_VC][BP_NB];
     __shared__ BPHeader hdr[BP_VC];
@@ -237,6 +242,7 @@ __global__ void __launch_bounds__(BP_THREADS, 3) cbp_bp_kernel(const BPParams P)
                 if (vi < nvc) {
                     const BPHeader& H = hdr[vi];
                     const int j = H.jlo + pass * BP_NB + jj;
+                    CBP_CHECK(j > H.jhi || (j >= 0 && j < g.n_det), "entry j=%d jlo=%d jhi=%d\n", j, H.jlo, H.jhi);
                     if (j <= H.jhi)
                         bp_build_entry(g, P.t, H, j,
                                        __ldg(y + (size_t)(vg0 + vc + vi) * g.n_det + j), tab[vi][jj]);
@@ -244,44 +250,62 @@ __global__ void __launch_bounds__(BP_THREADS, 3) cbp_bp_kernel(const BPParams P)
             }
             __syncthreads();
             float2 a0 = make_float2(0.f, 0.f), a1 = a0;
-            int mode = hdr[0].horiz;
+            int bucket = -1, horiz = 1, e0 = 0, e1 = 0;
+            float2 dc0, dr0, dc1, dr1;  // pixel offsets of the two pairs (lanes a, b)
             for (int vi = 0; vi < nvc; ++vi) {
                 const BPHeader& H = hdr[vi];
-                if (H.horiz != mode) {  // the pair axis flips: hand the pixels back
-                    bp_flush(acc_s, tid, mode, a0, a1);
-                    a0 = a1 = make_float2(0.f, 0.f);
-                    mode = H.horiz;
-                    __syncthreads();
+                const int4 hi = *reinterpret_cast<const int4*>(&H.ja);  // ja, jlo, jhi, bucket
+                if (hi.w != bucket) {  // new pair order: hand the pixels back first
+                    if (bucket >= 0) {
+                        bp_flush(acc_s, horiz, e0, e1, a0, a1);
+                        a0 = a1 = make_float2(0.f, 0.f);
+                        __syncthreads();
+                    }
+                    bucket = hi.w;
+                    horiz = bucket_horiz(bucket);
+                    const uint16_t* order = P.pairs + bucket * BP_PAIRS + (tid >> 5) * 64 + (tid & 31);
+                    CBP_CHECK(bucket >= 0 && bucket < BP_BUCKETS, "bucket %d\n", bucket);
+                    e0 = __ldg(order);
+                    e1 = __ldg(order + 32);
+                    const float sx = horiz ? 1.0f : 0.0f, sy = 1.0f - sx;  // pair step (dc, dr)
+                    const float c0 = (float)(e0 & 31) - hcx, r0 = (float)(e0 >> 5) - hcy;
+                    const float c1 = (float)(e1 & 31) - hcx, r1 = (float)(e1 >> 5) - hcy;
+                    dc0 = make_float2(c0, c0 + sx);
+                    dr0 = make_float2(r0, r0 + sy);
+                    dc1 = make_float2(c1, c1 + sx);
+                    dr1 = make_float2(r1, r1 + sy);
                 }
-                const int base = H.jlo + pass * BP_NB;
-                if (base > H.jhi) continue;
+                const int base = hi.y + pass * BP_NB;
+                if (base > hi.z) continue;
                 const BPEntry* row = tab[vi];
-                const float sx = mode ? 1.0f : 0.0f, sy = 1.0f - sx;  // pair step (dc, dr)
+                const float4 hf = *reinterpret_cast<const float4*>(&H.urel);  // urel, nx, ny, cW
+                const float4 hd = *reinterpret_cast<const float4*>(&H.dena);  // dena, dx, dy, -
+                const int jmax = min(hi.z, base + BP_NB - 1);
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    int r, c;
-                    pair_pixel(tid, p, mode, r, c);
-                    const float dc = (float)c - hcx, dr = (float)r - hcy;
+                    const float2 dcp = p ? dc1 : dc0, drp = p ? dr1 : dr0;
                     // exact bin coordinates of the two pixels, and their support bounds
-                    const float2 dcp = make_float2(dc, dc + sx), drp = make_float2(dr, dr + sy);
-                    const float2 num = __ffma2_rn(drp, make_float2(H.ny, H.ny),
-                                                  __fmul2_rn(dcp, make_float2(H.nx, H.nx)));
-                    const float2 den = __ffma2_rn(drp, make_float2(H.dy, H.dy),
-                                                  __ffma2_rn(dcp, make_float2(H.dx, H.dx),
-                                                             make_float2(H.dena, H.dena)));
+                    const float2 num = __ffma2_rn(drp, make_float2(hf.z, hf.z),
+                                                  __fmul2_rn(dcp, make_float2(hf.y, hf.y)));
+                    const float2 den = __ffma2_rn(drp, make_float2(hd.z, hd.z),
+                                                  __ffma2_rn(dcp, make_float2(hd.y, hd.y),
+                                                             make_float2(hd.x, hd.x)));
                     const float2 inv = rcp2(den);
-                    const float2 u = __ffma2_rn(num, inv, make_float2(H.urel, H.urel));
-                    const float2 w = __ffma2_rn(make_float2(H.cW, H.cW), inv, make_float2(2e-3f, 2e-3f));
-                    const float lo = fminf(u.x - w.x, u.y - w.y), hi = fmaxf(u.x + w.x, u.y + w.y);
-                    const int jl = max(H.ja + __float2int_rd(lo) + 1, base);
-                    const int jh = min(H.ja + __float2int_ru(hi) - 1, min(H.jhi, base + BP_NB - 1));
+                    const float2 u = __ffma2_rn(num, inv, make_float2(hf.x, hf.x));
+                    const float2 w = __ffma2_rn(make_float2(hf.w, hf.w), inv, make_float2(2e-3f, 2e-3f));
+                    // clamp before the integer conversion: pixels of a ragged tile that lie
+                    // outside the image can give inf / NaN here (their sums are discarded)
+                    const float lo = fmaxf(fminf(fminf(u.x - w.x, u.y - w.y), 1e6f), -1e6f);
+                    const float hi2 = fmaxf(fminf(fmaxf(u.x + w.x, u.y + w.y), 1e6f), -1e6f);
+                    const int jl = max(hi.x + __float2int_rd(lo) + 1, base);
+                    const int jh = min(hi.x + __float2int_ru(hi2) - 1, jmax);
                     if (p == 0)
-                        a0 = bp_pair(row, jl, jh, base, dc, dr, a0);
+                        a0 = bp_pair(row, jl, jh, base, dcp.x, drp.x, a0);
                     else
-                        a1 = bp_pair(row, jl, jh, base, dc, dr, a1);
+                        a1 = bp_pair(row, jl, jh, base, dcp.x, drp.x, a1);
                 }
             }
-            bp_flush(acc_s, tid, mode, a0, a1);
+            if (bucket >= 0) bp_flush(acc_s, horiz, e0, e1, a0, a1);
             __syncthreads();
         }
     }

@@ -7,6 +7,23 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Device-side index checks for the debug build (libcbp_debug.so, built with
+// -DCBP_DEBUG_CHECKS): print the violated condition; no-ops otherwise.
+#ifdef CBP_DEBUG_CHECKS
+#include <cstdio>
+#define CBP_CHECK(cond, ...)                                              \
+    do {                                                                  \
+        if (!(cond)) {                                                    \
+            printf("CBP_CHECK %s:%d %s | ", __FILE__, __LINE__, #cond);   \
+            printf(__VA_ARGS__);                                          \
+        }                                                                 \
+    } while (0)
+#else
+#define CBP_CHECK(cond, ...) \
+    do {                     \
+    } while (0)
+#endif
+
 namespace cbp {
 
 // Geometry as the kernels see it (FP64 scalars + derived constants).
