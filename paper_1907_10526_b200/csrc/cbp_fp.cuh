@@ -87,65 +87,94 @@ struct FPRay {
     const float* base;    // padded image of this ray's orientation (row / column major)
 };
 
-template <int K>
+// MAB: how min(A, tau') is known along the ray (warp-uniform): 0 = evaluate
+// per candidate, 1 = tau' <= A everywhere (min = tau'), 2 = tau' >= A (min = A).
+//
+// Along a line every knot argument is affine in the candidate index k, so the
+// four sat() arguments t.. = sat(z/C + ...) are formed directly from k
+// (u11 = z11/C + 1, u12 = u11 - tau'/C, u21 = u11 - A/C, u22 = u12 - A/C),
+// and the trapezoid bound r = A + tau' - z11 is affine in k too.
+template <int K, int MAB>
 __device__ __forceinline__ double fp_walk(const FPRay& R, int i0, int i1, int n, int np, int P)
 {
     double dacc = 0.0;
-    float2 acc = make_float2(0.0f, 0.0f);
     uint32_t flo = R.flo;
     int32_t fhi = R.fhi;
     const int qmax = n + P - K;
     const float* row = R.base + (size_t)(i0 + P) * np + P;  // line i0, column 0
     float2 fi = make_float2((float)i0, (float)i0 + 1.0f);
-    int iter = 0;
-    for (int i = i0; i <= i1; i += 2) {
-        // line a = i, line b = i + 1
-        const uint32_t fla = flo;
-        const int32_t ha = fhi;
-        uint32_t flb;
-        int32_t hb;
-        asm("add.cc.u32 %0, %2, %3;\n\taddc.s32 %1, %4, %5;"
-            : "=r"(flb), "=r"(hb) : "r"(flo), "r"(R.mlo), "r"(fhi), "r"(R.mhi));
-        asm("add.cc.u32 %0, %2, %3;\n\taddc.s32 %1, %4, %5;"
-            : "=r"(flo), "=r"(fhi) : "r"(flb), "r"(R.mlo), "r"(hb), "r"(R.mhi));
-        // first candidate (clamped into the zero border when the ray misses the line)
-        const int qa = min(max(ha + 1, -P), qmax), qb = min(max(hb + 1, -P), qmax);
-        const float* pa = row + qa;
-        const float* pb = row + np + qb;
-        row += 2 * (size_t)np;
-        const float2 f = make_float2((float)fla, (float)flb);
-        float2 B0 = __ffma2_rn(f, make_float2(R.btq, R.btq),
-                               __ffma2_rn(fi, make_float2(R.dB, R.dB), make_float2(R.Be0, R.Be0)));
-        B0 = make_float2(fmaxf(B0.x, 1e-30f), fmaxf(B0.y, 1e-30f));  // rays that miss: keep finite
-        fi = __fadd2_rn(fi, make_float2(2.0f, 2.0f));
-        float2 z11 = __ffma2_rn(f, make_float2(R.bqs, R.bqs), make_float2(R.z0c, R.z0c));
-        z11 = __ffma2_rn(make_float2(0.5f, 0.5f), B0, z11);
-        const float2 z21_0 = __fadd2_rn(z11, make_float2(-R.A, -R.A));
-        const float2 w1_0 = __ffma2_rn(neg2(B0), make_float2(R.invC, R.invC), make_float2(1.0f, 1.0f));
-        float ca[K], cb[K];
+    const float2 AC = make_float2(-R.A * R.invC, -R.A * R.invC);
+    const float dzC = R.dz * R.invC, dzC2 = dzC - R.tq * R.invC, dr = R.tq - R.dz;
+    for (int i = i0; i <= i1;) {
+        float2 acc = make_float2(0.0f, 0.0f);
+        const int iend = min(i1, i + 31);  // FP32 partial sums over <= 16 line pairs
+        for (; i <= iend; i += 2) {
+            // line a = i, line b = i + 1
+            const uint32_t fla = flo;
+            const int32_t ha = fhi;
+            uint32_t flb;
+            int32_t hb;
+            asm("add.cc.u32 %0, %2, %3;\n\taddc.s32 %1, %4, %5;"
+                : "=r"(flb), "=r"(hb) : "r"(flo), "r"(R.mlo), "r"(fhi), "r"(R.mhi));
+            asm("add.cc.u32 %0, %2, %3;\n\taddc.s32 %1, %4, %5;"
+                : "=r"(flo), "=r"(fhi) : "r"(flb), "r"(R.mlo), "r"(hb), "r"(R.mhi));
+            // first candidate (clamped into the zero border when the ray misses the line)
+            const int qa = min(max(ha + 1, -P), qmax), qb = min(max(hb + 1, -P), qmax);
+            const float* pa = row + qa;
+            const float* pb = row + np + qb;
+            row += 2 * (size_t)np;
+            float ca[K], cb[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            ca[k] = __ldg(pa + k);
-            cb[k] = __ldg(pb + k);
-        }
+            for (int k = 0; k < K; ++k) {
+                ca[k] = __ldg(pa + k);
+                cb[k] = __ldg(pb + k);
+            }
+            const float2 f = make_float2((float)fla, (float)flb);
+            float2 B0 = __ffma2_rn(f, make_float2(R.btq, R.btq),
+                                   __ffma2_rn(fi, make_float2(R.dB, R.dB), make_float2(R.Be0, R.Be0)));
+            B0 = make_float2(fmaxf(B0.x, 1e-30f), fmaxf(B0.y, 1e-30f));  // rays that miss: keep finite
+            fi = __fadd2_rn(fi, make_float2(2.0f, 2.0f));
+            float2 z0 = __ffma2_rn(f, make_float2(R.bqs, R.bqs), make_float2(R.z0c, R.z0c));
+            z0 = __ffma2_rn(make_float2(0.5f, 0.5f), B0, z0);                       // z11
+            const float2 r0 = __fadd2_rn(__fadd2_rn(B0, make_float2(R.A, R.A)), neg2(z0));  // A + B - z11
+            const float2 u11 = __ffma2_rn(z0, make_float2(R.invC, R.invC), make_float2(1.0f, 1.0f));
+            const float2 u12 = __ffma2_rn(neg2(B0), make_float2(R.invC, R.invC), u11);
+            const float2 u21 = __fadd2_rn(u11, AC), u22 = __fadd2_rn(u12, AC);
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const float2 kk = make_float2((float)k, (float)k);
-            const float2 zz11 = k ? __ffma2_rn(kk, make_float2(R.dz, R.dz), z11) : z11;
-            const float2 zz21 = k ? __ffma2_rn(kk, make_float2(R.dz, R.dz), z21_0) : z21_0;
-            const float2 B = k ? __ffma2_rn(kk, make_float2(R.tq, R.tq), B0) : B0;
-            const float2 w1 = k ? __ffma2_rn(kk, make_float2(R.mtqc, R.mtqc), w1_0) : w1_0;
-            const float2 num = cnsf_num2(zz11, zz21, B, w1, R.A, R.invC, R.hC);
-            const float2 cw = __fmul2_rn(make_float2(ca[k], cb[k]), rcp2(B));
-            acc = __ffma2_rn(cw, num, acc);
+            for (int k = 0; k < K; ++k) {
+                const float kf = (float)k;
+                const float2 kk = make_float2(kf, kf);
+                const float2 z11 = k ? __ffma2_rn(kk, make_float2(R.dz, R.dz), z0) : z0;
+                const float2 r = k ? __ffma2_rn(kk, make_float2(dr, dr), r0) : r0;
+                const float2 B = k ? __ffma2_rn(kk, make_float2(R.tq, R.tq), B0) : B0;
+                const float2 t11 = make_float2(sat_fma(kf, dzC, u11.x), sat_fma(kf, dzC, u11.y));
+                const float2 t12 = make_float2(sat_fma(kf, dzC2, u12.x), sat_fma(kf, dzC2, u12.y));
+                const float2 t21 = make_float2(sat_fma(kf, dzC, u21.x), sat_fma(kf, dzC, u21.y));
+                const float2 t22 = make_float2(sat_fma(kf, dzC2, u22.x), sat_fma(kf, dzC2, u22.y));
+                float2 T = __fmul2_rn(t11, t11);
+                T = __ffma2_rn(neg2(t12), t12, T);
+                T = __ffma2_rn(neg2(t21), t21, T);
+                T = __ffma2_rn(t22, t22, T);
+                const float ma = MAB == 1 ? B.x : (MAB == 2 ? R.A : fminf(R.A, B.x));
+                const float mb = MAB == 1 ? B.y : (MAB == 2 ? R.A : fminf(R.A, B.y));
+                const float2 M2 = make_float2(fmaxf(fmin3(z11.x, ma, r.x), 0.0f),
+                                              fmaxf(fmin3(z11.y, mb, r.y), 0.0f));
+                const float2 num = __ffma2_rn(make_float2(R.hC, R.hC), T, M2);
+                const float2 cw = __fmul2_rn(make_float2(ca[k], cb[k]), rcp2(B));
+                acc = __ffma2_rn(cw, num, acc);
+            }
         }
-        if (++iter == 16) {  // two-level accumulation: FP32 partials, FP64 total
-            dacc += (double)acc.x + (double)acc.y;
-            acc = make_float2(0.0f, 0.0f);
-            iter = 0;
-        }
+        dacc += (double)acc.x + (double)acc.y;  // two-level accumulation
     }
-    return dacc + (double)acc.x + (double)acc.y;
+    return dacc;
+}
+
+template <int K>
+__device__ __forceinline__ double fp_walk_k(const FPRay& R, int mab, int i0, int i1, int n, int np, int P)
+{
+    if (mab == 1) return fp_walk<K, 1>(R, i0, i1, n, np, P);
+    if (mab == 2) return fp_walk<K, 2>(R, i0, i1, n, np, P);
+    return fp_walk<K, 0>(R, i0, i1, n, np, P);
 }
 
 // generic K (wide bins relative to pixels): same arithmetic, runtime trip count
@@ -275,13 +304,21 @@ __global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
         R.hC = 0.5f * Cf;
         R.mtqc = -R.tq * R.invC;
         R.base = (rows_major ? P.pad : P.padT) + (size_t)b * P.np * P.np;
+        // is min(A, tau') decided along the whole ray?  tau' = g d with d affine
+        // over the image: its extremes are at the image corners
+        double dmin = D00;
+        dmin = fmin(dmin, D00 + (n - 1) * dcol);
+        dmin = fmin(dmin, D00 + (n - 1) * drow);
+        dmin = fmin(dmin, D00 + (n - 1) * (dcol + drow));
+        const int mab_t = gj * dmax * (1.0 + 1e-6) < A ? 1 : (gj * dmin * (1.0 - 1e-6) > A ? 2 : 0);
+        const int mab = __all_sync(0xffffffffu, mab_t == 1) ? 1 : (__all_sync(0xffffffffu, mab_t == 2) ? 2 : 0);
         switch (Kw) {
-            case 1: acc = fp_walk<1>(R, wlo, whi, n, P.np, P.P); break;
-            case 2: acc = fp_walk<2>(R, wlo, whi, n, P.np, P.P); break;
-            case 3: acc = fp_walk<3>(R, wlo, whi, n, P.np, P.P); break;
-            case 4: acc = fp_walk<4>(R, wlo, whi, n, P.np, P.P); break;
-            case 5: acc = fp_walk<5>(R, wlo, whi, n, P.np, P.P); break;
-            case 6: acc = fp_walk<6>(R, wlo, whi, n, P.np, P.P); break;
+            case 1: acc = fp_walk_k<1>(R, mab, wlo, whi, n, P.np, P.P); break;
+            case 2: acc = fp_walk_k<2>(R, mab, wlo, whi, n, P.np, P.P); break;
+            case 3: acc = fp_walk_k<3>(R, mab, wlo, whi, n, P.np, P.P); break;
+            case 4: acc = fp_walk_k<4>(R, mab, wlo, whi, n, P.np, P.P); break;
+            case 5: acc = fp_walk_k<5>(R, mab, wlo, whi, n, P.np, P.P); break;
+            case 6: acc = fp_walk_k<6>(R, mab, wlo, whi, n, P.np, P.P); break;
             default: acc = fp_walk_generic(R, Kw, wlo, whi, n, P.np, P.P); break;
         }
         acc *= h * h / A;  // W = (h^2 / A) num / B
