@@ -37,6 +37,7 @@ WORKLOADS = {
     "1": "config1: 64x64 Shepp-Logan, 90 views, 128 bins, SID 500 / SDD 1000 mm",
     "2": "config2: 512x512 Shepp-Logan, 720 views, 1024 bins, SID 500 / SDD 1000 mm",
     "3": "config3: 1024x1024 Shepp-Logan, 1440 views, 2048 bins, SID 500 / SDD 1000 mm",
+    "4": "config4: batch of 64 512x512 jittered Shepp-Logan slices, 720 views, 1024 bins",
 }
 
 
@@ -53,6 +54,7 @@ def parse():
 
 
 def weight_counts(cfg: str):
+    cfg = {"4": "2"}.get(cfg, cfg)  # config 4 = 64 slices in the geometry of config 2
     path = os.path.join(ROOT, "tests", "golden", "weight_counts.json")
     try:
         return json.load(open(path))[cfg]["per_view"]
@@ -218,9 +220,12 @@ def main():
     v0, nv = view_shard(g["n_views"], rank, world)
     n, ns = g["n"], g["n_det"]
 
-    img = torch.from_numpy(W.shepp_logan(n)).to(dev)
-    sino = torch.empty((nv, ns), dtype=torch.float32, device=dev)
-    out = torch.empty((n, n), dtype=torch.float32, device=dev)
+    batch = W.BATCH[args.config]
+    host_img = W.shepp_logan(n) if batch == 1 else W.jittered_batch(n, batch, seed=7)
+    img = torch.from_numpy(host_img).to(dev)
+    bshape = () if batch == 1 else (batch,)
+    sino = torch.empty(bshape + (nv, ns), dtype=torch.float32, device=dev)
+    out = torch.empty(bshape + (n, n), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -268,7 +273,7 @@ def main():
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     total_ms = float(tot.item())
-    value = args.steps / (total_ms * 1e-3)
+    value = args.steps * batch / (total_ms * 1e-3)  # FP+BP pairs (one per slice) per second
 
     # ---- roofline of the dominant kernel (ALU / FP32-pipe bound)
     counts = weight_counts(args.config)
@@ -280,7 +285,7 @@ def main():
     fp_avg, bp_avg = statistics.mean(fp_ms), statistics.mean(bp_ms)
     kernels = {}
     for name, ms in (("fp", fp_avg), ("bp", bp_avg)):
-        ach = nw * FLOPS_PER_WEIGHT / (ms * 1e-3) / 1e12 if nw else None
+        ach = nw * batch * FLOPS_PER_WEIGHT / (ms * 1e-3) / 1e12 if nw else None
         kernels[name] = {"ms": ms, "tflops": ach, "frac": ach / peak_tflops if ach else None,
                          "weights_per_launch": nw}
     dom = "bp" if bp_avg >= fp_avg else "fp"
@@ -290,16 +295,16 @@ def main():
             "traffic": traffic,
             "peak_basis": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 flop x "
                           f"{sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
-            "work": f"{nw} nonzero weights x {FLOPS_PER_WEIGHT} flop per launch",
-            "hbm_gbs_algorithmic": 4 * (n * n + nv * ns) / (ms_to_s(statistics.mean(step_ms))) / 1e9}
+            "work": f"{nw} nonzero weights x {batch} slices x {FLOPS_PER_WEIGHT} flop per launch",
+            "hbm_gbs_algorithmic": 4 * batch * (n * n + nv * ns) / (ms_to_s(statistics.mean(step_ms))) / 1e9}
 
     # ---- end to end through the C ABI with host buffers (pinned)
     e2e = None
     if not args.no_e2e:
-        h_img = torch.from_numpy(W.shepp_logan(n)).pin_memory()
-        h_sino = torch.empty((nv, ns), dtype=torch.float32).pin_memory()
-        h_out = torch.empty((n, n), dtype=torch.float32).pin_memory()
-        d_out = torch.empty((n, n), dtype=torch.float32, device=dev)
+        h_img = torch.from_numpy(host_img).pin_memory()
+        h_sino = torch.empty(bshape + (nv, ns), dtype=torch.float32).pin_memory()
+        h_out = torch.empty(bshape + (n, n), dtype=torch.float32).pin_memory()
+        d_out = torch.empty(bshape + (n, n), dtype=torch.float32, device=dev)
         ke = max(3, min(args.steps, 50))
 
         def e2e_step():
@@ -326,14 +331,14 @@ def main():
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": ke / (float(et.item()) * 1e-3), "unit": "pairs/s",
-               "h2d_bytes_per_step": 4 * (n * n + nv * ns),
-               "d2h_bytes_per_step": 4 * (nv * ns + n * n),
+        e2e = {"value": ke * batch / (float(et.item()) * 1e-3), "unit": "pairs/s",
+               "h2d_bytes_per_step": 4 * batch * (n * n + nv * ns),
+               "d2h_bytes_per_step": 4 * batch * (nv * ns + n * n),
                "path": "cbp_forward/cbp_back with pinned host buffers (library staging)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.config)
+        cpu = cpu_baseline(args.config)  # per slice: the oracle has no batch sharing
 
     if rank == 0:
         line = {
@@ -343,7 +348,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config], "n": n, "n_views": g["n_views"],
                        "n_det": ns, "pixel_mm": g["pixel"], "det_pitch_mm": g["det_pitch"],
-                       "sid_mm": g["sid"], "sdd_mm": g["sdd"], "batch": 1,
+                       "sid_mm": g["sid"], "sdd_mm": g["sdd"], "batch": batch,
                        "parallelism": f"views/{world}" if world > 1 else "single",
                        "l2": "flushed between steps (256 MiB write, outside the timed events)"},
             "roofline": roof,

@@ -235,19 +235,21 @@ int fp_pad_width(const cbp_geometry_t& g)
     return (int)std::floor(2.0 * sigq) + 2;
 }
 
-int launch_fp(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
-              int32_t batch, int32_t v0, int32_t nv, cudaStream_t stream)
+template <int S>
+int launch_fp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
+                int32_t batch, int32_t v0, int32_t nv, cudaStream_t stream)
 {
     const int P = fp_pad_width(g);
     const int np = g.n + 2 * P;
-    const size_t plane = (size_t)np * np;
+    const int G = (batch + S - 1) / S;
+    const size_t plane = (size_t)np * np * S * G;
     float* pad = nullptr;
-    int rc = scratch_alloc((void**)&pad, sizeof(float) * 2 * plane * batch, stream);
+    int rc = scratch_alloc((void**)&pad, sizeof(float) * 2 * plane, stream);
     if (rc != CBP_OK) return rc;
-    float* padT = pad + plane * batch;
-    dim3 pgrid((np + cbp::PAD_TILE - 1) / cbp::PAD_TILE, (np + cbp::PAD_TILE - 1) / cbp::PAD_TILE,
-               batch);
-    cbp::cbp_pad_kernel<<<pgrid, dim3(cbp::PAD_TILE, 8), 0, stream>>>(img, pad, padT, g.n, P, np);
+    float* padT = pad + plane;
+    dim3 pgrid((np + cbp::PAD_TILE - 1) / cbp::PAD_TILE, (np + cbp::PAD_TILE - 1) / cbp::PAD_TILE, G);
+    cbp::cbp_pad_kernel<S><<<pgrid, dim3(cbp::PAD_TILE, 8), 0, stream>>>(img, pad, padT, g.n, P, np,
+                                                                         batch);
     ++g_launches;
     cbp::FPParams Pm;
     Pm.g = to_dev(g);
@@ -259,33 +261,46 @@ int launch_fp(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, f
     Pm.sino = sino;
     Pm.view_begin = v0;
     Pm.view_count = nv;
-    dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, nv, batch);
-    cbp::cbp_fp_kernel<<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
+    Pm.batch = batch;
+    dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, nv, G);
+    cbp::cbp_fp_kernel<S><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
     ++g_launches;
     rc = cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
     cudaFreeAsync(pad, stream);
     return rc;
 }
 
-// number of view groups the BP splits the views into (one CTA per tile and
-// group): about 6 waves of 2 CTAs per SM, at least 8 views per group.
-int bp_groups(const cbp_geometry_t& g, int32_t batch, int32_t nv, int sms)
+// slices per thread: the weight of a (view, bin, pixel) is computed once and
+// applied to S images of the batch
+int launch_fp(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
+              int32_t batch, int32_t v0, int32_t nv, cudaStream_t stream)
+{
+    if (batch >= 4) return launch_fp_s<4>(g, t, img, sino, batch, v0, nv, stream);
+    if (batch >= 2) return launch_fp_s<2>(g, t, img, sino, batch, v0, nv, stream);
+    return launch_fp_s<1>(g, t, img, sino, batch, v0, nv, stream);
+}
+
+// number of view groups the BP splits the views into (one CTA per tile,
+// group and slice group): about 12 CTAs per SM, at least 8 views per group.
+int bp_groups(const cbp_geometry_t& g, int32_t slice_groups, int32_t nv, int sms)
 {
     const int tiles = ((g.n + cbp::BP_TILE - 1) / cbp::BP_TILE) * ((g.n + cbp::BP_TILE - 1) / cbp::BP_TILE);
     const double target = 12.0 * sms;
-    int G = (int)std::lround(target / ((double)tiles * batch));
+    int G = (int)std::lround(target / ((double)tiles * slice_groups));
     G = std::max(1, std::min(G, std::max(1, nv / 8)));
     const int vpg = (nv + G - 1) / G;
     return (nv + vpg - 1) / vpg;
 }
 
-int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
-              int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream)
+template <int S>
+int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
+                int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream)
 {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int G = bp_groups(g, batch, nv, sms);
+    const int SG = (batch + S - 1) / S;
+    const int G = bp_groups(g, SG, nv, sms);
     const int vpg = (nv + G - 1) / G;
     const size_t plane = (size_t)g.n * g.n;
     float* part = nullptr;
@@ -309,14 +324,18 @@ int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, 
     P.batch = batch;
     P.accumulate = accumulate ? 1 : 0;
     const int tiles = (g.n + cbp::BP_TILE - 1) / cbp::BP_TILE;
-    dim3 grid(tiles, tiles, G * batch);
+    dim3 grid(tiles, tiles, G * SG);
+    const size_t smem = cbp::bp_smem_bytes(S);
+    static std::once_flag attr[64];
+    std::call_once(attr[dev & 63], [smem] {
+        cudaFuncSetAttribute(cbp::cbp_bp_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    });
 #ifdef CBP_DEBUG_CHECKS
-    const char* skip = getenv("CBP_DEBUG_SKIP");
-    fprintf(stderr, "launch_bp G=%d vpg=%d grid=%d,%d,%d part=%p img=%p sino=%p\n", G, vpg, grid.x,
-            grid.y, grid.z, (void*)part, (void*)img, (const void*)sino);
-    if (!(skip && skip[0] == '1'))
+    fprintf(stderr, "launch_bp S=%d G=%d vpg=%d grid=%d,%d,%d smem=%zu\n", S, G, vpg, grid.x, grid.y,
+            grid.z, smem);
 #endif
-    cbp::cbp_bp_kernel<<<grid, cbp::BP_THREADS, 0, stream>>>(P);
+    cbp::cbp_bp_kernel<S><<<grid, cbp::BP_THREADS, smem, stream>>>(P);
     ++g_launches;
 #ifdef CBP_DEBUG_CHECKS
     fprintf(stderr, "bp kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
@@ -326,12 +345,17 @@ int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, 
         const int blocks = (int)std::min<size_t>((count + 255) / 256, (size_t)sms * 8);
         cbp::cbp_reduce_kernel<<<blocks, 256, 0, stream>>>(part, img, count, G, accumulate ? 1 : 0);
         ++g_launches;
-#ifdef CBP_DEBUG_CHECKS
-        fprintf(stderr, "reduce kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
-#endif
         cudaFreeAsync(part, stream);
     }
     return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+}
+
+int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
+              int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream)
+{
+    if (batch >= 4) return launch_bp_s<4>(g, t, sino, img, batch, v0, nv, accumulate, stream);
+    if (batch >= 2) return launch_bp_s<2>(g, t, sino, img, batch, v0, nv, accumulate, stream);
+    return launch_bp_s<1>(g, t, sino, img, batch, v0, nv, accumulate, stream);
 }
 
 }  // namespace

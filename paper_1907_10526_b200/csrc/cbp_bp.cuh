@@ -171,8 +171,9 @@ __device__ void bp_build_entry(const GeomDev& g, const Tables& t, const BPHeader
     E.c = make_float4(A, 1.0f / C, 0.5f * C, y * (h * h / A));
 }
 
-// one entry, one pixel pair (lane b = lane a + one pixel along the pair axis)
-__device__ __forceinline__ float2 bp_eval(const BPEntry* e, float dc, float dr, float2 acc)
+// one entry, one pixel pair (lane b = lane a + one pixel along the pair axis):
+// returns num / tau' for both pixels (the weight without the h^2/A factor)
+__device__ __forceinline__ float2 bp_weight(const BPEntry* e, float dc, float dr)
 {
     const float4 ea = e->a, eb = e->b, ec = e->c;
     const float za = fmaf(dr, ea.z, fmaf(dc, ea.y, ea.x));
@@ -182,42 +183,84 @@ __device__ __forceinline__ float2 bp_eval(const BPEntry* e, float dc, float dr, 
     const float2 z21 = __fadd2_rn(z11, make_float2(-ec.x, -ec.x));
     const float2 w1 = __ffma2_rn(neg2(B), make_float2(ec.y, ec.y), make_float2(1.0f, 1.0f));
     const float2 num = cnsf_num2(z11, z21, B, w1, ec.x, ec.y, ec.z);
-    return __ffma2_rn(__fmul2_rn(make_float2(ec.w, ec.w), rcp2(B)), num, acc);
+    return __fmul2_rn(num, rcp2(B));
 }
 
 // entries row[jl - base .. jh - base]; empty when jh < jl (no pointer is
-// formed outside the row: the trip count is an integer)
-__device__ __forceinline__ float2 bp_pair(const BPEntry* row, int jl, int jh, int base, float dc,
-                                          float dr, float2 acc)
+// formed outside the row: the trip count is an integer).  S slices: the
+// y h^2/A of slice q is ys[entry * S + q] (S > 1) or entry.c.w (S == 1).
+template <int S>
+__device__ __forceinline__ void bp_pair(const BPEntry* row, const float* yrow, int jl, int jh,
+                                        int base, float dc, float dr, float2 (&acc)[S])
 {
-    if (jh < jl) return acc;
+    if (jh < jl) return;
     CBP_CHECK(jl >= base && jh - base < BP_NB, "bp_pair jl=%d jh=%d base=%d\n", jl, jh, base);
     const int cnt = jh - jl + 1;
     const BPEntry* e = row + (jl - base);
-    for (int k = 0; k < cnt; ++k, ++e) acc = bp_eval(e, dc, dr, acc);
-    return acc;
+    const float* ys = yrow + (jl - base) * S;
+    for (int k = 0; k < cnt; ++k, ++e, ys += S) {
+        const float2 w = bp_weight(e, dc, dr);
+        if constexpr (S == 1) {
+            const float yw = e->c.w;
+            acc[0] = __ffma2_rn(make_float2(yw, yw), w, acc[0]);
+        } else if constexpr (S == 2) {
+            const float2 y2 = *reinterpret_cast<const float2*>(ys);
+            acc[0] = __ffma2_rn(make_float2(y2.x, y2.x), w, acc[0]);
+            acc[1] = __ffma2_rn(make_float2(y2.y, y2.y), w, acc[1]);
+        } else {
+            static_assert(S % 4 == 0, "S is 1, 2 or a multiple of 4");
+#pragma unroll
+            for (int q = 0; q < S; q += 4) {
+                const float4 y4 = *reinterpret_cast<const float4*>(ys + q);
+                acc[q] = __ffma2_rn(make_float2(y4.x, y4.x), w, acc[q]);
+                if (q + 1 < S) acc[q + 1] = __ffma2_rn(make_float2(y4.y, y4.y), w, acc[q + 1]);
+                if (q + 2 < S) acc[q + 2] = __ffma2_rn(make_float2(y4.z, y4.z), w, acc[q + 2]);
+                if (q + 3 < S) acc[q + 3] = __ffma2_rn(make_float2(y4.w, y4.w), w, acc[q + 3]);
+            }
+        }
+    }
 }
 
-__device__ __forceinline__ void bp_flush(double (*acc_s)[BP_TILE + 1], int horiz, int e0, int e1,
-                                         float2 a0, float2 a1)
+template <int S>
+__device__ __forceinline__ void bp_flush(double* acc_s, int horiz, int e0, int e1, float2 (&a0)[S],
+                                         float2 (&a1)[S])
 {
-    const int r0 = e0 >> 5, c0 = e0 & 31, r1 = e1 >> 5, c1 = e1 & 31;
-    acc_s[r0][c0] += (double)a0.x;
-    acc_s[r0 + !horiz][c0 + horiz] += (double)a0.y;
-    acc_s[r1][c1] += (double)a1.x;
-    acc_s[r1 + !horiz][c1 + horiz] += (double)a1.y;
+    constexpr int LD = BP_TILE + 1, PL = BP_TILE * LD;
+    const int i0 = (e0 >> 5) * LD + (e0 & 31), i1 = (e1 >> 5) * LD + (e1 & 31);
+    const int st = horiz ? 1 : LD;  // second pixel of a pair
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+        acc_s[q * PL + i0] += (double)a0[q].x;
+        acc_s[q * PL + i0 + st] += (double)a0[q].y;
+        acc_s[q * PL + i1] += (double)a1[q].x;
+        acc_s[q * PL + i1 + st] += (double)a1[q].y;
+        a0[q] = a1[q] = make_float2(0.f, 0.f);
+    }
 }
 
-__global__ void __launch_bounds__(BP_THREADS, 4) cbp_bp_kernel(const BPParams P)
+// dynamic shared memory of the BP kernel for S slices
+__host__ __device__ constexpr size_t bp_smem_bytes(int S)
 {
-    __shared__ BPEntry tab[BP_VC][BP_NB];
-    __shared__ BPHeader hdr[BP_VC];
-    __shared__ double acc_s[BP_TILE][BP_TILE + 1];
+    return sizeof(BPEntry) * BP_VC * BP_NB + sizeof(BPHeader) * BP_VC +
+           (S > 1 ? sizeof(float) * BP_VC * BP_NB * S : 0) +
+           sizeof(double) * S * BP_TILE * (BP_TILE + 1);
+}
+
+template <int S>
+__global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : 2) cbp_bp_kernel(const BPParams P)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    BPEntry(*tab)[BP_NB] = reinterpret_cast<BPEntry(*)[BP_NB]>(smem);
+    BPHeader* hdr = reinterpret_cast<BPHeader*>(smem + sizeof(BPEntry) * BP_VC * BP_NB);
+    float* ytab = reinterpret_cast<float*>(smem + sizeof(BPEntry) * BP_VC * BP_NB +
+                                           sizeof(BPHeader) * BP_VC);  // [VC][NB][S] (S > 1)
+    double* acc_s = reinterpret_cast<double*>(smem + bp_smem_bytes(S) -
+                                              sizeof(double) * S * BP_TILE * (BP_TILE + 1));
 
     const GeomDev& g = P.g;
     const int tid = threadIdx.x;
     const int col0 = blockIdx.x * BP_TILE, row0 = blockIdx.y * BP_TILE;
-    const int grp = blockIdx.z % P.groups, b = blockIdx.z / P.groups;
+    const int grp = blockIdx.z % P.groups, sg = blockIdx.z / P.groups;  // view group, slice group
     const int vg0 = grp * P.views_per_group;
     const int vgn = min(P.views_per_group, P.view_count - vg0);
     // anchor k_a = centre of the tile's valid pixels (clipped at the border)
@@ -225,9 +268,9 @@ __global__ void __launch_bounds__(BP_THREADS, 4) cbp_bp_kernel(const BPParams P)
     const float hcy = 0.5f * (float)(min(BP_TILE, g.n - row0) - 1);
     const double kax = ((double)col0 + hcx - g.c0) * g.h;
     const double kay = (g.c0 - (double)row0 - hcy) * g.h;
-    const float* y = P.sino + (size_t)b * P.view_count * g.n_det;
+    const size_t sino_plane = (size_t)P.view_count * g.n_det;
 
-    for (int i = tid; i < BP_TILE * BP_TILE; i += BP_THREADS) acc_s[i / BP_TILE][i % BP_TILE] = 0.0;
+    for (int i = tid; i < S * BP_TILE * (BP_TILE + 1); i += BP_THREADS) acc_s[i] = 0.0;
 
     for (int vc = 0; vc < vgn; vc += BP_VC) {
         const int nvc = min(BP_VC, vgn - vc);
@@ -243,13 +286,28 @@ __global__ void __launch_bounds__(BP_THREADS, 4) cbp_bp_kernel(const BPParams P)
                     const BPHeader& H = hdr[vi];
                     const int j = H.jlo + pass * BP_NB + jj;
                     CBP_CHECK(j > H.jhi || (j >= 0 && j < g.n_det), "entry j=%d jlo=%d jhi=%d\n", j, H.jlo, H.jhi);
-                    if (j <= H.jhi)
-                        bp_build_entry(g, P.t, H, j,
-                                       __ldg(y + (size_t)(vg0 + vc + vi) * g.n_det + j), tab[vi][jj]);
+                    if (j <= H.jhi) {
+                        const size_t yo = (size_t)(vg0 + vc + vi) * g.n_det + j;
+                        if constexpr (S == 1) {
+                            bp_build_entry(g, P.t, H, j, __ldg(P.sino + (size_t)sg * sino_plane + yo),
+                                           tab[vi][jj]);
+                        } else {
+                            bp_build_entry(g, P.t, H, j, 1.0f, tab[vi][jj]);  // c.w = h^2 / A
+                            const float hA = tab[vi][jj].c.w;
+#pragma unroll
+                            for (int q = 0; q < S; ++q) {
+                                const int b = sg * S + q;
+                                ytab[(vi * BP_NB + jj) * S + q] =
+                                    b < P.batch ? __ldg(P.sino + (size_t)b * sino_plane + yo) * hA : 0.0f;
+                            }
+                        }
+                    }
                 }
             }
             __syncthreads();
-            float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+            float2 a0[S], a1[S];
+#pragma unroll
+            for (int q = 0; q < S; ++q) a0[q] = a1[q] = make_float2(0.f, 0.f);
             int bucket = -1, horiz = 1, e0 = 0, e1 = 0;
             float2 dc0, dr0, dc1, dr1;  // pixel offsets of the two pairs (lanes a, b)
             for (int vi = 0; vi < nvc; ++vi) {
@@ -257,8 +315,7 @@ __global__ void __launch_bounds__(BP_THREADS, 4) cbp_bp_kernel(const BPParams P)
                 const int4 hi = *reinterpret_cast<const int4*>(&H.ja);  // ja, jlo, jhi, bucket
                 if (hi.w != bucket) {  // new pair order: hand the pixels back first
                     if (bucket >= 0) {
-                        bp_flush(acc_s, horiz, e0, e1, a0, a1);
-                        a0 = a1 = make_float2(0.f, 0.f);
+                        bp_flush<S>(acc_s, horiz, e0, e1, a0, a1);
                         __syncthreads();
                     }
                     bucket = hi.w;
@@ -278,6 +335,7 @@ __global__ void __launch_bounds__(BP_THREADS, 4) cbp_bp_kernel(const BPParams P)
                 const int base = hi.y + pass * BP_NB;
                 if (base > hi.z) continue;
                 const BPEntry* row = tab[vi];
+                const float* yrow = ytab + vi * BP_NB * S;
                 const float4 hf = *reinterpret_cast<const float4*>(&H.urel);  // urel, nx, ny, cW
                 const float4 hd = *reinterpret_cast<const float4*>(&H.dena);  // dena, dx, dy, -
                 const int jmax = min(hi.z, base + BP_NB - 1);
@@ -300,24 +358,28 @@ __global__ void __launch_bounds__(BP_THREADS, 4) cbp_bp_kernel(const BPParams P)
                     const int jl = max(hi.x + __float2int_rd(lo) + 1, base);
                     const int jh = min(hi.x + __float2int_ru(hi2) - 1, jmax);
                     if (p == 0)
-                        a0 = bp_pair(row, jl, jh, base, dcp.x, drp.x, a0);
+                        bp_pair<S>(row, yrow, jl, jh, base, dcp.x, drp.x, a0);
                     else
-                        a1 = bp_pair(row, jl, jh, base, dcp.x, drp.x, a1);
+                        bp_pair<S>(row, yrow, jl, jh, base, dcp.x, drp.x, a1);
                 }
             }
-            if (bucket >= 0) bp_flush(acc_s, horiz, e0, e1, a0, a1);
+            if (bucket >= 0) bp_flush<S>(acc_s, horiz, e0, e1, a0, a1);
             __syncthreads();
         }
     }
     const size_t plane = (size_t)g.n * g.n;
-    float* out = P.out + (P.groups > 1 ? ((size_t)grp * P.batch + b) : (size_t)b) * plane;
-    for (int i = tid; i < BP_TILE * BP_TILE; i += BP_THREADS) {
-        const int r = i / BP_TILE, c = i % BP_TILE;
-        const int row = row0 + r, col = col0 + c;
-        if (row < g.n && col < g.n) {
-            float* o = out + (size_t)row * g.n + col;
-            const float v = (float)acc_s[r][c];
-            *o = (P.groups == 1 && P.accumulate) ? *o + v : v;
+    for (int q = 0; q < S; ++q) {
+        const int b = sg * S + q;
+        if (b >= P.batch) break;
+        float* out = P.out + (P.groups > 1 ? ((size_t)grp * P.batch + b) : (size_t)b) * plane;
+        for (int i = tid; i < BP_TILE * BP_TILE; i += BP_THREADS) {
+            const int r = i / BP_TILE, c = i % BP_TILE;
+            const int row = row0 + r, col = col0 + c;
+            if (row < g.n && col < g.n) {
+                float* o = out + (size_t)row * g.n + col;
+                const float v = (float)acc_s[(q * BP_TILE + r) * (BP_TILE + 1) + c];
+                *o = (P.groups == 1 && P.accumulate) ? *o + v : v;
+            }
         }
     }
 }

@@ -31,42 +31,73 @@ namespace cbp {
 struct FPParams {
     GeomDev g;
     Tables t;
-    const float* pad;   // [batch][np][np] zero-padded image, pixel (r, c) at (r + P, c + P)
-    const float* padT;  // [batch][np][np] its transpose
+    // zero-padded image copies, S slices interleaved per pixel:
+    // pad [G][np][np][S], pixel (r, c) of slice g S + s at ((g np + r + P) np + c + P) S + s;
+    // padT the same with r and c swapped (G = ceil(batch / S))
+    const float* pad;
+    const float* padT;
     int np, P;          // padded side, pad width (>= max K)
     float* sino;        // [batch][view_count][n_det]
-    int view_begin, view_count;
+    int view_begin, view_count, batch;
 };
 
 constexpr int FP_BLOCK = 128;
 constexpr int FP_KMAX_UNROLLED = 6;
 
-// ---- zero-padded (and transposed) image copies ----------------------------
+// ---- zero-padded (and transposed) image copies, S slices interleaved ------
 constexpr int PAD_TILE = 32;
 
+template <int S>
 __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_kernel(const float* __restrict__ img,
                                                                float* __restrict__ pad,
                                                                float* __restrict__ padT, int n,
-                                                               int P, int np)
+                                                               int P, int np, int batch)
 {
-    __shared__ float tile[PAD_TILE][PAD_TILE + 1];
-    const int b = blockIdx.z;
+    __shared__ float tile[PAD_TILE][PAD_TILE + 1][S];
+    const int grp = blockIdx.z;
     const int r0 = blockIdx.y * PAD_TILE, c0 = blockIdx.x * PAD_TILE;
-    const float* src = img + (size_t)b * n * n;
-    float* dst = pad + (size_t)b * np * np;
-    float* dstT = padT + (size_t)b * np * np;
+    float* dst = pad + (size_t)grp * np * np * S;
+    float* dstT = padT + (size_t)grp * np * np * S;
     for (int rr = threadIdx.y; rr < PAD_TILE; rr += 8) {
         const int r = r0 + rr, c = c0 + threadIdx.x;
         const int sr = r - P, sc = c - P;
-        float v = 0.0f;
-        if (sr >= 0 && sr < n && sc >= 0 && sc < n) v = src[(size_t)sr * n + sc];
-        tile[rr][threadIdx.x] = v;
-        if (r < np && c < np) dst[(size_t)r * np + c] = v;
+        const bool in = sr >= 0 && sr < n && sc >= 0 && sc < n;
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const int b = grp * S + k;
+            const float v = (in && b < batch) ? img[((size_t)b * n + sr) * n + sc] : 0.0f;
+            tile[rr][threadIdx.x][k] = v;
+            if (r < np && c < np) dst[((size_t)r * np + c) * S + k] = v;
+        }
     }
     __syncthreads();
     for (int cc = threadIdx.y; cc < PAD_TILE; cc += 8) {
         const int c = c0 + cc, r = r0 + threadIdx.x;
-        if (r < np && c < np) dstT[(size_t)c * np + r] = tile[threadIdx.x][cc];
+        if (r < np && c < np)
+#pragma unroll
+            for (int k = 0; k < S; ++k) dstT[((size_t)c * np + r) * S + k] = tile[threadIdx.x][cc][k];
+    }
+}
+
+// S consecutive floats of one padded pixel
+template <int S>
+__device__ __forceinline__ void ld_pix(const float* p, float (&v)[S])
+{
+    if constexpr (S == 1) {
+        v[0] = __ldg(p);
+    } else if constexpr (S == 2) {
+        const float2 a = __ldg(reinterpret_cast<const float2*>(p));
+        v[0] = a.x;
+        v[1] = a.y;
+    } else {
+#pragma unroll
+        for (int q = 0; q < S; q += 4) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(p) + q / 4);
+            v[q] = a.x;
+            v[q + 1] = a.y;
+            v[q + 2] = a.z;
+            v[q + 3] = a.w;
+        }
     }
 }
 
@@ -94,19 +125,23 @@ struct FPRay {
 // four sat() arguments t.. = sat(z/C + ...) are formed directly from k
 // (u11 = z11/C + 1, u12 = u11 - tau'/C, u21 = u11 - A/C, u22 = u12 - A/C),
 // and the trapezoid bound r = A + tau' - z11 is affine in k too.
-template <int K, int MAB>
-__device__ __forceinline__ double fp_walk(const FPRay& R, int i0, int i1, int n, int np, int P)
+template <int K, int MAB, int S>
+__device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, int np, int P,
+                                        double (&out)[S])
 {
-    double dacc = 0.0;
+#pragma unroll
+    for (int q = 0; q < S; ++q) out[q] = 0.0;
     uint32_t flo = R.flo;
     int32_t fhi = R.fhi;
     const int qmax = n + P - K;
-    const float* row = R.base + (size_t)(i0 + P) * np + P;  // line i0, column 0
+    const float* row = R.base + ((size_t)(i0 + P) * np + P) * S;  // line i0, column 0
     float2 fi = make_float2((float)i0, (float)i0 + 1.0f);
     const float2 AC = make_float2(-R.A * R.invC, -R.A * R.invC);
     const float dzC = R.dz * R.invC, dzC2 = dzC - R.tq * R.invC, dr = R.tq - R.dz;
     for (int i = i0; i <= i1;) {
-        float2 acc = make_float2(0.0f, 0.0f);
+        float2 acc[S];
+#pragma unroll
+        for (int q = 0; q < S; ++q) acc[q] = make_float2(0.0f, 0.0f);
         const int iend = min(i1, i + 31);  // FP32 partial sums over <= 16 line pairs
         for (; i <= iend; i += 2) {
             // line a = i, line b = i + 1
@@ -120,15 +155,9 @@ __device__ __forceinline__ double fp_walk(const FPRay& R, int i0, int i1, int n,
                 : "=r"(flo), "=r"(fhi) : "r"(flb), "r"(R.mlo), "r"(hb), "r"(R.mhi));
             // first candidate (clamped into the zero border when the ray misses the line)
             const int qa = min(max(ha + 1, -P), qmax), qb = min(max(hb + 1, -P), qmax);
-            const float* pa = row + qa;
-            const float* pb = row + np + qb;
-            row += 2 * (size_t)np;
-            float ca[K], cb[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                ca[k] = __ldg(pa + k);
-                cb[k] = __ldg(pb + k);
-            }
+            const float* pa = row + qa * S;
+            const float* pb = row + ((size_t)np + qb) * S;
+            row += 2 * (size_t)np * S;
             const float2 f = make_float2((float)fla, (float)flb);
             float2 B0 = __ffma2_rn(f, make_float2(R.btq, R.btq),
                                    __ffma2_rn(fi, make_float2(R.dB, R.dB), make_float2(R.Be0, R.Be0)));
@@ -140,8 +169,28 @@ __device__ __forceinline__ double fp_walk(const FPRay& R, int i0, int i1, int n,
             const float2 u11 = __ffma2_rn(z0, make_float2(R.invC, R.invC), make_float2(1.0f, 1.0f));
             const float2 u12 = __ffma2_rn(neg2(B0), make_float2(R.invC, R.invC), u11);
             const float2 u21 = __fadd2_rn(u11, AC), u22 = __fadd2_rn(u12, AC);
+            // S <= 2: issue all of the line pair's loads first (more loads in flight)
+            float cpa[S <= 2 ? K : 1][S], cpb[S <= 2 ? K : 1][S];
+            if constexpr (S <= 2) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    ld_pix<S>(pa + k * S, cpa[k]);
+                    ld_pix<S>(pb + k * S, cpb[k]);
+                }
+            }
 #pragma unroll
             for (int k = 0; k < K; ++k) {
+                float ca[S], cb[S];
+                if constexpr (S <= 2) {
+#pragma unroll
+                    for (int q = 0; q < S; ++q) {
+                        ca[q] = cpa[k][q];
+                        cb[q] = cpb[k][q];
+                    }
+                } else {
+                    ld_pix<S>(pa + k * S, ca);
+                    ld_pix<S>(pb + k * S, cb);
+                }
                 const float kf = (float)k;
                 const float2 kk = make_float2(kf, kf);
                 const float2 z11 = k ? __ffma2_rn(kk, make_float2(R.dz, R.dz), z0) : z0;
@@ -160,40 +209,52 @@ __device__ __forceinline__ double fp_walk(const FPRay& R, int i0, int i1, int n,
                 const float2 M2 = make_float2(fmaxf(fmin3(z11.x, ma, r.x), 0.0f),
                                               fmaxf(fmin3(z11.y, mb, r.y), 0.0f));
                 const float2 num = __ffma2_rn(make_float2(R.hC, R.hC), T, M2);
-                const float2 cw = __fmul2_rn(make_float2(ca[k], cb[k]), rcp2(B));
-                acc = __ffma2_rn(cw, num, acc);
+                if constexpr (S == 1) {
+                    const float2 cw = __fmul2_rn(make_float2(ca[0], cb[0]), rcp2(B));
+                    acc[0] = __ffma2_rn(cw, num, acc[0]);
+                } else {  // one weight, S slices
+                    const float2 w = __fmul2_rn(num, rcp2(B));
+#pragma unroll
+                    for (int q = 0; q < S; ++q) acc[q] = __ffma2_rn(make_float2(ca[q], cb[q]), w, acc[q]);
+                }
             }
         }
-        dacc += (double)acc.x + (double)acc.y;  // two-level accumulation
+#pragma unroll
+        for (int q = 0; q < S; ++q) out[q] += (double)acc[q].x + (double)acc[q].y;  // two-level sum
     }
-    return dacc;
 }
 
-template <int K>
-__device__ __forceinline__ double fp_walk_k(const FPRay& R, int mab, int i0, int i1, int n, int np, int P)
+template <int K, int S>
+__device__ __forceinline__ void fp_walk_k(const FPRay& R, int mab, int i0, int i1, int n, int np,
+                                          int P, double (&out)[S])
 {
-    if (mab == 1) return fp_walk<K, 1>(R, i0, i1, n, np, P);
-    if (mab == 2) return fp_walk<K, 2>(R, i0, i1, n, np, P);
-    return fp_walk<K, 0>(R, i0, i1, n, np, P);
+    if (mab == 1) fp_walk<K, 1, S>(R, i0, i1, n, np, P, out);
+    else if (mab == 2) fp_walk<K, 2, S>(R, i0, i1, n, np, P, out);
+    else fp_walk<K, 0, S>(R, i0, i1, n, np, P, out);
 }
 
 // generic K (wide bins relative to pixels): same arithmetic, runtime trip count
-__device__ double fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, int np, int P)
+template <int S>
+__device__ void fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, int np, int P,
+                                double (&out)[S])
 {
-    double dacc = 0.0;
+#pragma unroll
+    for (int q = 0; q < S; ++q) out[q] = 0.0;
     uint32_t flo = R.flo;
     int32_t fhi = R.fhi;
     const int qmax = n + P - K;
     for (int i = i0; i <= i1; ++i) {
         const uint32_t fl = flo;
-        const int q = min(max(fhi + 1, -P), qmax);
+        const int qc = min(max(fhi + 1, -P), qmax);
         asm("add.cc.u32 %0, %0, %2;\n\taddc.s32 %1, %1, %3;"
             : "+r"(flo), "+r"(fhi) : "r"(R.mlo), "r"(R.mhi));
-        const float* p = R.base + (size_t)(i + P) * np + (q + P);
+        const float* p = R.base + ((size_t)(i + P) * np + (qc + P)) * S;
         const float ff = (float)fl;
         const float B0 = fmaxf(fmaf(ff, R.btq, fmaf((float)i, R.dB, R.Be0)), 1e-30f);
         const float z0 = fmaf(0.5f, B0, fmaf(ff, R.bqs, R.z0c));
-        float part = 0.0f;
+        float part[S];
+#pragma unroll
+        for (int q = 0; q < S; ++q) part[q] = 0.0f;
         for (int k = 0; k < K; ++k) {
             const float kf = (float)k;
             const float z11 = fmaf(kf, R.dz, z0);
@@ -202,13 +263,18 @@ __device__ double fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, 
             const float w1 = fmaf(-B, R.invC, 1.0f);
             const float2 num = cnsf_num2(make_float2(z11, z11), make_float2(z21, z21),
                                          make_float2(B, B), make_float2(w1, w1), R.A, R.invC, R.hC);
-            part = fmaf(__ldg(p + k) * rcp_approx(B), num.x, part);
+            const float w = num.x * rcp_approx(B);
+            float c[S];
+            ld_pix<S>(p + k * S, c);
+#pragma unroll
+            for (int q = 0; q < S; ++q) part[q] = fmaf(c[q], w, part[q]);
         }
-        dacc += (double)part;
+#pragma unroll
+        for (int q = 0; q < S; ++q) out[q] += (double)part[q];
     }
-    return dacc;
 }
 
+template <int S>
 __global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
 {
     const GeomDev& g = P.g;
@@ -216,7 +282,7 @@ __global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
     const bool valid = jr < g.n_det;
     const int j = valid ? jr : g.n_det - 1;
     const int vl = blockIdx.y;
-    const int b = blockIdx.z;
+    const int grp = blockIdx.z;  // slices grp S .. grp S + S - 1
     const int v = P.view_begin + vl;
     const int n = g.n;
 
@@ -278,8 +344,9 @@ __global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
     const int whi = __reduce_max_sync(0xffffffffu, ihi);
     const int Kw = __reduce_max_sync(0xffffffffu, K);
 
-    double acc = 0.0;
-    if (Kw > P.P) acc = __longlong_as_double(0x7ff8000000000000ll);  // pad too thin: fail loudly (NaN)
+    double acc[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) acc[q] = Kw > P.P ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;  // pad too thin: NaN
     if (wlo <= whi && Kw <= P.P) {
         FPRay R;
         // lower support edge on line i: q*(i) - sig_q, as 32.32 fixed point from line wlo
@@ -303,7 +370,7 @@ __global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
         R.invC = 1.0f / Cf;  // +inf for C == 0: handled by sat()
         R.hC = 0.5f * Cf;
         R.mtqc = -R.tq * R.invC;
-        R.base = (rows_major ? P.pad : P.padT) + (size_t)b * P.np * P.np;
+        R.base = (rows_major ? P.pad : P.padT) + (size_t)grp * P.np * P.np * S;
         // is min(A, tau') decided along the whole ray?  tau' = g d with d affine
         // over the image: its extremes are at the image corners
         double dmin = D00;
@@ -313,17 +380,23 @@ __global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
         const int mab_t = gj * dmax * (1.0 + 1e-6) < A ? 1 : (gj * dmin * (1.0 - 1e-6) > A ? 2 : 0);
         const int mab = __all_sync(0xffffffffu, mab_t == 1) ? 1 : (__all_sync(0xffffffffu, mab_t == 2) ? 2 : 0);
         switch (Kw) {
-            case 1: acc = fp_walk_k<1>(R, mab, wlo, whi, n, P.np, P.P); break;
-            case 2: acc = fp_walk_k<2>(R, mab, wlo, whi, n, P.np, P.P); break;
-            case 3: acc = fp_walk_k<3>(R, mab, wlo, whi, n, P.np, P.P); break;
-            case 4: acc = fp_walk_k<4>(R, mab, wlo, whi, n, P.np, P.P); break;
-            case 5: acc = fp_walk_k<5>(R, mab, wlo, whi, n, P.np, P.P); break;
-            case 6: acc = fp_walk_k<6>(R, mab, wlo, whi, n, P.np, P.P); break;
-            default: acc = fp_walk_generic(R, Kw, wlo, whi, n, P.np, P.P); break;
+            case 1: fp_walk_k<1, S>(R, mab, wlo, whi, n, P.np, P.P, acc); break;
+            case 2: fp_walk_k<2, S>(R, mab, wlo, whi, n, P.np, P.P, acc); break;
+            case 3: fp_walk_k<3, S>(R, mab, wlo, whi, n, P.np, P.P, acc); break;
+            case 4: fp_walk_k<4, S>(R, mab, wlo, whi, n, P.np, P.P, acc); break;
+            case 5: fp_walk_k<5, S>(R, mab, wlo, whi, n, P.np, P.P, acc); break;
+            case 6: fp_walk_k<6, S>(R, mab, wlo, whi, n, P.np, P.P, acc); break;
+            default: fp_walk_generic<S>(R, Kw, wlo, whi, n, P.np, P.P, acc); break;
         }
-        acc *= h * h / A;  // W = (h^2 / A) num / B
+#pragma unroll
+        for (int q = 0; q < S; ++q) acc[q] *= h * h / A;  // W = (h^2 / A) num / B
     }
-    if (valid) P.sino[((size_t)b * P.view_count + vl) * g.n_det + j] = (float)acc;
+    if (valid)
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+            const int b = grp * S + q;
+            if (b < P.batch) P.sino[((size_t)b * P.view_count + vl) * g.n_det + j] = (float)acc[q];
+        }
 }
 
 }  // namespace cbp
