@@ -280,16 +280,29 @@ int launch_fp(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, f
     return launch_fp_s<1>(g, t, img, sino, batch, v0, nv, stream);
 }
 
-// number of view groups the BP splits the views into (one CTA per tile,
-// group and slice group): about 12 CTAs per SM, at least 8 views per group.
-int bp_groups(const cbp_geometry_t& g, int32_t slice_groups, int32_t nv, int sms)
+// Number of view groups the BP splits the views into (one CTA per tile,
+// view group and slice group).  The grid should fill whole waves of the
+// resident CTA slots (the last wave of a ragged grid runs mostly idle) and
+// have >= 4 waves for dynamic load balance; each group has >= 8 views and the
+// partial images (G per slice, summed by cbp_reduce_kernel) are capped at
+// 32 / slice_groups per slice.
+int bp_groups(const cbp_geometry_t& g, int32_t slice_groups, int32_t nv, int slots)
 {
     const int tiles = ((g.n + cbp::BP_TILE - 1) / cbp::BP_TILE) * ((g.n + cbp::BP_TILE - 1) / cbp::BP_TILE);
-    const double target = 12.0 * sms;
-    int G = (int)std::lround(target / ((double)tiles * slice_groups));
-    G = std::max(1, std::min(G, std::max(1, nv / 8)));
-    const int vpg = (nv + G - 1) / G;
-    return (nv + vpg - 1) / vpg;
+    const int gmax = std::max(1, std::min(std::min(nv / 8, 64), 32 / std::max(1, (int)slice_groups)));
+    int best = 1;
+    double best_score = -1.0;
+    for (int G = 1; G <= gmax; ++G) {
+        const int vpg = (nv + G - 1) / G;
+        const int Geff = (nv + vpg - 1) / vpg;
+        const double waves = (double)tiles * Geff * slice_groups / slots;
+        const double score = std::min(1.0, waves / 4.0) * waves / std::ceil(waves);
+        if (score > best_score + 1e-9) {
+            best_score = score;
+            best = Geff;
+        }
+    }
+    return best;
 }
 
 template <int S>
@@ -300,7 +313,19 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int SG = (batch + S - 1) / S;
-    const int G = bp_groups(g, SG, nv, sms);
+    const size_t smem = cbp::bp_smem_bytes(S);
+    static std::once_flag attr[64];
+    static int per_sm[64];
+    std::call_once(attr[dev & 63], [smem, dev] {
+        cudaFuncSetAttribute(cbp::cbp_bp_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        int k = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_bp_kernel<S>, cbp::BP_THREADS,
+                                                          smem) != cudaSuccess || k < 1)
+            k = 1;
+        per_sm[dev & 63] = k;
+    });
+    const int G = bp_groups(g, SG, nv, sms * per_sm[dev & 63]);
     const int vpg = (nv + G - 1) / G;
     const size_t plane = (size_t)g.n * g.n;
     float* part = nullptr;
@@ -313,6 +338,16 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
         if (part) cudaFreeAsync(part, stream);
         return CBP_ECUDA;
     }
+    const int tiles = (g.n + cbp::BP_TILE - 1) / cbp::BP_TILE;
+    cbp::BPHeader* hdrs = nullptr;
+    if (scratch_alloc((void**)&hdrs, sizeof(cbp::BPHeader) * tiles * tiles * nv, stream) != CBP_OK) {
+        if (part) cudaFreeAsync(part, stream);
+        return CBP_ECUDA;
+    }
+    cbp::cbp_bp_header_kernel<<<dim3(tiles * tiles, (nv + 127) / 128), 128, 0, stream>>>(
+        to_dev(g), t, v0, nv, tiles, hdrs);
+    ++g_launches;
+    P.hdrs = hdrs;
     P.g = to_dev(g);
     P.t = t;
     P.sino = sino;
@@ -323,14 +358,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     P.views_per_group = vpg;
     P.batch = batch;
     P.accumulate = accumulate ? 1 : 0;
-    const int tiles = (g.n + cbp::BP_TILE - 1) / cbp::BP_TILE;
     dim3 grid(tiles, tiles, G * SG);
-    const size_t smem = cbp::bp_smem_bytes(S);
-    static std::once_flag attr[64];
-    std::call_once(attr[dev & 63], [smem] {
-        cudaFuncSetAttribute(cbp::cbp_bp_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    });
 #ifdef CBP_DEBUG_CHECKS
     fprintf(stderr, "launch_bp S=%d G=%d vpg=%d grid=%d,%d,%d smem=%zu\n", S, G, vpg, grid.x, grid.y,
             grid.z, smem);
@@ -340,6 +368,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
 #ifdef CBP_DEBUG_CHECKS
     fprintf(stderr, "bp kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
 #endif
+    cudaFreeAsync(hdrs, stream);
     if (G > 1) {
         const size_t count = plane * batch;
         const int blocks = (int)std::min<size_t>((count + 255) / 256, (size_t)sms * 8);

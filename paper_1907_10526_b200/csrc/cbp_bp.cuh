@@ -39,6 +39,7 @@ struct BPParams {
     GeomDev g;
     Tables t;
     const uint16_t* pairs;  // [BP_BUCKETS][512] tile pair order per ray direction (r * 32 + c)
+    const struct BPHeader* hdrs;  // [tiles_y][tiles_x][view_count] from cbp_bp_header_kernel
     const float* sino;  // [batch][view_count][n_det]
     float* out;         // groups == 1: image [batch][n][n]; else partials [groups][batch][n][n]
     int view_begin, view_count;
@@ -142,6 +143,34 @@ __device__ void bp_view_header(const GeomDev& g, const Tables& t, int v, double 
     H.cth = cth;
     H.sth = sth;
     H.kae = kae;
+}
+
+// anchor of a tile: centre of its valid pixels (tiles are clipped by the border)
+__device__ __forceinline__ void bp_tile_anchor(const GeomDev& g, int tx, int ty, float& hcx,
+                                               float& hcy, double& kax, double& kay)
+{
+    const int col0 = tx * BP_TILE, row0 = ty * BP_TILE;
+    hcx = 0.5f * (float)(min(BP_TILE, g.n - col0) - 1);
+    hcy = 0.5f * (float)(min(BP_TILE, g.n - row0) - 1);
+    kax = ((double)col0 + hcx - g.c0) * g.h;
+    kay = (g.c0 - (double)row0 - hcy) * g.h;
+}
+
+// all (tile, view) headers of one BP launch, ahead of the BP kernel (so the
+// FP64 header chain is off the BP kernel's critical path)
+__global__ void __launch_bounds__(128) cbp_bp_header_kernel(GeomDev g, Tables t, int view_begin,
+                                                            int view_count, int tiles_x,
+                                                            BPHeader* __restrict__ out)
+{
+    const int tile = blockIdx.x;
+    const int vl = blockIdx.y * blockDim.x + threadIdx.x;
+    if (vl >= view_count) return;
+    float hcx, hcy;
+    double kax, kay;
+    bp_tile_anchor(g, tile % tiles_x, tile / tiles_x, hcx, hcy, kax, kay);
+    BPHeader H;
+    bp_view_header(g, t, view_begin + vl, kax, kay, hcx, hcy, H);
+    out[(size_t)tile * view_count + vl] = H;
 }
 
 // pairs along x for ray directions within 45 degrees of the x axis
@@ -263,23 +292,24 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : 2) cbp_bp_kernel(cons
     const int grp = blockIdx.z % P.groups, sg = blockIdx.z / P.groups;  // view group, slice group
     const int vg0 = grp * P.views_per_group;
     const int vgn = min(P.views_per_group, P.view_count - vg0);
-    // anchor k_a = centre of the tile's valid pixels (clipped at the border)
-    const float hcx = 0.5f * (float)(min(BP_TILE, g.n - col0) - 1);
-    const float hcy = 0.5f * (float)(min(BP_TILE, g.n - row0) - 1);
-    const double kax = ((double)col0 + hcx - g.c0) * g.h;
-    const double kay = (g.c0 - (double)row0 - hcy) * g.h;
+    float hcx, hcy;  // anchor k_a = centre of the tile's valid pixels
+    double kax, kay;
+    bp_tile_anchor(g, blockIdx.x, blockIdx.y, hcx, hcy, kax, kay);
+    const BPHeader* hsrc = P.hdrs + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * P.view_count + vg0;
     const size_t sino_plane = (size_t)P.view_count * g.n_det;
 
     for (int i = tid; i < S * BP_TILE * (BP_TILE + 1); i += BP_THREADS) acc_s[i] = 0.0;
 
     for (int vc = 0; vc < vgn; vc += BP_VC) {
         const int nvc = min(BP_VC, vgn - vc);
-        if (tid < nvc)
-            bp_view_header(g, P.t, P.view_begin + vg0 + vc + tid, kax, kay, hcx, hcy, hdr[tid]);
+        constexpr int HW = sizeof(BPHeader) / 16;  // 16-byte words per header
+        if (tid < nvc * HW)
+            reinterpret_cast<int4*>(hdr)[tid] = __ldg(reinterpret_cast<const int4*>(hsrc + vc) + tid);
         __syncthreads();
         int npass = 0;
         for (int vi = 0; vi < nvc; ++vi) npass = max(npass, (int)hdr[vi].npass_f);
         for (int pass = 0; pass < npass; ++pass) {
+#pragma unroll 3
             for (int e = tid; e < BP_VC * BP_NB; e += BP_THREADS) {
                 const int vi = e / BP_NB, jj = e % BP_NB;
                 if (vi < nvc) {
