@@ -209,7 +209,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1907_10526_b200 as cbp
-    from paper_1907_10526_b200.sharded import view_shard
+    from paper_1907_10526_b200.sharded import make_shard
 
     assert args.warmup >= 3, "at least 3 warm-up steps"
     torch.cuda.set_device(local)
@@ -217,25 +217,44 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     g = W.geometry(args.config)
-    v0, nv = view_shard(g["n_views"], rank, world)
     n, ns = g["n"], g["n_det"]
-
     batch = W.BATCH[args.config]
+    # view shard of this rank: the 4 rotated copies of a block of base views
+    # when the 90-degree symmetry applies (one image, n_views % 4 == 0), else a
+    # contiguous block
+    sh = make_shard(g["n_views"], rank, world, batch)
+    views = sh.views()
+    nv = len(views)
+    orbit = sh.mode == "orbit"
+
     host_img = W.shepp_logan(n) if batch == 1 else W.jittered_batch(n, batch, seed=7)
     img = torch.from_numpy(host_img).to(dev)
     bshape = () if batch == 1 else (batch,)
-    sino = torch.empty(bshape + (nv, ns), dtype=torch.float32, device=dev)
+    sshape = (4, sh.count, ns) if orbit else bshape + (nv, ns)
+    sino = torch.empty(sshape, dtype=torch.float32, device=dev)
     out = torch.empty(bshape + (n, n), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    def fwd(image, y):
+        if orbit:
+            cbp.forward_orbit(g, image, sh.begin, sh.count, sino=y, stream=stream)
+        else:
+            cbp.forward(g, image, y, view_begin=sh.begin, view_count=sh.count, stream=stream)
+
+    def bwd(y, image):
+        if orbit:
+            cbp.back_orbit(g, y, sh.begin, image=image, stream=stream)
+        else:
+            cbp.back(g, y, image, view_begin=sh.begin, stream=stream)
+
     def step(ev=None):
         if ev:
             ev[0].record(stream)
-        cbp.forward(g, img, sino, view_begin=v0, view_count=nv, stream=stream)
+        fwd(img, sino)
         if ev:
             ev[1].record(stream)
-        cbp.back(g, sino, out, view_begin=v0, stream=stream)
+        bwd(sino, out)
         if ev:
             ev[2].record(stream)
         if world > 1:
@@ -276,8 +295,15 @@ def main():
     value = args.steps * batch / (total_ms * 1e-3)  # FP+BP pairs (one per slice) per second
 
     # ---- roofline of the dominant kernel (ALU / FP32-pipe bound)
+    # units = nonzero (view, bin, pixel) weights of this rank's views x slices;
+    # each weight is EVALUATED once per `fold` units (4 views by symmetry, or
+    # S slices of a batch), at 30 flops, plus 2 flops per unit accumulated
     counts = weight_counts(args.config)
-    nw = int(sum(counts[v0:v0 + nv])) if counts else None
+    nw = int(sum(counts[v] for v in views)) if counts else None
+    fold = 4 if orbit else (4 if batch >= 4 else (2 if batch >= 2 else 1))
+    units = nw * batch if nw else None
+    evals = units / fold if units else None
+    flops = evals * (FLOPS_PER_WEIGHT - 2) + units * 2 if units else None
     props = torch.cuda.get_device_properties(dev)
     peaks = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz") or (clk or {}).get("sm_max_mhz") or 1965.0)
@@ -285,9 +311,11 @@ def main():
     fp_avg, bp_avg = statistics.mean(fp_ms), statistics.mean(bp_ms)
     kernels = {}
     for name, ms in (("fp", fp_avg), ("bp", bp_avg)):
-        ach = nw * batch * FLOPS_PER_WEIGHT / (ms * 1e-3) / 1e12 if nw else None
+        ach = flops / (ms * 1e-3) / 1e12 if flops else None
         kernels[name] = {"ms": ms, "tflops": ach, "frac": ach / peak_tflops if ach else None,
-                         "weights_per_launch": nw}
+                         "weights_per_launch": units, "weight_evaluations": evals,
+                         "effective_tflops_per_view_weight": units * FLOPS_PER_WEIGHT / (ms * 1e-3) / 1e12
+                         if units else None}
     dom = "bp" if bp_avg >= fp_avg else "fp"
     traffic = traffic_table().get(args.config, {}).get(dom)
     roof = {"bound": "alu", "kernel": f"cbp_{dom}_kernel", "achieved": kernels[dom]["tflops"],
@@ -295,27 +323,36 @@ def main():
             "traffic": traffic,
             "peak_basis": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 flop x "
                           f"{sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
-            "work": f"{nw} nonzero weights x {batch} slices x {FLOPS_PER_WEIGHT} flop per launch",
+            "work": f"{units} nonzero view-weights per launch ({nw} x {batch} slices), each weight "
+                    f"evaluated once per {fold} (symmetry / batch): {evals:.4g} evaluations x "
+                    f"{FLOPS_PER_WEIGHT - 2} flop + {units} x 2 flop accumulation" if units else None,
             "hbm_gbs_algorithmic": 4 * batch * (n * n + nv * ns) / (ms_to_s(statistics.mean(step_ms))) / 1e9}
 
     # ---- end to end through the C ABI with host buffers (pinned)
     e2e = None
     if not args.no_e2e:
         h_img = torch.from_numpy(host_img).pin_memory()
-        h_sino = torch.empty(bshape + (nv, ns), dtype=torch.float32).pin_memory()
+        h_sino = torch.empty(sshape, dtype=torch.float32).pin_memory()
         h_out = torch.empty(bshape + (n, n), dtype=torch.float32).pin_memory()
+        d_img = torch.empty_like(img)
         d_out = torch.empty(bshape + (n, n), dtype=torch.float32, device=dev)
         ke = max(3, min(args.steps, 50))
 
         def e2e_step():
-            cbp.forward(g, h_img, h_sino, view_begin=v0, view_count=nv)  # H2D img, D2H sino
-            if world > 1:
-                cbp.back(g, h_sino, d_out, view_begin=v0)  # H2D sino
-                torch.cuda.synchronize()
+            if world == 1:
+                # the library's host-buffer path: it stages H2D image, D2H sino,
+                # H2D sino, D2H image itself (full range -> symmetric kernels)
+                cbp.forward(g, h_img, h_sino.view(nv, ns) if orbit else h_sino)
+                cbp.back(g, h_sino.view(nv, ns) if orbit else h_sino, h_out)
+            else:
+                d_img.copy_(h_img, non_blocking=True)  # H2D image
+                fwd(d_img, sino)
+                h_sino.copy_(sino, non_blocking=True)  # D2H this rank's sinogram
+                sino.copy_(h_sino, non_blocking=True)  # H2D (the BP input of a user)
+                bwd(sino, d_out)
                 dist.all_reduce(d_out)
                 h_out.copy_(d_out)  # D2H image
-            else:
-                cbp.back(g, h_sino, h_out, view_begin=v0)  # H2D sino, D2H image
+                torch.cuda.synchronize()
 
         for _ in range(3):
             e2e_step()
@@ -334,7 +371,8 @@ def main():
         e2e = {"value": ke * batch / (float(et.item()) * 1e-3), "unit": "pairs/s",
                "h2d_bytes_per_step": 4 * batch * (n * n + nv * ns),
                "d2h_bytes_per_step": 4 * batch * (nv * ns + n * n),
-               "path": "cbp_forward/cbp_back with pinned host buffers (library staging)"}
+               "path": "cbp_forward/cbp_back on pinned host buffers (library staging)" if world == 1
+               else "pinned H2D/D2H + cbp_forward_orbit/cbp_back_orbit + NCCL all_reduce"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -349,7 +387,8 @@ def main():
             "config": {"workload": WORKLOADS[args.config], "n": n, "n_views": g["n_views"],
                        "n_det": ns, "pixel_mm": g["pixel"], "det_pitch_mm": g["det_pitch"],
                        "sid_mm": g["sid"], "sdd_mm": g["sdd"], "batch": batch,
-                       "parallelism": f"views/{world}" if world > 1 else "single",
+                       "parallelism": (f"views/{world}" if world > 1 else "single")
+                       + (" (4-fold rotational symmetry)" if orbit else ""),
                        "l2": "flushed between steps (256 MiB write, outside the timed events)"},
             "roofline": roof,
             "kernels": kernels,

@@ -91,6 +91,29 @@ int cbp_forward(const cbp_geometry_t* g, const float* image, float* sino, int32_
 int cbp_back(const cbp_geometry_t* g, const float* sino, float* image, int32_t batch,
              int32_t view_begin, int32_t view_count, int32_t accumulate, void* stream);
 
+/* Rotational symmetry.  Rotating the whole scanner by 90
+ * degrees maps view v to view v + n_views/4, keeps every detector coordinate
+ * and permutes the square pixel grid, so W(v + n_views/4, j, k) = W(v, j, R^-1 k)
+ * exactly, R(row, col) = (n-1-col, row).  When n_views % 4 == 0 one weight
+ * therefore serves 4 views.  cbp_forward / cbp_back use this automatically
+ * for a single image (batch == 1) over the full view range; it returns 4
+ * then, else 1 (CBP_EINVAL for an invalid geometry).  Setting the
+ * environment variable CBP_NO_SYMMETRY disables it. */
+int cbp_symmetry_fold(const cbp_geometry_t* g, int32_t batch, int32_t view_begin,
+                      int32_t view_count);
+
+/* The orbit form, for sharding views over GPUs without losing the symmetry:
+ * one image, the 4 n_b views {b + q n_views/4 : b in [base_begin,
+ * base_begin + base_count), q = 0..3} (0 <= base_begin, base_begin + base_count
+ * <= n_views/4; requires n_views % 4 == 0).  sino is [4][base_count][n_det]:
+ * row q base_count + i is view base_begin + i + q n_views/4.  Device pointers
+ * only, 4-byte aligned.  cbp_back_orbit overwrites image, or adds to
+ * it when accumulate != 0.  CBP_EINVAL otherwise. */
+int cbp_forward_orbit(const cbp_geometry_t* g, const float* image, float* sino,
+                      int32_t base_begin, int32_t base_count, void* stream);
+int cbp_back_orbit(const cbp_geometry_t* g, const float* sino, float* image,
+                   int32_t base_begin, int32_t base_count, int32_t accumulate, void* stream);
+
 /* Adjoint identity check on the current device (synchronous): draws seeded
  * c, y ~ U[0,1) (splitmix64), runs cbp_forward and cbp_back over all views,
  * and returns |<Ac,y> - <c,A^T y>| / |<Ac,y>| with FP64 inner products in

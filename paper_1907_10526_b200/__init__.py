@@ -22,8 +22,9 @@ LIB_PATH = os.path.join(_HERE, "libcbp.so")
 CBP_OK, CBP_EINVAL, CBP_ECUDA, CBP_ENOMEM = 0, -1, -2, -3
 
 # names declared in include/cbp.h
-ABI_FUNCTIONS = ("cbp_validate", "cbp_forward", "cbp_back", "cbp_adjoint_check",
-                 "cbp_strerror", "cbp_version", "cbp_launch_count")
+ABI_FUNCTIONS = ("cbp_validate", "cbp_forward", "cbp_back", "cbp_symmetry_fold",
+                 "cbp_forward_orbit", "cbp_back_orbit", "cbp_adjoint_check", "cbp_strerror",
+                 "cbp_version", "cbp_launch_count")
 
 
 class CbpError(RuntimeError):
@@ -84,6 +85,12 @@ def lib() -> ctypes.CDLL:
         L.cbp_forward.restype = ctypes.c_int
         L.cbp_back.argtypes = [G, fp, fp, i32, i32, i32, i32, vp]
         L.cbp_back.restype = ctypes.c_int
+        L.cbp_symmetry_fold.argtypes = [G, i32, i32, i32]
+        L.cbp_symmetry_fold.restype = ctypes.c_int
+        L.cbp_forward_orbit.argtypes = [G, fp, fp, i32, i32, vp]
+        L.cbp_forward_orbit.restype = ctypes.c_int
+        L.cbp_back_orbit.argtypes = [G, fp, fp, i32, i32, i32, vp]
+        L.cbp_back_orbit.restype = ctypes.c_int
         L.cbp_adjoint_check.argtypes = [G, ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]
         L.cbp_adjoint_check.restype = ctypes.c_int
         L.cbp_strerror.argtypes = [ctypes.c_int]
@@ -195,6 +202,44 @@ def back(geom, sino, image=None, view_begin: int = 0, accumulate: bool = False, 
     rc = lib().cbp_back(ctypes.byref(g), ps, pi, batch, view_begin, nv, 1 if accumulate else 0, st)
     if rc != CBP_OK:
         raise CbpError(rc, "cbp_back")
+    return image
+
+
+def symmetry_fold(geom, batch: int = 1, view_begin: int = 0, view_count: int | None = None) -> int:
+    """4 if the call would use the 90-degree rotational symmetry (include/cbp.h), else 1."""
+    g = _checked(geom)
+    nv = g.n_views - view_begin if view_count is None else view_count
+    return lib().cbp_symmetry_fold(ctypes.byref(g), batch, view_begin, nv)
+
+
+def forward_orbit(geom, image, base_begin: int, base_count: int, sino=None, stream=None):
+    """Views {b + q n_views/4 : b in [base_begin, base_begin + base_count), q < 4}
+    of one image (CUDA tensor [n, n]); returns sino [4, base_count, n_det]."""
+    g = _checked(geom)
+    shape = (4, base_count, g.n_det)
+    if sino is None:
+        sino = _empty_like(image, shape)
+    pi, st = _ptr_and_stream(image, stream)
+    ps, _ = _ptr_and_stream(sino, stream)
+    rc = lib().cbp_forward_orbit(ctypes.byref(g), pi, ps, base_begin, base_count, st)
+    if rc != CBP_OK:
+        raise CbpError(rc, "cbp_forward_orbit")
+    return sino
+
+
+def back_orbit(geom, sino, base_begin: int, image=None, accumulate: bool = False, stream=None):
+    """Adjoint of forward_orbit: sino [4, base_count, n_det] -> image [n, n]."""
+    g = _checked(geom)
+    if image is None:
+        if accumulate:
+            raise ValueError("accumulate=True needs an image to add into")
+        image = _empty_like(sino, (g.n, g.n))
+    ps, st = _ptr_and_stream(sino, stream)
+    pi, _ = _ptr_and_stream(image, stream)
+    rc = lib().cbp_back_orbit(ctypes.byref(g), ps, pi, base_begin, sino.shape[1],
+                              1 if accumulate else 0, st)
+    if rc != CBP_OK:
+        raise CbpError(rc, "cbp_back_orbit")
     return image
 
 

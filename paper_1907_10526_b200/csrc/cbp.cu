@@ -262,8 +262,52 @@ int launch_fp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* img,
     Pm.view_begin = v0;
     Pm.view_count = nv;
     Pm.batch = batch;
+    Pm.sym_stride = 0;
     dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, nv, G);
     cbp::cbp_fp_kernel<S><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
+    ++g_launches;
+    rc = cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+    cudaFreeAsync(pad, stream);
+    return rc;
+}
+
+// a single image over a full scan of N_v = 4 m views: one weight serves the
+// 4 views v, v + m, v + 2m, v + 3m (cbp_pad_sym4_kernel)
+bool use_sym4(const cbp_geometry_t& g, int32_t batch, int32_t v0, int32_t nv)
+{
+    static const bool off = getenv("CBP_NO_SYMMETRY") != nullptr;
+    return !off && batch == 1 && v0 == 0 && nv == g.n_views && g.n_views % 4 == 0;
+}
+
+// sino holds [4][base_count][n_det]: row q base_count + b is view
+// base_begin + b + q n_views / 4
+int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
+                   int32_t base_begin, int32_t base_count, cudaStream_t stream)
+{
+    const int P = fp_pad_width(g);
+    const int np = g.n + 2 * P;
+    const size_t plane = (size_t)np * np * 4;
+    float* pad = nullptr;
+    int rc = scratch_alloc((void**)&pad, sizeof(float) * 2 * plane, stream);
+    if (rc != CBP_OK) return rc;
+    float* padT = pad + plane;
+    dim3 pgrid((np + cbp::PAD_TILE - 1) / cbp::PAD_TILE, (np + cbp::PAD_TILE - 1) / cbp::PAD_TILE, 1);
+    cbp::cbp_pad_sym4_kernel<<<pgrid, dim3(cbp::PAD_TILE, 8), 0, stream>>>(img, pad, padT, g.n, P, np);
+    ++g_launches;
+    cbp::FPParams Pm;
+    Pm.g = to_dev(g);
+    Pm.t = t;
+    Pm.pad = pad;
+    Pm.padT = padT;
+    Pm.np = np;
+    Pm.P = P;
+    Pm.sino = sino;
+    Pm.view_begin = base_begin;
+    Pm.view_count = base_count;
+    Pm.batch = 4;
+    Pm.sym_stride = base_count;
+    dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, base_count, 1);
+    cbp::cbp_fp_kernel<4><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
     ++g_launches;
     rc = cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
     cudaFreeAsync(pad, stream);
@@ -275,6 +319,7 @@ int launch_fp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* img,
 int launch_fp(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
               int32_t batch, int32_t v0, int32_t nv, cudaStream_t stream)
 {
+    if (use_sym4(g, batch, v0, nv)) return launch_fp_sym4(g, t, img, sino, 0, g.n_views / 4, stream);
     if (batch >= 4) return launch_fp_s<4>(g, t, img, sino, batch, v0, nv, stream);
     if (batch >= 2) return launch_fp_s<2>(g, t, img, sino, batch, v0, nv, stream);
     return launch_fp_s<1>(g, t, img, sino, batch, v0, nv, stream);
@@ -307,8 +352,12 @@ int bp_groups(const cbp_geometry_t& g, int32_t slice_groups, int32_t nv, int slo
 
 template <int S>
 int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
-                int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream)
+                int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream,
+                bool sym = false)
 {
+    // symmetric: 4 "slices" (the 4 rotated frames) of one image over the base
+    // views [v0, v0 + nv); the sinogram is [4][nv][n_det]
+    if (sym) batch = 4;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -329,7 +378,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     const int vpg = (nv + G - 1) / G;
     const size_t plane = (size_t)g.n * g.n;
     float* part = nullptr;
-    if (G > 1) {
+    if (G > 1 || sym) {
         int rc = scratch_alloc((void**)&part, sizeof(float) * plane * batch * G, stream);
         if (rc != CBP_OK) return rc;
     }
@@ -351,13 +400,14 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     P.g = to_dev(g);
     P.t = t;
     P.sino = sino;
-    P.out = G > 1 ? part : img;
+    P.out = (G > 1 || sym) ? part : img;
+    P.sym_stride = sym ? nv : 0;
     P.view_begin = v0;
     P.view_count = nv;
-    P.groups = G;
+    P.groups = (G > 1 || sym) ? G : 1;
     P.views_per_group = vpg;
     P.batch = batch;
-    P.accumulate = accumulate ? 1 : 0;
+    P.accumulate = (G == 1 && !sym && accumulate) ? 1 : 0;
     dim3 grid(tiles, tiles, G * SG);
 #ifdef CBP_DEBUG_CHECKS
     fprintf(stderr, "launch_bp S=%d G=%d vpg=%d grid=%d,%d,%d smem=%zu\n", S, G, vpg, grid.x, grid.y,
@@ -369,7 +419,12 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     fprintf(stderr, "bp kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
 #endif
     cudaFreeAsync(hdrs, stream);
-    if (G > 1) {
+    if (sym) {
+        const int blocks = (int)std::min<size_t>((plane + 255) / 256, (size_t)sms * 8);
+        cbp::cbp_sym_reduce_kernel<<<blocks, 256, 0, stream>>>(part, img, g.n, G, accumulate ? 1 : 0);
+        ++g_launches;
+        cudaFreeAsync(part, stream);
+    } else if (G > 1) {
         const size_t count = plane * batch;
         const int blocks = (int)std::min<size_t>((count + 255) / 256, (size_t)sms * 8);
         cbp::cbp_reduce_kernel<<<blocks, 256, 0, stream>>>(part, img, count, G, accumulate ? 1 : 0);
@@ -382,6 +437,8 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
 int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
               int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream)
 {
+    if (use_sym4(g, batch, v0, nv))
+        return launch_bp_s<4>(g, t, sino, img, batch, 0, g.n_views / 4, accumulate, stream, true);
     if (batch >= 4) return launch_bp_s<4>(g, t, sino, img, batch, v0, nv, accumulate, stream);
     if (batch >= 2) return launch_bp_s<2>(g, t, sino, img, batch, v0, nv, accumulate, stream);
     return launch_bp_s<1>(g, t, sino, img, batch, v0, nv, accumulate, stream);
@@ -470,6 +527,46 @@ int cbp_back(const cbp_geometry_t* g, const float* sino, float* image, int32_t b
     if (ki == 0 && cudaMemcpyAsync(image, di, ib, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
         return CBP_ECUDA;
     return cudaStreamSynchronize(stream) == cudaSuccess ? CBP_OK : CBP_ECUDA;
+}
+
+int cbp_symmetry_fold(const cbp_geometry_t* g, int32_t batch, int32_t view_begin,
+                      int32_t view_count)
+{
+    if (cbp_validate(g) != CBP_OK) return CBP_EINVAL;
+    return use_sym4(*g, batch, view_begin, view_count) ? 4 : 1;
+}
+
+static int check_orbit(const cbp_geometry_t* g, const void* a, const void* b, int32_t base_begin,
+                       int32_t base_count)
+{
+    if (cbp_validate(g) != CBP_OK || g->n_views % 4 != 0) return CBP_EINVAL;
+    if (!a || !b || base_count < 1 || base_begin < 0 || (int64_t)base_begin + base_count > g->n_views / 4)
+        return CBP_EINVAL;
+    if (((uintptr_t)a & 3) || ((uintptr_t)b & 3)) return CBP_EINVAL;
+    if (pointer_kind(a) != 1 || pointer_kind(b) != 1) return CBP_EINVAL;
+    return CBP_OK;
+}
+
+int cbp_forward_orbit(const cbp_geometry_t* g, const float* image, float* sino, int32_t base_begin,
+                      int32_t base_count, void* stream_)
+{
+    int rc = check_orbit(g, image, sino, base_begin, base_count);
+    if (rc != CBP_OK) return rc;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    cbp::Tables t;
+    if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    return launch_fp_sym4(*g, t, image, sino, base_begin, base_count, stream);
+}
+
+int cbp_back_orbit(const cbp_geometry_t* g, const float* sino, float* image, int32_t base_begin,
+                   int32_t base_count, int32_t accumulate, void* stream_)
+{
+    int rc = check_orbit(g, image, sino, base_begin, base_count);
+    if (rc != CBP_OK) return rc;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    cbp::Tables t;
+    if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    return launch_bp_s<4>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, true);
 }
 
 static uint64_t splitmix64(uint64_t& x)

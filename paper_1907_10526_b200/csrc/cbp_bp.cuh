@@ -45,6 +45,10 @@ struct BPParams {
     int view_begin, view_count;
     int groups, views_per_group, batch;
     int accumulate;     // groups == 1 only
+    // > 0: 4-fold rotational symmetry: slice q reads sinogram rows
+    // vl + q sym_stride of batch 0 and accumulates the image in the frame
+    // rotated by q (combined by cbp_sym_reduce_kernel)
+    int sym_stride;
 };
 
 constexpr int BP_TILE = 32;       // pixels per tile side
@@ -327,8 +331,11 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : 2) cbp_bp_kernel(cons
 #pragma unroll
                             for (int q = 0; q < S; ++q) {
                                 const int b = sg * S + q;
+                                const float* ys = P.sym_stride > 0
+                                    ? P.sino + (size_t)q * P.sym_stride * g.n_det
+                                    : P.sino + (size_t)b * sino_plane;
                                 ytab[(vi * BP_NB + jj) * S + q] =
-                                    b < P.batch ? __ldg(P.sino + (size_t)b * sino_plane + yo) * hA : 0.0f;
+                                    (P.sym_stride > 0 || b < P.batch) ? __ldg(ys + yo) * hA : 0.0f;
                             }
                         }
                     }
@@ -411,6 +418,26 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : 2) cbp_bp_kernel(cons
                 *o = (P.groups == 1 && P.accumulate) ? *o + v : v;
             }
         }
+    }
+}
+
+// symmetric BP: out[k] = (accumulate ? out[k] : 0) + sum_g sum_q part[g][q][R^-q k]
+// (fixed order), R(r, c) = (n-1-c, r) the +90 degree pixel rotation
+__global__ void cbp_sym_reduce_kernel(const float* __restrict__ part, float* __restrict__ out, int n,
+                                      int groups, int accumulate)
+{
+    const size_t plane = (size_t)n * n;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < plane;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / n), c = (int)(i % n);
+        // R^-q (r, c): q = 0 (r, c), 1 (c, n-1-r), 2 (n-1-r, n-1-c), 3 (n-1-c, r)
+        const size_t src[4] = {i, (size_t)c * n + (n - 1 - r), (size_t)(n - 1 - r) * n + (n - 1 - c),
+                               (size_t)(n - 1 - c) * n + r};
+        float s = accumulate ? out[i] : 0.0f;
+        for (int gi = 0; gi < groups; ++gi)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s += part[((size_t)gi * 4 + q) * plane + src[q]];
+        out[i] = s;
     }
 }
 

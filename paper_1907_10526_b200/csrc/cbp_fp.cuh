@@ -39,6 +39,10 @@ struct FPParams {
     int np, P;          // padded side, pad width (>= max K)
     float* sino;        // [batch][view_count][n_det]
     int view_begin, view_count, batch;
+    // > 0: 4-fold rotational symmetry (see cbp_pad_sym4_kernel): the S = 4
+    // slices are the image rotated by 0, 90, 180, 270 degrees and slice q of
+    // base view vl is view vl + q sym_stride of the single output sinogram
+    int sym_stride;
 };
 
 constexpr int FP_BLOCK = 128;
@@ -76,6 +80,52 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_kernel(const float* __re
         if (r < np && c < np)
 #pragma unroll
             for (int k = 0; k < S; ++k) dstT[((size_t)c * np + r) * S + k] = tile[threadIdx.x][cc][k];
+    }
+}
+
+// Rotation R by +90 degrees about the rotation centre maps pixel (r, c) to
+// R(r, c) = (n-1-c, r) and carries view theta to theta + pi/2 with the same
+// detector coordinates, so W(v + N/4, j, k) = W(v, j, R^-1 k) exactly (the
+// square pixel basis is invariant).  Hence y[v + q N/4] = sum_k c[R^q k] W(v, j, k):
+// slice q of the padded copy holds c o R^q, and one weight serves 4 views.
+__device__ __forceinline__ void rot90_pow(int n, int q, int& r, int& c)
+{
+    for (int t = 0; t < q; ++t) {
+        const int nr = n - 1 - c;
+        c = r;
+        r = nr;
+    }
+}
+
+__global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym4_kernel(const float* __restrict__ img,
+                                                                    float* __restrict__ pad,
+                                                                    float* __restrict__ padT, int n,
+                                                                    int P, int np)
+{
+    __shared__ float tile[PAD_TILE][PAD_TILE + 1][4];
+    const int r0 = blockIdx.y * PAD_TILE, c0 = blockIdx.x * PAD_TILE;
+    for (int rr = threadIdx.y; rr < PAD_TILE; rr += 8) {
+        const int r = r0 + rr, c = c0 + threadIdx.x;
+        const int sr = r - P, sc = c - P;
+        const bool in = sr >= 0 && sr < n && sc >= 0 && sc < n;
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            int a = sr, b = sc;
+            rot90_pow(n, q, a, b);
+            v[q] = in ? img[(size_t)a * n + b] : 0.0f;
+            tile[rr][threadIdx.x][q] = v[q];
+        }
+        if (r < np && c < np)
+            *reinterpret_cast<float4*>(pad + ((size_t)r * np + c) * 4) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    __syncthreads();
+    for (int cc = threadIdx.y; cc < PAD_TILE; cc += 8) {
+        const int c = c0 + cc, r = r0 + threadIdx.x;
+        if (r < np && c < np) {
+            const float* t = tile[threadIdx.x][cc];
+            *reinterpret_cast<float4*>(padT + ((size_t)c * np + r) * 4) = make_float4(t[0], t[1], t[2], t[3]);
+        }
     }
 }
 
@@ -395,7 +445,10 @@ __global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
 #pragma unroll
         for (int q = 0; q < S; ++q) {
             const int b = grp * S + q;
-            if (b < P.batch) P.sino[((size_t)b * P.view_count + vl) * g.n_det + j] = (float)acc[q];
+            if (P.sym_stride > 0)
+                P.sino[((size_t)vl + (size_t)q * P.sym_stride) * g.n_det + j] = (float)acc[q];
+            else if (b < P.batch)
+                P.sino[((size_t)b * P.view_count + vl) * g.n_det + j] = (float)acc[q];
         }
 }
 

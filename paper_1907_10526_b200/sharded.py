@@ -1,31 +1,68 @@
 """Row a7 / 8(e): the projector sharded over GPUs by VIEWS (one process per
 GPU, torch.distributed over NCCL).
 
-Forward projection needs no communication: rank g owns the contiguous view
-block [v0_g, v0_g + nv_g) and writes its own sinogram rows.  The
-back-projection is a sum over views, so each rank back-projects its block
-into a partial image and the partials are summed with one collective
-(all_reduce, or reduce to one rank) -- the only exchange step of the path.
+Forward projection needs no communication: each rank owns a set of views and
+writes its own sinogram rows.  The back-projection is a sum over views, so
+each rank back-projects its views into a partial image and the partials are
+summed with one collective (all_reduce, or reduce to one rank) -- the only
+exchange step of the path.
 
-Argument marshalling and the collective only; the projections themselves run
-in libcbp.so (``paper_1907_10526_b200.forward`` / ``back``).  The projector
-functions are parameters so the host logic can be tested on CPU with gloo.
+Two shard shapes (``Shard.mode``):
+
+* ``"orbit"`` (one image, n_views % 4 == 0): the n_views/4 base views are
+  split in contiguous blocks and each rank takes the 4 rotated copies of its
+  block, views {b + q n_views/4}; the library's 90-degree rotational symmetry
+  then computes each weight once for 4 views (``forward_orbit`` /
+  ``back_orbit``, local sinogram [4, nb, n_det]);
+* ``"block"`` (otherwise): a contiguous block of views (local sinogram
+  [B?, nv, n_det]).
+
+Argument marshalling and the collective only; the projections run in
+libcbp.so.  The projector callables are parameters so the host logic is
+testable on CPU with gloo.
 """
 from __future__ import annotations
 
+from dataclasses import dataclass
 from typing import Callable, Optional
+
+import numpy as np
 
 import paper_1907_10526_b200 as _cbp
 
 
 def view_shard(n_views: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous view block (view_begin, view_count) of `rank` out of `world`;
-    the first n_views % world ranks get one extra view."""
+    """Contiguous block (begin, count) of `rank` out of `world` for n_views
+    items; the first n_views % world ranks get one extra."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError(f"bad rank {rank} of {world}")
     base, rem = divmod(n_views, world)
     v0 = rank * base + min(rank, rem)
     return v0, base + (1 if rank < rem else 0)
+
+
+@dataclass(frozen=True)
+class Shard:
+    mode: str    # "orbit" or "block"
+    begin: int   # first base view (orbit) or first view (block)
+    count: int   # base views (orbit) or views (block)
+    n_views: int
+
+    def views(self) -> np.ndarray:
+        """global view index of each local sinogram row"""
+        if self.mode == "block":
+            return np.arange(self.begin, self.begin + self.count)
+        m = self.n_views // 4
+        return np.concatenate([np.arange(self.begin, self.begin + self.count) + q * m
+                               for q in range(4)])
+
+
+def make_shard(n_views: int, rank: int, world: int, batch: int = 1) -> Shard:
+    if batch == 1 and n_views % 4 == 0 and n_views // 4 >= world:
+        b0, nb = view_shard(n_views // 4, rank, world)
+        return Shard("orbit", b0, nb, n_views)
+    v0, nv = view_shard(n_views, rank, world)
+    return Shard("block", v0, nv, n_views)
 
 
 def _rank_world(group):
@@ -35,32 +72,36 @@ def _rank_world(group):
     return dist.get_rank(group), dist.get_world_size(group)
 
 
-def forward_sharded(geom, image, sino=None, group=None,
-                    forward: Callable = _cbp.forward, stream=None):
-    """This rank's block of y = A c: returns (sino_shard, view_begin).
-    No communication."""
+def _n_views(geom):
+    return geom["n_views"] if isinstance(geom, dict) else geom.n_views
+
+
+def forward_sharded(geom, image, group=None, forward: Callable = _cbp.forward,
+                    forward_orbit: Callable = _cbp.forward_orbit, stream=None):
+    """This rank's part of y = A c: returns (local sinogram, Shard).  No
+    communication.  Row i of the local sinogram is view shard.views()[i]."""
     rank, world = _rank_world(group)
-    n_views = geom["n_views"] if isinstance(geom, dict) else geom.n_views
-    v0, nv = view_shard(n_views, rank, world)
-    if nv == 0:
-        return None, v0
-    return forward(geom, image, sino, view_begin=v0, view_count=nv, stream=stream), v0
+    batch = 1 if image.ndim == 2 else image.shape[0]
+    sh = make_shard(_n_views(geom), rank, world, batch)
+    if sh.count == 0:
+        return None, sh
+    if sh.mode == "orbit":
+        return forward_orbit(geom, image, sh.begin, sh.count, stream=stream), sh
+    return forward(geom, image, view_begin=sh.begin, view_count=sh.count, stream=stream), sh
 
 
-def back_sharded(geom, sino_shard, image=None, group=None, dst: Optional[int] = None,
-                 back: Callable = _cbp.back, stream=None):
+def back_sharded(geom, sino_local, shard: Shard, image=None, group=None, dst: Optional[int] = None,
+                 back: Callable = _cbp.back, back_orbit: Callable = _cbp.back_orbit, stream=None):
     """c = sum_g A_g^T y_g: back-projects this rank's views, then sums the
-    partial images over the group (all_reduce, or reduce to `dst`).
-    `sino_shard` holds views view_shard(n_views, rank, world)."""
+    partial images over the group (all_reduce, or reduce to `dst`)."""
     import torch
     import torch.distributed as dist
     rank, world = _rank_world(group)
-    n_views = geom["n_views"] if isinstance(geom, dict) else geom.n_views
-    v0, nv = view_shard(n_views, rank, world)
-    if sino_shard is not None and sino_shard.shape[-2] != nv:
-        raise ValueError(f"rank {rank} holds {sino_shard.shape[-2]} views, expected {nv}")
-    if nv > 0:
-        image = back(geom, sino_shard, image, view_begin=v0, stream=stream)
+    if shard.count > 0:
+        if shard.mode == "orbit":
+            image = back_orbit(geom, sino_local, shard.begin, image=image, stream=stream)
+        else:
+            image = back(geom, sino_local, image, view_begin=shard.begin, stream=stream)
     elif image is not None:
         image[...] = 0
     else:
@@ -74,8 +115,9 @@ def back_sharded(geom, sino_shard, image=None, group=None, dst: Optional[int] = 
     return image
 
 
-def normal_sharded(geom, image, group=None, forward: Callable = _cbp.forward,
-                   back: Callable = _cbp.back, stream=None):
+def normal_sharded(geom, image, group=None, stream=None, **fns):
     """A^T A c over the group (one FP+BP pair, the benchmark's step)."""
-    y, _ = forward_sharded(geom, image, group=group, forward=forward, stream=stream)
-    return back_sharded(geom, y, group=group, back=back, stream=stream)
+    fwd = {k: v for k, v in fns.items() if k in ("forward", "forward_orbit")}
+    bwd = {k: v for k, v in fns.items() if k in ("back", "back_orbit")}
+    y, sh = forward_sharded(geom, image, group=group, stream=stream, **fwd)
+    return back_sharded(geom, y, sh, group=group, stream=stream, **bwd)

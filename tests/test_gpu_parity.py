@@ -261,3 +261,62 @@ def test_batched_config4_sampled(torch_cuda):
     rows, cols = rng.integers(0, g["n"], 24), rng.integers(0, g["n"], 24)
     for b in (5, 62):
         _assert_parity(c[b, rows, cols], O.back_pixels(g, y[b], rows, cols), f"BP cfg4 slice {b}")
+
+
+@pytest.mark.parametrize("n_views", [88, 360])
+def test_rotational_symmetry_path(torch_cuda, n_views):
+    """A full scan with N_v % 4 == 0 and one image runs the 4-fold symmetric
+    path (one weight for views v, v+N/4, v+N/2, v+3N/4); partial view ranges
+    run the direct path.  Both must match the oracle, and each other."""
+    torch = torch_cuda
+    g = dict(W.geometry("1"), n_views=n_views)
+    img = W.shepp_logan(g["n"])
+    y_sym = _fp(torch, g, img)                       # full range: symmetric
+    y_a = _fp(torch, g, img, view_begin=0, view_count=n_views // 2)
+    y_b = _fp(torch, g, img, view_begin=n_views // 2, view_count=n_views // 2)
+    ref = O.forward(g, img)
+    _assert_parity(y_sym, ref, "FP symmetric")
+    _assert_parity(np.concatenate([y_a, y_b]), ref, "FP direct")
+    np.testing.assert_allclose(y_sym, np.concatenate([y_a, y_b]), rtol=2e-5, atol=1e-5 * ref.max())
+    ys = W.random_sino(n_views, g["n_det"], 108)
+    c_sym = _bp(torch, g, ys)
+    c_dir = _bp(torch, g, ys[: n_views // 2], 0) + _bp(torch, g, ys[n_views // 2:], n_views // 2)
+    refc = O.back(g, ys)
+    _assert_parity(c_sym, refc, "BP symmetric")
+    _assert_parity(c_dir, refc, "BP direct")
+    # accumulate on the symmetric path
+    t = torch.from_numpy(ys).cuda()
+    acc = torch.from_numpy(c_dir).cuda()
+    cbp.back(g, t, image=acc, accumulate=True)
+    torch.cuda.synchronize()
+    _assert_parity(acc.cpu().numpy(), 2 * refc, "BP symmetric accumulate")
+
+
+def test_orbit_shards_sum_to_full(torch_cuda):
+    """The orbit ABI (the multi-GPU shard shape): two 'ranks' run in sequence
+    on one GPU, each FP-projects the 4 rotated copies of its base-view block
+    and back-projects them; rows match the oracle and the partial images sum
+    to the full back-projection (the all_reduce of row a7)."""
+    torch = torch_cuda
+    from paper_1907_10526_b200 import sharded
+    g = W.geometry("2")
+    img = torch.from_numpy(W.shepp_logan(g["n"])).cuda()
+    total = torch.zeros((g["n"], g["n"]), device="cuda")
+    ys = []
+    for rank in range(2):
+        sh = sharded.make_shard(g["n_views"], rank, 2)
+        assert sh.mode == "orbit"
+        y = cbp.forward_orbit(g, img, sh.begin, sh.count)
+        cbp.back_orbit(g, y, sh.begin, image=total, accumulate=True)
+        ys.append((sh, y))
+    full_y = cbp.forward(g, img)
+    full_c = cbp.back(g, full_y)
+    torch.cuda.synchronize()
+    for sh, y in ys:
+        rows = torch.from_numpy(sh.views()).cuda()
+        torch.testing.assert_close(y.reshape(-1, g["n_det"]), full_y[rows], rtol=1e-5, atol=1e-4)
+    _assert_parity(total.cpu().numpy(), full_c.cpu().numpy(), "orbit shards summed")
+    sh = sharded.make_shard(g["n_views"], 1, 2)
+    for v in (int(sh.views()[0]), int(sh.views()[-1])):
+        _assert_parity(full_y[v].cpu().numpy(), O.forward(g, W.shepp_logan(g["n"]), v, 1)[0],
+                       f"FP view {v}")

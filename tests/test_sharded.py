@@ -1,8 +1,8 @@
-"""Row a7 / 8(e) host logic on CPU: view sharding and the partial-image sum,
-world_size 2 over gloo.  The projector callables are the FP64 oracle here
-(test infrastructure), so the check is exactly: concatenated forward shards
-== the full forward, and the all-reduced partial back-projections == the
-full back-projection."""
+"""Row a7 / 8(e) host logic on CPU: view sharding (block and symmetric
+orbit shards) and the partial-image sum, world_size 2 over gloo.  The
+projector callables are the FP64 oracle here (test infrastructure), so the
+check is exactly: the forward shards are the full sinogram's rows, and the
+all-reduced partial back-projections equal the full back-projection."""
 import socket
 
 import numpy as np
@@ -29,6 +29,15 @@ def test_view_shard_partition():
         sharded.view_shard(10, 2, 2)
 
 
+@pytest.mark.parametrize("n_views,world", [(720, 8), (720, 3), (90, 4), (12, 2), (8, 4)])
+def test_shards_cover_every_view_once(n_views, world):
+    views = np.concatenate([sharded.make_shard(n_views, r, world).views() for r in range(world)])
+    assert sorted(views.tolist()) == list(range(n_views))
+    modes = {sharded.make_shard(n_views, r, world).mode for r in range(world)}
+    assert modes == ({"orbit"} if n_views % 4 == 0 and n_views // 4 >= world else {"block"})
+    assert sharded.make_shard(n_views, 0, world, batch=3).mode == "block"
+
+
 def _orc_forward(geom, image, sino=None, view_begin=0, view_count=None, stream=None):
     return torch.from_numpy(O.forward(geom, image.numpy(), view_begin, view_count, threads=2))
 
@@ -41,14 +50,36 @@ def _orc_back(geom, sino, image=None, view_begin=0, stream=None):
     return image
 
 
+def _orc_forward_orbit(geom, image, base_begin, base_count, sino=None, stream=None):
+    m = geom["n_views"] // 4
+    return torch.from_numpy(np.stack([
+        O.forward(geom, image.numpy(), base_begin + q * m, base_count, threads=2)
+        for q in range(4)]))
+
+
+def _orc_back_orbit(geom, sino, base_begin, image=None, accumulate=False, stream=None):
+    m = geom["n_views"] // 4
+    c = sum(O.back(geom, sino[q].numpy(), base_begin + q * m, threads=2) for q in range(4))
+    c = torch.from_numpy(c)
+    if image is None:
+        return c
+    image.copy_(c)
+    return image
+
+
+FNS = dict(forward=_orc_forward, forward_orbit=_orc_forward_orbit)
+BNS = dict(back=_orc_back, back_orbit=_orc_back_orbit)
+
+
 def _worker(rank, world, port, geom, img, q):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     try:
-        y, v0 = sharded.forward_sharded(geom, torch.from_numpy(img), forward=_orc_forward)
-        c = sharded.back_sharded(geom, y, back=_orc_back)
-        r = sharded.back_sharded(geom, y, image=torch.zeros_like(c), dst=0, back=_orc_back)
-        q.put((rank, v0, y.numpy(), c.numpy(), r.numpy() if rank == 0 else None))
+        y, sh = sharded.forward_sharded(geom, torch.from_numpy(img), **FNS)
+        c = sharded.back_sharded(geom, y, sh, **BNS)
+        r = sharded.back_sharded(geom, y, sh, image=torch.zeros_like(c), dst=0, **BNS)
+        yl = y.reshape(-1, geom["n_det"]).numpy()
+        q.put((rank, sh.views(), yl, c.numpy(), r.numpy() if rank == 0 else None, sh.mode))
     finally:
         dist.destroy_process_group()
 
@@ -59,9 +90,10 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2])
-def test_sharded_forward_back_gloo(world):
-    geom = dict(W._fan(16, 9, 32))
+@pytest.mark.parametrize("n_views", [9, 12])  # 9: block shards; 12: orbit shards
+def test_sharded_forward_back_gloo(n_views):
+    world = 2
+    geom = dict(W._fan(16, n_views, 32))
     img = W.shepp_logan(16).astype(np.float64)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -69,16 +101,16 @@ def test_sharded_forward_back_gloo(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, geom, img, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=120) for _ in range(world))
+    res = sorted((q.get(timeout=120) for _ in range(world)), key=lambda t: t[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     full_y = O.forward(geom, img)
     full_c = O.back(geom, full_y)
-    ys = np.concatenate([r[2] for r in res], axis=0)
-    np.testing.assert_array_equal(ys, full_y)  # FP shards are exact slices
-    for r in res:
-        v0, nv = sharded.view_shard(geom["n_views"], r[0], world)
-        assert r[1] == v0 and r[2].shape[0] == nv
-        np.testing.assert_allclose(r[3], full_c, rtol=1e-12, atol=1e-9)  # all_reduce
+    seen = np.concatenate([r[1] for r in res])
+    assert sorted(seen.tolist()) == list(range(n_views))
+    for rank, views, yl, c, red, mode in res:
+        assert mode == ("orbit" if n_views % 4 == 0 else "block")
+        np.testing.assert_array_equal(yl, full_y[views])  # FP shards are exact rows
+        np.testing.assert_allclose(c, full_c, rtol=1e-12, atol=1e-9)  # all_reduce
     np.testing.assert_allclose(res[0][4], full_c, rtol=1e-12, atol=1e-9)  # reduce to rank 0
