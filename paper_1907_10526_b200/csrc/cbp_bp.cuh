@@ -280,7 +280,7 @@ __host__ __device__ constexpr size_t bp_smem_bytes(int S)
 }
 
 template <int S>
-__global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : 2) cbp_bp_kernel(const BPParams P)
+__global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp_bp_kernel(const BPParams P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     BPEntry(*tab)[BP_NB] = reinterpret_cast<BPEntry(*)[BP_NB]>(smem);

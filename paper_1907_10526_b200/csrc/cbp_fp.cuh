@@ -175,12 +175,11 @@ struct FPRay {
 // four sat() arguments t.. = sat(z/C + ...) are formed directly from k
 // (u11 = z11/C + 1, u12 = u11 - tau'/C, u21 = u11 - A/C, u22 = u12 - A/C),
 // and the trapezoid bound r = A + tau' - z11 is affine in k too.
+// `out` holds the thread's S FP64 totals at stride FP_BLOCK (shared memory)
 template <int K, int MAB, int S>
 __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, int np, int P,
-                                        double (&out)[S])
+                                        double* out)
 {
-#pragma unroll
-    for (int q = 0; q < S; ++q) out[q] = 0.0;
     uint32_t flo = R.flo;
     int32_t fhi = R.fhi;
     const int qmax = n + P - K;
@@ -270,13 +269,13 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
             }
         }
 #pragma unroll
-        for (int q = 0; q < S; ++q) out[q] += (double)acc[q].x + (double)acc[q].y;  // two-level sum
+        for (int q = 0; q < S; ++q) out[q * FP_BLOCK] += (double)acc[q].x + (double)acc[q].y;  // two-level sum
     }
 }
 
 template <int K, int S>
 __device__ __forceinline__ void fp_walk_k(const FPRay& R, int mab, int i0, int i1, int n, int np,
-                                          int P, double (&out)[S])
+                                          int P, double* out)
 {
     if (mab == 1) fp_walk<K, 1, S>(R, i0, i1, n, np, P, out);
     else if (mab == 2) fp_walk<K, 2, S>(R, i0, i1, n, np, P, out);
@@ -286,10 +285,8 @@ __device__ __forceinline__ void fp_walk_k(const FPRay& R, int mab, int i0, int i
 // generic K (wide bins relative to pixels): same arithmetic, runtime trip count
 template <int S>
 __device__ void fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, int np, int P,
-                                double (&out)[S])
+                                double* out)
 {
-#pragma unroll
-    for (int q = 0; q < S; ++q) out[q] = 0.0;
     uint32_t flo = R.flo;
     int32_t fhi = R.fhi;
     const int qmax = n + P - K;
@@ -320,12 +317,12 @@ __device__ void fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, in
             for (int q = 0; q < S; ++q) part[q] = fmaf(c[q], w, part[q]);
         }
 #pragma unroll
-        for (int q = 0; q < S; ++q) out[q] += (double)part[q];
+        for (int q = 0; q < S; ++q) out[q * FP_BLOCK] += (double)part[q];
     }
 }
 
 template <int S>
-__global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
+__global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_fp_kernel(const FPParams P)
 {
     const GeomDev& g = P.g;
     const int jr = blockIdx.x * FP_BLOCK + threadIdx.x;
@@ -394,9 +391,11 @@ __global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
     const int whi = __reduce_max_sync(0xffffffffu, ihi);
     const int Kw = __reduce_max_sync(0xffffffffu, K);
 
-    double acc[S];
+    __shared__ double sacc[S * FP_BLOCK];  // FP64 totals, [q][thread]
+    double* acc = sacc + threadIdx.x;
 #pragma unroll
-    for (int q = 0; q < S; ++q) acc[q] = Kw > P.P ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;  // pad too thin: NaN
+    for (int q = 0; q < S; ++q)
+        acc[q * FP_BLOCK] = Kw > P.P ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;  // pad too thin: NaN
     if (wlo <= whi && Kw <= P.P) {
         FPRay R;
         // lower support edge on line i: q*(i) - sig_q, as 32.32 fixed point from line wlo
@@ -439,16 +438,16 @@ __global__ void __launch_bounds__(FP_BLOCK) cbp_fp_kernel(const FPParams P)
             default: fp_walk_generic<S>(R, Kw, wlo, whi, n, P.np, P.P, acc); break;
         }
 #pragma unroll
-        for (int q = 0; q < S; ++q) acc[q] *= h * h / A;  // W = (h^2 / A) num / B
+        for (int q = 0; q < S; ++q) acc[q * FP_BLOCK] *= h * h / A;  // W = (h^2 / A) num / B
     }
     if (valid)
 #pragma unroll
         for (int q = 0; q < S; ++q) {
             const int b = grp * S + q;
             if (P.sym_stride > 0)
-                P.sino[((size_t)vl + (size_t)q * P.sym_stride) * g.n_det + j] = (float)acc[q];
+                P.sino[((size_t)vl + (size_t)q * P.sym_stride) * g.n_det + j] = (float)acc[q * FP_BLOCK];
             else if (b < P.batch)
-                P.sino[((size_t)b * P.view_count + vl) * g.n_det + j] = (float)acc[q];
+                P.sino[((size_t)b * P.view_count + vl) * g.n_det + j] = (float)acc[q * FP_BLOCK];
         }
 }
 
