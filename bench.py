@@ -300,10 +300,13 @@ def main():
     # S slices of a batch), at 30 flops, plus 2 flops per unit accumulated
     counts = weight_counts(args.config)
     nw = int(sum(counts[v] for v in views)) if counts else None
-    fold = 4 if orbit else (4 if batch >= 4 else (2 if batch >= 2 else 1))
+    # views (symmetry) or slices (batch) per weight evaluation, FP and BP
+    sym = 4 if orbit else cbp.symmetry_fold(g, batch, sh.begin, sh.count)
+    fp_mirror = bool(os.environ.get("CBP_FP_MIRROR"))
+    folds = {"fp": sym if (sym != 8 or fp_mirror) else 4, "bp": sym}
+    if sym == 1:
+        folds = {k: (4 if batch >= 4 else (2 if batch >= 2 else 1)) for k in folds}
     units = nw * batch if nw else None
-    evals = units / fold if units else None
-    flops = evals * (FLOPS_PER_WEIGHT - 2) + units * 2 if units else None
     props = torch.cuda.get_device_properties(dev)
     peaks = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz") or (clk or {}).get("sm_max_mhz") or 1965.0)
@@ -311,9 +314,12 @@ def main():
     fp_avg, bp_avg = statistics.mean(fp_ms), statistics.mean(bp_ms)
     kernels = {}
     for name, ms in (("fp", fp_avg), ("bp", bp_avg)):
+        evals = units / folds[name] if units else None
+        flops = evals * (FLOPS_PER_WEIGHT - 2) + units * 2 if units else None
         ach = flops / (ms * 1e-3) / 1e12 if flops else None
         kernels[name] = {"ms": ms, "tflops": ach, "frac": ach / peak_tflops if ach else None,
                          "weights_per_launch": units, "weight_evaluations": evals,
+                         "views_or_slices_per_evaluation": folds[name],
                          "effective_tflops_per_view_weight": units * FLOPS_PER_WEIGHT / (ms * 1e-3) / 1e12
                          if units else None}
     dom = "bp" if bp_avg >= fp_avg else "fp"
@@ -324,8 +330,9 @@ def main():
             "peak_basis": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 flop x "
                           f"{sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
             "work": f"{units} nonzero view-weights per launch ({nw} x {batch} slices), each weight "
-                    f"evaluated once per {fold} (symmetry / batch): {evals:.4g} evaluations x "
-                    f"{FLOPS_PER_WEIGHT - 2} flop + {units} x 2 flop accumulation" if units else None,
+                    f"evaluated once per {folds[dom]} views/slices (symmetry / batch): "
+                    f"{kernels[dom]['weight_evaluations']:.4g} evaluations x {FLOPS_PER_WEIGHT - 2} flop"
+                    f" + {units} x 2 flop accumulation" if units else None,
             "hbm_gbs_algorithmic": 4 * batch * (n * n + nv * ns) / (ms_to_s(statistics.mean(step_ms))) / 1e9}
 
     # ---- end to end through the C ABI with host buffers (pinned)

@@ -95,10 +95,13 @@ int cbp_back(const cbp_geometry_t* g, const float* sino, float* image, int32_t b
  * degrees maps view v to view v + n_views/4, keeps every detector coordinate
  * and permutes the square pixel grid, so W(v + n_views/4, j, k) = W(v, j, R^-1 k)
  * exactly, R(row, col) = (n-1-col, row).  When n_views % 4 == 0 one weight
- * therefore serves 4 views.  cbp_forward / cbp_back use this automatically
- * for a single image (batch == 1) over the full view range; it returns 4
- * then, else 1 (CBP_EINVAL for an invalid geometry).  Setting the
- * environment variable CBP_NO_SYMMETRY disables it. */
+ * therefore serves 4 views.  With the mirror (x, y) -> (x, -y), which maps
+ * view v to n_views - v, bin j to n_det-1-j and (row, col) to (n-1-row, col),
+ * one weight serves 8 views when n_views % 8 == 0.  cbp_forward / cbp_back
+ * use this automatically for a single image (batch == 1) over the full view
+ * range; cbp_symmetry_fold returns the views per weight evaluation (8, 4 or
+ * 1; CBP_EINVAL for an invalid geometry).  The environment variables
+ * CBP_NO_SYMMETRY (all) and CBP_NO_MIRROR (the mirror) disable it. */
 int cbp_symmetry_fold(const cbp_geometry_t* g, int32_t batch, int32_t view_begin,
                       int32_t view_count);
 

@@ -263,6 +263,7 @@ int launch_fp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* img,
     Pm.view_count = nv;
     Pm.batch = batch;
     Pm.sym_stride = 0;
+    Pm.sym_mode = 0;
     dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, nv, G);
     cbp::cbp_fp_kernel<S><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
     ++g_launches;
@@ -306,8 +307,51 @@ int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     Pm.view_count = base_count;
     Pm.batch = 4;
     Pm.sym_stride = base_count;
+    Pm.sym_mode = 4;
     dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, base_count, 1);
     cbp::cbp_fp_kernel<4><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
+    ++g_launches;
+    rc = cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+    cudaFreeAsync(pad, stream);
+    return rc;
+}
+
+// the full dihedral symmetry (rotations and the mirror): one weight serves 8
+// views; a single image over a full scan of N_v = 8 m views
+bool use_sym8(const cbp_geometry_t& g, int32_t batch, int32_t v0, int32_t nv)
+{
+    static const bool off = getenv("CBP_NO_MIRROR") != nullptr;
+    return !off && use_sym4(g, batch, v0, nv) && g.n_views % 8 == 0;
+}
+
+int launch_fp_sym8(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
+                   cudaStream_t stream)
+{
+    const int P = fp_pad_width(g);
+    const int np = g.n + 2 * P;
+    const size_t plane = (size_t)np * np * 8;
+    float* pad = nullptr;
+    int rc = scratch_alloc((void**)&pad, sizeof(float) * 2 * plane, stream);
+    if (rc != CBP_OK) return rc;
+    float* padT = pad + plane;
+    dim3 pgrid((np + cbp::PAD_TILE - 1) / cbp::PAD_TILE, (np + cbp::PAD_TILE - 1) / cbp::PAD_TILE, 1);
+    cbp::cbp_pad_sym8_kernel<<<pgrid, dim3(cbp::PAD_TILE, 8), 0, stream>>>(img, pad, padT, g.n, P, np);
+    ++g_launches;
+    cbp::FPParams Pm;
+    Pm.g = to_dev(g);
+    Pm.t = t;
+    Pm.pad = pad;
+    Pm.padT = padT;
+    Pm.np = np;
+    Pm.P = P;
+    Pm.sino = sino;
+    Pm.view_begin = 0;
+    Pm.view_count = g.n_views / 8 + 1;
+    Pm.batch = 8;
+    Pm.sym_stride = 0;
+    Pm.sym_mode = 8;
+    dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, g.n_views / 8 + 1, 1);
+    cbp::cbp_fp_kernel<8><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
     ++g_launches;
     rc = cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
     cudaFreeAsync(pad, stream);
@@ -319,6 +363,11 @@ int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
 int launch_fp(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
               int32_t batch, int32_t v0, int32_t nv, cudaStream_t stream)
 {
+    // FP: the 8-fold kernel needs 128 registers (8 slices x 2 lines); on
+    // sm_100a the 4-fold one is faster, so the FP uses the mirror only when
+    // CBP_FP_MIRROR is set
+    static const bool fp_mirror = getenv("CBP_FP_MIRROR") != nullptr;
+    if (fp_mirror && use_sym8(g, batch, v0, nv)) return launch_fp_sym8(g, t, img, sino, stream);
     if (use_sym4(g, batch, v0, nv)) return launch_fp_sym4(g, t, img, sino, 0, g.n_views / 4, stream);
     if (batch >= 4) return launch_fp_s<4>(g, t, img, sino, batch, v0, nv, stream);
     if (batch >= 2) return launch_fp_s<2>(g, t, img, sino, batch, v0, nv, stream);
@@ -353,11 +402,13 @@ int bp_groups(const cbp_geometry_t& g, int32_t slice_groups, int32_t nv, int slo
 template <int S>
 int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
                 int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream,
-                bool sym = false)
+                int symmode = 0)
 {
     // symmetric: 4 "slices" (the 4 rotated frames) of one image over the base
-    // views [v0, v0 + nv); the sinogram is [4][nv][n_det]
-    if (sym) batch = 4;
+    // views [v0, v0 + nv), sinogram [4][nv][n_det]; or 8 frames (rotations
+    // and mirror) over base views [0, n_views/8], natural sinogram
+    const bool sym = symmode != 0;
+    if (sym) batch = symmode;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -401,7 +452,8 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     P.t = t;
     P.sino = sino;
     P.out = (G > 1 || sym) ? part : img;
-    P.sym_stride = sym ? nv : 0;
+    P.sym_stride = symmode == 4 ? nv : 0;
+    P.sym_mode = symmode;
     P.view_begin = v0;
     P.view_count = nv;
     P.groups = (G > 1 || sym) ? G : 1;
@@ -419,7 +471,12 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     fprintf(stderr, "bp kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
 #endif
     cudaFreeAsync(hdrs, stream);
-    if (sym) {
+    if (symmode == 8) {
+        const int blocks = (int)std::min<size_t>((plane + 255) / 256, (size_t)sms * 8);
+        cbp::cbp_sym8_reduce_kernel<<<blocks, 256, 0, stream>>>(part, img, g.n, G, accumulate ? 1 : 0);
+        ++g_launches;
+        cudaFreeAsync(part, stream);
+    } else if (sym) {
         const int blocks = (int)std::min<size_t>((plane + 255) / 256, (size_t)sms * 8);
         cbp::cbp_sym_reduce_kernel<<<blocks, 256, 0, stream>>>(part, img, g.n, G, accumulate ? 1 : 0);
         ++g_launches;
@@ -437,8 +494,10 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
 int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
               int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream)
 {
+    if (use_sym8(g, batch, v0, nv))
+        return launch_bp_s<8>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8);
     if (use_sym4(g, batch, v0, nv))
-        return launch_bp_s<4>(g, t, sino, img, batch, 0, g.n_views / 4, accumulate, stream, true);
+        return launch_bp_s<4>(g, t, sino, img, batch, 0, g.n_views / 4, accumulate, stream, 4);
     if (batch >= 4) return launch_bp_s<4>(g, t, sino, img, batch, v0, nv, accumulate, stream);
     if (batch >= 2) return launch_bp_s<2>(g, t, sino, img, batch, v0, nv, accumulate, stream);
     return launch_bp_s<1>(g, t, sino, img, batch, v0, nv, accumulate, stream);
@@ -533,7 +592,7 @@ int cbp_symmetry_fold(const cbp_geometry_t* g, int32_t batch, int32_t view_begin
                       int32_t view_count)
 {
     if (cbp_validate(g) != CBP_OK) return CBP_EINVAL;
-    return use_sym4(*g, batch, view_begin, view_count) ? 4 : 1;
+    return use_sym8(*g, batch, view_begin, view_count) ? 8 : (use_sym4(*g, batch, view_begin, view_count) ? 4 : 1);
 }
 
 static int check_orbit(const cbp_geometry_t* g, const void* a, const void* b, int32_t base_begin,
@@ -566,7 +625,7 @@ int cbp_back_orbit(const cbp_geometry_t* g, const float* sino, float* image, int
     cudaStream_t stream = (cudaStream_t)stream_;
     cbp::Tables t;
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
-    return launch_bp_s<4>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, true);
+    return launch_bp_s<4>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 4);
 }
 
 static uint64_t splitmix64(uint64_t& x)

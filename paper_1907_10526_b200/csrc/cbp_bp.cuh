@@ -31,6 +31,8 @@
 // atomics anywhere: the result is deterministic.
 #pragma once
 
+#include <type_traits>
+
 #include "cbp_common.cuh"
 
 namespace cbp {
@@ -49,6 +51,9 @@ struct BPParams {
     // vl + q sym_stride of batch 0 and accumulates the image in the frame
     // rotated by q (combined by cbp_sym_reduce_kernel)
     int sym_stride;
+    // 8: dihedral symmetry, S = 8 frames g = R^q M^m over base views
+    // [0, n_views/8] of the natural sinogram (see cbp_pad_sym8_kernel)
+    int sym_mode;
 };
 
 constexpr int BP_TILE = 32;       // pixels per tile side
@@ -255,18 +260,21 @@ __device__ __forceinline__ void bp_pair(const BPEntry* row, const float* yrow, i
 }
 
 template <int S>
-__device__ __forceinline__ void bp_flush(double* acc_s, int horiz, int e0, int e1, float2 (&a0)[S],
-                                         float2 (&a1)[S])
+using bp_acc_t = typename std::conditional<S == 8, float, double>::type;  // smem budget at S = 8
+
+template <int S>
+__device__ __forceinline__ void bp_flush(bp_acc_t<S>* acc_s, int horiz, int e0, int e1,
+                                         float2 (&a0)[S], float2 (&a1)[S])
 {
     constexpr int LD = BP_TILE + 1, PL = BP_TILE * LD;
     const int i0 = (e0 >> 5) * LD + (e0 & 31), i1 = (e1 >> 5) * LD + (e1 & 31);
     const int st = horiz ? 1 : LD;  // second pixel of a pair
 #pragma unroll
     for (int q = 0; q < S; ++q) {
-        acc_s[q * PL + i0] += (double)a0[q].x;
-        acc_s[q * PL + i0 + st] += (double)a0[q].y;
-        acc_s[q * PL + i1] += (double)a1[q].x;
-        acc_s[q * PL + i1 + st] += (double)a1[q].y;
+        acc_s[q * PL + i0] += (bp_acc_t<S>)a0[q].x;
+        acc_s[q * PL + i0 + st] += (bp_acc_t<S>)a0[q].y;
+        acc_s[q * PL + i1] += (bp_acc_t<S>)a1[q].x;
+        acc_s[q * PL + i1 + st] += (bp_acc_t<S>)a1[q].y;
         a0[q] = a1[q] = make_float2(0.f, 0.f);
     }
 }
@@ -276,7 +284,7 @@ __host__ __device__ constexpr size_t bp_smem_bytes(int S)
 {
     return sizeof(BPEntry) * BP_VC * BP_NB + sizeof(BPHeader) * BP_VC +
            (S > 1 ? sizeof(float) * BP_VC * BP_NB * S : 0) +
-           sizeof(double) * S * BP_TILE * (BP_TILE + 1);
+           (S == 8 ? sizeof(float) : sizeof(double)) * S * BP_TILE * (BP_TILE + 1);
 }
 
 template <int S>
@@ -287,8 +295,8 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
     BPHeader* hdr = reinterpret_cast<BPHeader*>(smem + sizeof(BPEntry) * BP_VC * BP_NB);
     float* ytab = reinterpret_cast<float*>(smem + sizeof(BPEntry) * BP_VC * BP_NB +
                                            sizeof(BPHeader) * BP_VC);  // [VC][NB][S] (S > 1)
-    double* acc_s = reinterpret_cast<double*>(smem + bp_smem_bytes(S) -
-                                              sizeof(double) * S * BP_TILE * (BP_TILE + 1));
+    bp_acc_t<S>* acc_s = reinterpret_cast<bp_acc_t<S>*>(
+        smem + bp_smem_bytes(S) - sizeof(bp_acc_t<S>) * S * BP_TILE * (BP_TILE + 1));
 
     const GeomDev& g = P.g;
     const int tid = threadIdx.x;
@@ -302,7 +310,7 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
     const BPHeader* hsrc = P.hdrs + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * P.view_count + vg0;
     const size_t sino_plane = (size_t)P.view_count * g.n_det;
 
-    for (int i = tid; i < S * BP_TILE * (BP_TILE + 1); i += BP_THREADS) acc_s[i] = 0.0;
+    for (int i = tid; i < S * BP_TILE * (BP_TILE + 1); i += BP_THREADS) acc_s[i] = 0;
 
     for (int vc = 0; vc < vgn; vc += BP_VC) {
         const int nvc = min(BP_VC, vgn - vc);
@@ -331,11 +339,20 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
 #pragma unroll
                             for (int q = 0; q < S; ++q) {
                                 const int b = sg * S + q;
-                                const float* ys = P.sym_stride > 0
-                                    ? P.sino + (size_t)q * P.sym_stride * g.n_det
-                                    : P.sino + (size_t)b * sino_plane;
-                                ytab[(vi * BP_NB + jj) * S + q] =
-                                    (P.sym_stride > 0 || b < P.batch) ? __ldg(ys + yo) * hA : 0.0f;
+                                float yv;
+                                if (P.sym_mode == 8) {  // frame (qq, m): view_g(v), bin_m(j)
+                                    const int N = g.n_views, v = P.view_begin + vg0 + vc + vi;
+                                    const int m = q >> 2, qq = q & 3;
+                                    const int view = ((m ? N - v : v) + qq * (N / 4)) % N;
+                                    const int bin = m ? g.n_det - 1 - j : j;
+                                    yv = (m && (v == 0 || 8 * v == N)) ? 0.0f
+                                                                       : __ldg(P.sino + (size_t)view * g.n_det + bin);
+                                } else if (P.sym_stride > 0) {
+                                    yv = __ldg(P.sino + (size_t)q * P.sym_stride * g.n_det + yo);
+                                } else {
+                                    yv = b < P.batch ? __ldg(P.sino + (size_t)b * sino_plane + yo) : 0.0f;
+                                }
+                                ytab[(vi * BP_NB + jj) * S + q] = yv * hA;
                             }
                         }
                     }
@@ -437,6 +454,29 @@ __global__ void cbp_sym_reduce_kernel(const float* __restrict__ part, float* __r
         for (int gi = 0; gi < groups; ++gi)
 #pragma unroll
             for (int q = 0; q < 4; ++q) s += part[((size_t)gi * 4 + q) * plane + src[q]];
+        out[i] = s;
+    }
+}
+
+// dihedral BP: out[k] = (accumulate ? out[k] : 0) + sum_g sum_f part[g][f][g_f^-1 k],
+// g_f = R^q M^m (f = 4 m + q), g_f^-1 k = M^m R^-q k, fixed order
+__global__ void cbp_sym8_reduce_kernel(const float* __restrict__ part, float* __restrict__ out, int n,
+                                       int groups, int accumulate)
+{
+    const size_t plane = (size_t)n * n;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < plane;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / n), c = (int)(i % n);
+        // R^-q (r, c): q = 0 (r, c), 1 (c, n-1-r), 2 (n-1-r, n-1-c), 3 (n-1-c, r); then M: row -> n-1-row
+        const int rq[4] = {r, c, n - 1 - r, n - 1 - c}, cq[4] = {c, n - 1 - r, n - 1 - c, r};
+        float s = accumulate ? out[i] : 0.0f;
+        for (int gi = 0; gi < groups; ++gi)
+#pragma unroll
+            for (int f = 0; f < 8; ++f) {
+                const int q = f & 3;
+                const int rr = f >= 4 ? n - 1 - rq[q] : rq[q];
+                s += part[((size_t)gi * 8 + f) * plane + (size_t)rr * n + cq[q]];
+            }
         out[i] = s;
     }
 }

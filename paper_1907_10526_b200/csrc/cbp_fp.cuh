@@ -43,6 +43,9 @@ struct FPParams {
     // slices are the image rotated by 0, 90, 180, 270 degrees and slice q of
     // base view vl is view vl + q sym_stride of the single output sinogram
     int sym_stride;
+    // 8: the full dihedral symmetry (S = 8, cbp_pad_sym8_kernel) over base
+    // views [0, n_views/8], output the natural [n_views][n_det] sinogram
+    int sym_mode;
 };
 
 constexpr int FP_BLOCK = 128;
@@ -125,6 +128,50 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym4_kernel(const float*
         if (r < np && c < np) {
             const float* t = tile[threadIdx.x][cc];
             *reinterpret_cast<float4*>(padT + ((size_t)c * np + r) * 4) = make_float4(t[0], t[1], t[2], t[3]);
+        }
+    }
+}
+
+// The mirror M: (x, y) -> (x, -y) maps view theta to -theta and detector
+// coordinate s to -s (bin j to N_s-1-j), and pixel (r, c) to (n-1-r, c).  With
+// the rotations it gives 8 frames g = R^q M^m:  W(view_g(v), bin_m(j), g k) =
+// W(v, j, k), view_g(v) = (m ? n_views - v : v) + q n_views/4 (mod n_views),
+// so y[view_g(v)][bin_m(j)] = sum_k c[g k] W(v, j, k): slice 4m + q of the
+// padded copy holds c o (R^q M^m).  Base views v in [0, n_views/8]; for v = 0
+// and v = n_views/8 the mirrored frames repeat the rotated ones.
+__global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym8_kernel(const float* __restrict__ img,
+                                                                    float* __restrict__ pad,
+                                                                    float* __restrict__ padT, int n,
+                                                                    int P, int np)
+{
+    __shared__ float tile[PAD_TILE][PAD_TILE + 1][8];
+    const int r0 = blockIdx.y * PAD_TILE, c0 = blockIdx.x * PAD_TILE;
+    for (int rr = threadIdx.y; rr < PAD_TILE; rr += 8) {
+        const int r = r0 + rr, c = c0 + threadIdx.x;
+        const int sr = r - P, sc = c - P;
+        const bool in = sr >= 0 && sr < n && sc >= 0 && sc < n;
+        float v[8];
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+            int a = f >= 4 ? n - 1 - sr : sr, b = sc;  // M first, then R^q
+            rot90_pow(n, f & 3, a, b);
+            v[f] = in ? img[(size_t)a * n + b] : 0.0f;
+            tile[rr][threadIdx.x][f] = v[f];
+        }
+        if (r < np && c < np) {
+            float4* d = reinterpret_cast<float4*>(pad + ((size_t)r * np + c) * 8);
+            d[0] = make_float4(v[0], v[1], v[2], v[3]);
+            d[1] = make_float4(v[4], v[5], v[6], v[7]);
+        }
+    }
+    __syncthreads();
+    for (int cc = threadIdx.y; cc < PAD_TILE; cc += 8) {
+        const int c = c0 + cc, r = r0 + threadIdx.x;
+        if (r < np && c < np) {
+            const float* t = tile[threadIdx.x][cc];
+            float4* d = reinterpret_cast<float4*>(padT + ((size_t)c * np + r) * 8);
+            d[0] = make_float4(t[0], t[1], t[2], t[3]);
+            d[1] = make_float4(t[4], t[5], t[6], t[7]);
         }
     }
 }
@@ -444,7 +491,13 @@ __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_f
 #pragma unroll
         for (int q = 0; q < S; ++q) {
             const int b = grp * S + q;
-            if (P.sym_stride > 0)
+            if (P.sym_mode == 8) {
+                const int N = g.n_views, m = q >> 2, qq = q & 3;
+                if (m && (v == 0 || 8 * v == N)) continue;  // mirrored frame repeats a rotation
+                const int view = ((m ? N - v : v) + qq * (N / 4)) % N;
+                const int bin = m ? g.n_det - 1 - j : j;
+                P.sino[(size_t)view * g.n_det + bin] = (float)acc[q * FP_BLOCK];
+            } else if (P.sym_stride > 0)
                 P.sino[((size_t)vl + (size_t)q * P.sym_stride) * g.n_det + j] = (float)acc[q * FP_BLOCK];
             else if (b < P.batch)
                 P.sino[((size_t)b * P.view_count + vl) * g.n_det + j] = (float)acc[q * FP_BLOCK];

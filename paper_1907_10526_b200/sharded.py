@@ -58,6 +58,8 @@ class Shard:
 
 
 def make_shard(n_views: int, rank: int, world: int, batch: int = 1) -> Shard:
+    if world == 1:  # the whole scan: the library picks its widest symmetry itself
+        return Shard("block", 0, n_views, n_views)
     if batch == 1 and n_views % 4 == 0 and n_views // 4 >= world:
         b0, nb = view_shard(n_views // 4, rank, world)
         return Shard("orbit", b0, nb, n_views)

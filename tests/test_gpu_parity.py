@@ -263,13 +263,15 @@ def test_batched_config4_sampled(torch_cuda):
         _assert_parity(c[b, rows, cols], O.back_pixels(g, y[b], rows, cols), f"BP cfg4 slice {b}")
 
 
-@pytest.mark.parametrize("n_views", [88, 360])
-def test_rotational_symmetry_path(torch_cuda, n_views):
-    """A full scan with N_v % 4 == 0 and one image runs the 4-fold symmetric
-    path (one weight for views v, v+N/4, v+N/2, v+3N/4); partial view ranges
-    run the direct path.  Both must match the oracle, and each other."""
+@pytest.mark.parametrize("n_views,fold", [(88, 8), (92, 4), (360, 8)])
+def test_rotational_symmetry_path(torch_cuda, n_views, fold):
+    """A full scan with one image runs the symmetric path -- 8-fold (rotations
+    and mirror) when N_v % 8 == 0, 4-fold (rotations) when N_v % 4 == 0 --
+    partial view ranges run the direct path.  Both must match the oracle,
+    and each other."""
     torch = torch_cuda
     g = dict(W.geometry("1"), n_views=n_views)
+    assert cbp.symmetry_fold(g) == fold
     img = W.shepp_logan(g["n"])
     y_sym = _fp(torch, g, img)                       # full range: symmetric
     y_a = _fp(torch, g, img, view_begin=0, view_count=n_views // 2)
@@ -320,3 +322,14 @@ def test_orbit_shards_sum_to_full(torch_cuda):
     for v in (int(sh.views()[0]), int(sh.views()[-1])):
         _assert_parity(full_y[v].cpu().numpy(), O.forward(g, W.shepp_logan(g["n"]), v, 1)[0],
                        f"FP view {v}")
+
+
+def test_symmetry_ragged_odd_grid(torch_cuda):
+    """8-fold path on an odd, ragged grid (n = 37: the pixel rotations and the
+    mirror must map the grid onto itself exactly)."""
+    g = dict(EDGE["ragged"], n_views=16)
+    assert cbp.symmetry_fold(g) == 8
+    img = W.random_image(g["n"], 9)
+    _assert_parity(_fp(torch_cuda, g, img), O.forward(g, img), "FP ragged sym8")
+    y = W.random_sino(g["n_views"], g["n_det"], 109)
+    _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), "BP ragged sym8")

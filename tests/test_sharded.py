@@ -35,6 +35,7 @@ def test_shards_cover_every_view_once(n_views, world):
     assert sorted(views.tolist()) == list(range(n_views))
     modes = {sharded.make_shard(n_views, r, world).mode for r in range(world)}
     assert modes == ({"orbit"} if n_views % 4 == 0 and n_views // 4 >= world else {"block"})
+    assert sharded.make_shard(n_views, 0, 1).views().tolist() == list(range(n_views))
     assert sharded.make_shard(n_views, 0, world, batch=3).mode == "block"
 
 
