@@ -117,6 +117,30 @@ int cbp_forward_orbit(const cbp_geometry_t* g, const float* image, float* sino,
 int cbp_back_orbit(const cbp_geometry_t* g, const float* sino, float* image,
                    int32_t base_begin, int32_t base_count, int32_t accumulate, void* stream);
 
+/* ---- Row f1: building blocks of the iterative loops (SART, CGLS) around
+ * the projector.  Device pointers, FP32 vectors of `count` elements,
+ * stream-ordered; CBP_EINVAL for null pointers or negative counts.
+ *
+ * SART (the simultaneous ART step used inside ASD-POCS):
+ *   c <- c + beta A^T((y - A c) ./ A1) ./ A^T 1, zero where a weight sum <= 1e-12,
+ *   optionally clamped to c >= 0.                                            */
+int cbp_sart_residual(const float* y, const float* ay, const float* rowsum, float* r,
+                      int64_t count, void* stream);   /* r = (y - ay) ./ rowsum       */
+int cbp_sart_update(float* c, const float* bp, const float* colsum, float beta,
+                    int32_t nonneg, int64_t count, void* stream);  /* c += beta bp ./ colsum */
+int cbp_fill(float* x, float value, int64_t count, void* stream);
+/* <a, b> into the DEVICE double *out: deterministic two-stage FP64 sum.    */
+int cbp_dot(const float* a, const float* b, int64_t count, double* out, void* stream);
+/* CGLS (conjugate gradients on A^T A x = A^T y) with device-resident FP64
+ * scalars, so an iteration never waits for the host:
+ *   cbp_cgls_step:       x += (num/den) p (nx elements), r -= (num/den) q (nr)
+ *   cbp_cgls_direction:  p = s + (num/den) p
+ * (den == 0 leaves the vectors unchanged).                                  */
+int cbp_cgls_step(float* x, const float* p, float* r, const float* q, const double* num,
+                  const double* den, int64_t nx, int64_t nr, void* stream);
+int cbp_cgls_direction(float* p, const float* s, const double* num, const double* den,
+                       int64_t count, void* stream);
+
 /* Adjoint identity check on the current device (synchronous): draws seeded
  * c, y ~ U[0,1) (splitmix64), runs cbp_forward and cbp_back over all views,
  * and returns |<Ac,y> - <c,A^T y>| / |<Ac,y>| with FP64 inner products in

@@ -23,8 +23,9 @@ CBP_OK, CBP_EINVAL, CBP_ECUDA, CBP_ENOMEM = 0, -1, -2, -3
 
 # names declared in include/cbp.h
 ABI_FUNCTIONS = ("cbp_validate", "cbp_forward", "cbp_back", "cbp_symmetry_fold",
-                 "cbp_forward_orbit", "cbp_back_orbit", "cbp_adjoint_check", "cbp_strerror",
-                 "cbp_version", "cbp_launch_count")
+                 "cbp_forward_orbit", "cbp_back_orbit", "cbp_sart_residual", "cbp_sart_update",
+                 "cbp_fill", "cbp_dot", "cbp_cgls_step", "cbp_cgls_direction", "cbp_adjoint_check",
+                 "cbp_strerror", "cbp_version", "cbp_launch_count")
 
 
 class CbpError(RuntimeError):
@@ -91,6 +92,16 @@ def lib() -> ctypes.CDLL:
         L.cbp_forward_orbit.restype = ctypes.c_int
         L.cbp_back_orbit.argtypes = [G, fp, fp, i32, i32, i32, vp]
         L.cbp_back_orbit.restype = ctypes.c_int
+        i64 = ctypes.c_int64
+        L.cbp_sart_residual.argtypes = [fp, fp, fp, fp, i64, vp]
+        L.cbp_sart_update.argtypes = [fp, fp, fp, ctypes.c_float, i32, i64, vp]
+        L.cbp_fill.argtypes = [fp, ctypes.c_float, i64, vp]
+        L.cbp_dot.argtypes = [fp, fp, i64, fp, vp]
+        L.cbp_cgls_step.argtypes = [fp, fp, fp, fp, fp, fp, i64, i64, vp]
+        L.cbp_cgls_direction.argtypes = [fp, fp, fp, fp, i64, vp]
+        for name in ("cbp_sart_residual", "cbp_sart_update", "cbp_fill", "cbp_dot",
+                     "cbp_cgls_step", "cbp_cgls_direction"):
+            getattr(L, name).restype = ctypes.c_int
         L.cbp_adjoint_check.argtypes = [G, ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]
         L.cbp_adjoint_check.restype = ctypes.c_int
         L.cbp_strerror.argtypes = [ctypes.c_int]
@@ -241,6 +252,56 @@ def back_orbit(geom, sino, base_begin: int, image=None, accumulate: bool = False
     if rc != CBP_OK:
         raise CbpError(rc, "cbp_back_orbit")
     return image
+
+
+# ---- row f1 building blocks (device tensors, current stream) ---------------
+def _dev(t):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.is_contiguous()):
+        raise ValueError("expected a contiguous CUDA tensor")
+    return t.data_ptr()
+
+
+def _stream():
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _call(name, *args):
+    rc = getattr(lib(), name)(*args, _stream())
+    if rc != CBP_OK:
+        raise CbpError(rc, name)
+
+
+def sart_residual(y, ay, rowsum, r):
+    _call("cbp_sart_residual", _dev(y), _dev(ay), _dev(rowsum), _dev(r), y.numel())
+    return r
+
+
+def sart_update(c, bp, colsum, beta: float = 1.0, nonneg: bool = True):
+    _call("cbp_sart_update", _dev(c), _dev(bp), _dev(colsum), ctypes.c_float(beta),
+          1 if nonneg else 0, c.numel())
+    return c
+
+
+def fill(x, value: float):
+    _call("cbp_fill", _dev(x), ctypes.c_float(value), x.numel())
+    return x
+
+
+def dot(a, b, out):
+    """<a, b> into the device float64 tensor `out` (shape [1])."""
+    _call("cbp_dot", _dev(a), _dev(b), a.numel(), _dev(out))
+    return out
+
+
+def cgls_step(x, p, r, q, num, den):
+    _call("cbp_cgls_step", _dev(x), _dev(p), _dev(r), _dev(q), _dev(num), _dev(den), x.numel(),
+          r.numel())
+
+
+def cgls_direction(p, s, num, den):
+    _call("cbp_cgls_direction", _dev(p), _dev(s), _dev(num), _dev(den), p.numel())
 
 
 def adjoint_check(geom, seed: int = 0) -> float:

@@ -19,6 +19,7 @@
 #include "cbp_common.cuh"
 #include "cbp_fp.cuh"
 #include "cbp_tables.cuh"
+#include "cbp_vec.cuh"
 
 namespace {
 
@@ -626,6 +627,83 @@ int cbp_back_orbit(const cbp_geometry_t* g, const float* sino, float* image, int
     cbp::Tables t;
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
     return launch_bp_s<4>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 4);
+}
+
+// ---- row f1: SART / CGLS building blocks ---------------------------------
+static int vec_grid(int64_t count)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t b = (count + cbp::VEC_BLOCK - 1) / cbp::VEC_BLOCK;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)sms * 8));
+}
+
+static int launched()
+{
+    ++g_launches;
+    return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+}
+
+int cbp_sart_residual(const float* y, const float* ay, const float* rowsum, float* r, int64_t count,
+                      void* stream)
+{
+    if (!y || !ay || !rowsum || !r || count < 0) return CBP_EINVAL;
+    if (count == 0) return CBP_OK;
+    cbp::cbp_sart_residual_kernel<<<vec_grid(count), cbp::VEC_BLOCK, 0, (cudaStream_t)stream>>>(
+        y, ay, rowsum, r, count);
+    return launched();
+}
+
+int cbp_sart_update(float* c, const float* bp, const float* colsum, float beta, int32_t nonneg,
+                    int64_t count, void* stream)
+{
+    if (!c || !bp || !colsum || count < 0 || !std::isfinite(beta)) return CBP_EINVAL;
+    if (count == 0) return CBP_OK;
+    cbp::cbp_sart_update_kernel<<<vec_grid(count), cbp::VEC_BLOCK, 0, (cudaStream_t)stream>>>(
+        c, bp, colsum, beta, nonneg ? 1 : 0, count);
+    return launched();
+}
+
+int cbp_fill(float* x, float value, int64_t count, void* stream)
+{
+    if (!x || count < 0) return CBP_EINVAL;
+    if (count == 0) return CBP_OK;
+    cbp::cbp_fill_kernel<<<vec_grid(count), cbp::VEC_BLOCK, 0, (cudaStream_t)stream>>>(x, value, count);
+    return launched();
+}
+
+int cbp_dot(const float* a, const float* b, int64_t count, double* out, void* stream_)
+{
+    if (!a || !b || !out || count < 0) return CBP_EINVAL;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    double* part = nullptr;
+    int rc = scratch_alloc((void**)&part, sizeof(double) * cbp::DOT_BLOCKS, stream);
+    if (rc != CBP_OK) return rc;
+    cbp::cbp_dot_partial_kernel<<<cbp::DOT_BLOCKS, cbp::VEC_BLOCK, 0, stream>>>(a, b, count, part);
+    ++g_launches;
+    cbp::cbp_dot_final_kernel<<<1, cbp::VEC_BLOCK, 0, stream>>>(part, cbp::DOT_BLOCKS, out);
+    rc = launched();
+    cudaFreeAsync(part, stream);
+    return rc;
+}
+
+int cbp_cgls_step(float* x, const float* p, float* r, const float* q, const double* num,
+                  const double* den, int64_t nx, int64_t nr, void* stream)
+{
+    if (!x || !p || !r || !q || !num || !den || nx < 0 || nr < 0) return CBP_EINVAL;
+    cbp::cbp_cgls_step_kernel<<<vec_grid(std::max(nx, nr)), cbp::VEC_BLOCK, 0, (cudaStream_t)stream>>>(
+        x, p, r, q, num, den, nx, nr);
+    return launched();
+}
+
+int cbp_cgls_direction(float* p, const float* s, const double* num, const double* den, int64_t count,
+                       void* stream)
+{
+    if (!p || !s || !num || !den || count < 0) return CBP_EINVAL;
+    cbp::cbp_cgls_dir_kernel<<<vec_grid(count), cbp::VEC_BLOCK, 0, (cudaStream_t)stream>>>(
+        p, s, num, den, count);
+    return launched();
 }
 
 static uint64_t splitmix64(uint64_t& x)
