@@ -235,6 +235,9 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
     const float2 AC = make_float2(-R.A * R.invC, -R.A * R.invC);
     const float dzC = R.dz * R.invC, dzC2 = dzC - R.tq * R.invC, dr = R.tq - R.dz;
     for (int i = i0; i <= i1;) {
+        // S == 1: acc[0] = (line a, line b).  S >= 2: acc[q2] = slices (2 q2, 2 q2 + 1) of
+        // line a, acc[S/2 + q2] the same of line b -- the packed operands are then the
+        // register pairs of the pixel loads (no moves to pair up the two lines)
         float2 acc[S];
 #pragma unroll
         for (int q = 0; q < S; ++q) acc[q] = make_float2(0.0f, 0.0f);
@@ -311,12 +314,23 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
                 } else {  // one weight, S slices
                     const float2 w = __fmul2_rn(num, rcp2(B));
 #pragma unroll
-                    for (int q = 0; q < S; ++q) acc[q] = __ffma2_rn(make_float2(ca[q], cb[q]), w, acc[q]);
+                    for (int q = 0; q < S; q += 2) {
+                        acc[q / 2] = __ffma2_rn(make_float2(ca[q], ca[q + 1]), make_float2(w.x, w.x), acc[q / 2]);
+                        acc[S / 2 + q / 2] = __ffma2_rn(make_float2(cb[q], cb[q + 1]), make_float2(w.y, w.y),
+                                                        acc[S / 2 + q / 2]);
+                    }
                 }
             }
         }
+        if constexpr (S == 1) {
+            out[0] += (double)acc[0].x + (double)acc[0].y;  // two-level sum
+        } else {
 #pragma unroll
-        for (int q = 0; q < S; ++q) out[q * FP_BLOCK] += (double)acc[q].x + (double)acc[q].y;  // two-level sum
+            for (int q = 0; q < S; q += 2) {
+                out[q * FP_BLOCK] += (double)acc[q / 2].x + (double)acc[S / 2 + q / 2].x;
+                out[(q + 1) * FP_BLOCK] += (double)acc[q / 2].y + (double)acc[S / 2 + q / 2].y;
+            }
+        }
     }
 }
 
