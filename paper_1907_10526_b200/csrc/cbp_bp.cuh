@@ -225,8 +225,9 @@ __device__ __forceinline__ float2 bp_weight(const BPEntry* e, float dc, float dr
 }
 
 // entries row[jl - base .. jh - base]; empty when jh < jl (no pointer is
-// formed outside the row: the trip count is an integer).  S slices: the
-// y h^2/A of slice q is ys[entry * S + q] (S > 1) or entry.c.w (S == 1).
+// formed outside the row: the trip count is an integer).  S == 1: the entry's
+// c.w is y h^2/A.  S > 1: c.w is h^2/A and the S raw y values of the entry
+// are yrow[entry * S + q] (staged from the sinogram by bp_y_load).
 template <int S>
 __device__ __forceinline__ void bp_pair(const BPEntry* row, const float* yrow, int jl, int jh,
                                         int base, float dc, float dr, float2 (&acc)[S])
@@ -237,30 +238,36 @@ __device__ __forceinline__ void bp_pair(const BPEntry* row, const float* yrow, i
     const BPEntry* e = row + (jl - base);
     const float* ys = yrow + (jl - base) * S;
     for (int k = 0; k < cnt; ++k, ++e, ys += S) {
-        const float2 w = bp_weight(e, dc, dr);
         if constexpr (S == 1) {
+            const float2 w = bp_weight(e, dc, dr);
             const float yw = e->c.w;
             acc[0] = __ffma2_rn(make_float2(yw, yw), w, acc[0]);
-        } else if constexpr (S == 2) {
-            const float2 y2 = *reinterpret_cast<const float2*>(ys);
-            acc[0] = __ffma2_rn(make_float2(y2.x, y2.x), w, acc[0]);
-            acc[1] = __ffma2_rn(make_float2(y2.y, y2.y), w, acc[1]);
         } else {
-            static_assert(S % 4 == 0, "S is 1, 2 or a multiple of 4");
+            const float hA = e->c.w;
+            const float2 w = __fmul2_rn(bp_weight(e, dc, dr), make_float2(hA, hA));
+            if constexpr (S == 2) {
+                const float2 y2 = *reinterpret_cast<const float2*>(ys);
+                acc[0] = __ffma2_rn(make_float2(y2.x, y2.x), w, acc[0]);
+                acc[1] = __ffma2_rn(make_float2(y2.y, y2.y), w, acc[1]);
+            } else {
+                static_assert(S % 4 == 0, "S is 1, 2 or a multiple of 4");
 #pragma unroll
-            for (int q = 0; q < S; q += 4) {
-                const float4 y4 = *reinterpret_cast<const float4*>(ys + q);
-                acc[q] = __ffma2_rn(make_float2(y4.x, y4.x), w, acc[q]);
-                if (q + 1 < S) acc[q + 1] = __ffma2_rn(make_float2(y4.y, y4.y), w, acc[q + 1]);
-                if (q + 2 < S) acc[q + 2] = __ffma2_rn(make_float2(y4.z, y4.z), w, acc[q + 2]);
-                if (q + 3 < S) acc[q + 3] = __ffma2_rn(make_float2(y4.w, y4.w), w, acc[q + 3]);
+                for (int q = 0; q < S; q += 4) {
+                    const float4 y4 = *reinterpret_cast<const float4*>(ys + q);
+                    acc[q] = __ffma2_rn(make_float2(y4.x, y4.x), w, acc[q]);
+                    acc[q + 1] = __ffma2_rn(make_float2(y4.y, y4.y), w, acc[q + 1]);
+                    acc[q + 2] = __ffma2_rn(make_float2(y4.z, y4.z), w, acc[q + 2]);
+                    acc[q + 3] = __ffma2_rn(make_float2(y4.w, y4.w), w, acc[q + 3]);
+                }
             }
         }
     }
 }
 
+// per-tile accumulators: FP64 for S <= 2, FP32 for S >= 4 (shared-memory
+// budget; each term is already a partial over a run of views)
 template <int S>
-using bp_acc_t = typename std::conditional<S == 8, float, double>::type;  // smem budget at S = 8
+using bp_acc_t = typename std::conditional<(S >= 4), float, double>::type;
 
 template <int S>
 __device__ __forceinline__ void bp_flush(bp_acc_t<S>* acc_s, int horiz, int e0, int e1,
@@ -279,22 +286,89 @@ __device__ __forceinline__ void bp_flush(bp_acc_t<S>* acc_s, int horiz, int e0, 
     }
 }
 
-// dynamic shared memory of the BP kernel for S slices
+// header buffers: S > 1 keeps three chunks of headers in flight (current,
+// next, the one after), S == 1 one
+__host__ __device__ constexpr int bp_hdr_bufs(int S) { return S > 1 ? 3 : 1; }
+
+// dynamic shared memory of the BP kernel for S slices: entries, headers,
+// (S > 1) two y buffers [2][VC][NB][S], tile accumulators [S][32][33]
 __host__ __device__ constexpr size_t bp_smem_bytes(int S)
 {
-    return sizeof(BPEntry) * BP_VC * BP_NB + sizeof(BPHeader) * BP_VC +
-           (S > 1 ? sizeof(float) * BP_VC * BP_NB * S : 0) +
-           (S == 8 ? sizeof(float) : sizeof(double)) * S * BP_TILE * (BP_TILE + 1);
+    return sizeof(BPEntry) * BP_VC * BP_NB + sizeof(BPHeader) * BP_VC * bp_hdr_bufs(S) +
+           (S > 1 ? 2 * sizeof(float) * BP_VC * BP_NB * S : 0) +
+           (S >= 4 ? sizeof(float) : sizeof(double)) * S * BP_TILE * (BP_TILE + 1);
+}
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// S > 1: the raw y values of one chunk (views vl0 .. vl0 + nvc - 1 of this
+// CTA, bins jlo + pass NB + jj of each, all S frames / slices) into
+// ybuf[VC][NB][S] -- asynchronously (cp.async, overlapping the previous
+// chunk's compute) or with plain loads (later passes of a wide bin range).
+// Four .. sixteen threads per (view, slice) walk its bins.
+template <int S>
+__device__ __forceinline__ void bp_y_load(const BPParams& P, int vl0, int nvc, int pass,
+                                          const BPHeader* H, float* ybuf, bool async)
+{
+    const GeomDev& g = P.g;
+    constexpr int TPC = BP_THREADS / (BP_VC * S);  // threads per (view, slice)
+    static_assert(TPC >= 1 && BP_THREADS % (BP_VC * S) == 0, "BP_VC * S must divide the CTA");
+    const int tid = threadIdx.x;
+    const int combo = tid / TPC, sub = tid % TPC;
+    const int vi = combo / S, q = combo % S;
+    if (vi >= nvc) return;
+    const BPHeader& h = H[vi];
+    const int j0 = h.jlo + pass * BP_NB;
+    const int cnt = min(h.jhi - j0 + 1, BP_NB);
+    const int vl = vl0 + vi;
+    const float* src = nullptr;
+    int dir = 1;
+    if (P.sym_mode == 8) {  // frame (qq, m) of base view v: view_g(v), bin_m(j)
+        const int N = g.n_views, v = P.view_begin + vl, m = q >> 2, qq = q & 3;
+        int view = (m ? N - v : v) + qq * (N / 4);
+        if (view >= N) view -= N;  // 0 <= v <= N/8
+        if (!(m && (v == 0 || 8 * v == N))) {  // else the mirrored frame repeats a rotation: y = 0
+            src = P.sino + (size_t)view * g.n_det + (m ? g.n_det - 1 - j0 : j0);
+            dir = m ? -1 : 1;
+        }
+    } else if (P.sym_stride > 0) {
+        src = P.sino + ((size_t)q * P.sym_stride + vl) * g.n_det + j0;
+    } else {
+        const int b = blockIdx.z / P.groups * S + q;
+        if (b < P.batch) src = P.sino + ((size_t)b * P.view_count + vl) * g.n_det + j0;
+    }
+    float* dst = ybuf + (size_t)vi * BP_NB * S + q;
+    for (int jj = sub; jj < cnt; jj += TPC) {
+        CBP_CHECK(j0 + jj >= 0 && j0 + jj < g.n_det, "y_load j=%d\n", j0 + jj);
+        if (!src)
+            dst[jj * S] = 0.0f;
+        else if (async)
+            cp_async4(dst + jj * S, src + dir * jj);
+        else
+            dst[jj * S] = __ldg(src + dir * jj);
+    }
 }
 
 template <int S>
 __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp_bp_kernel(const BPParams P)
 {
+    constexpr bool STAGE = S > 1;  // y staged asynchronously one chunk ahead
+    constexpr int HB = bp_hdr_bufs(S);
     extern __shared__ __align__(16) unsigned char smem[];
     BPEntry(*tab)[BP_NB] = reinterpret_cast<BPEntry(*)[BP_NB]>(smem);
-    BPHeader* hdr = reinterpret_cast<BPHeader*>(smem + sizeof(BPEntry) * BP_VC * BP_NB);
-    float* ytab = reinterpret_cast<float*>(smem + sizeof(BPEntry) * BP_VC * BP_NB +
-                                           sizeof(BPHeader) * BP_VC);  // [VC][NB][S] (S > 1)
+    BPHeader* hdr_all = reinterpret_cast<BPHeader*>(smem + sizeof(BPEntry) * BP_VC * BP_NB);  // [HB][VC]
+    float* ytab_all = reinterpret_cast<float*>(hdr_all + HB * BP_VC);  // [2][VC][NB][S] (S > 1)
     bp_acc_t<S>* acc_s = reinterpret_cast<bp_acc_t<S>*>(
         smem + bp_smem_bytes(S) - sizeof(bp_acc_t<S>) * S * BP_TILE * (BP_TILE + 1));
 
@@ -303,24 +377,59 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
     const int col0 = blockIdx.x * BP_TILE, row0 = blockIdx.y * BP_TILE;
     const int grp = blockIdx.z % P.groups, sg = blockIdx.z / P.groups;  // view group, slice group
     const int vg0 = grp * P.views_per_group;
-    const int vgn = min(P.views_per_group, P.view_count - vg0);
+    const int vgn = max(0, min(P.views_per_group, P.view_count - vg0));
+    const int nchunks = (vgn + BP_VC - 1) / BP_VC;
     float hcx, hcy;  // anchor k_a = centre of the tile's valid pixels
     double kax, kay;
     bp_tile_anchor(g, blockIdx.x, blockIdx.y, hcx, hcy, kax, kay);
     const BPHeader* hsrc = P.hdrs + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * P.view_count + vg0;
     const size_t sino_plane = (size_t)P.view_count * g.n_det;
+    constexpr int HW = sizeof(BPHeader) / 16;  // 16-byte words per header
+    auto hdr_buf = [&](int c) { return hdr_all + (c % HB) * BP_VC; };
+    auto y_buf = [&](int c) { return ytab_all + (c & 1) * (BP_VC * BP_NB * S); };
+    auto hdr_copy = [&](int c) {  // chunk c's headers (async)
+        const int nvc = min(BP_VC, vgn - c * BP_VC);
+        if (tid < nvc * HW)
+            cp_async16(reinterpret_cast<int4*>(hdr_buf(c)) + tid, reinterpret_cast<const int4*>(hsrc + c * BP_VC) + tid);
+    };
 
     for (int i = tid; i < S * BP_TILE * (BP_TILE + 1); i += BP_THREADS) acc_s[i] = 0;
 
-    for (int vc = 0; vc < vgn; vc += BP_VC) {
+    if constexpr (STAGE) {
+        if (nchunks > 0) {
+            hdr_copy(0);
+            if (nchunks > 1) hdr_copy(1);
+            cp_async_commit();
+            cp_async_wait_all();
+            __syncthreads();
+            bp_y_load<S>(P, vg0, min(BP_VC, vgn), 0, hdr_buf(0), y_buf(0), true);
+            cp_async_commit();
+        }
+    }
+    for (int c = 0; c < nchunks; ++c) {
+        const int vc = c * BP_VC;
         const int nvc = min(BP_VC, vgn - vc);
-        constexpr int HW = sizeof(BPHeader) / 16;  // 16-byte words per header
-        if (tid < nvc * HW)
-            reinterpret_cast<int4*>(hdr)[tid] = __ldg(reinterpret_cast<const int4*>(hsrc + vc) + tid);
-        __syncthreads();
+        BPHeader* hdr = hdr_buf(c);
+        float* ytab = y_buf(c);
+        if constexpr (STAGE) {
+            // chunk c's headers and y, chunk c+1's headers have landed, and every
+            // thread is done with chunk c-1 (whose buffers are refilled next)
+            cp_async_wait_all();
+            __syncthreads();
+            if (c + 2 < nchunks) hdr_copy(c + 2);
+            if (c + 1 < nchunks)
+                bp_y_load<S>(P, vg0 + vc + BP_VC, min(BP_VC, vgn - vc - BP_VC), 0, hdr_buf(c + 1), y_buf(c + 1),
+                             true);
+            cp_async_commit();
+        } else {
+            if (tid < nvc * HW)
+                reinterpret_cast<int4*>(hdr)[tid] = __ldg(reinterpret_cast<const int4*>(hsrc + vc) + tid);
+            __syncthreads();
+        }
         int npass = 0;
         for (int vi = 0; vi < nvc; ++vi) npass = max(npass, (int)hdr[vi].npass_f);
         for (int pass = 0; pass < npass; ++pass) {
+            if (STAGE && pass > 0) bp_y_load<S>(P, vg0 + vc, nvc, pass, hdr, ytab, false);
 #pragma unroll 3
             for (int e = tid; e < BP_VC * BP_NB; e += BP_THREADS) {
                 const int vi = e / BP_NB, jj = e % BP_NB;
@@ -329,31 +438,12 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                     const int j = H.jlo + pass * BP_NB + jj;
                     CBP_CHECK(j > H.jhi || (j >= 0 && j < g.n_det), "entry j=%d jlo=%d jhi=%d\n", j, H.jlo, H.jhi);
                     if (j <= H.jhi) {
-                        const size_t yo = (size_t)(vg0 + vc + vi) * g.n_det + j;
                         if constexpr (S == 1) {
+                            const size_t yo = (size_t)(vg0 + vc + vi) * g.n_det + j;
                             bp_build_entry(g, P.t, H, j, __ldg(P.sino + (size_t)sg * sino_plane + yo),
                                            tab[vi][jj]);
                         } else {
                             bp_build_entry(g, P.t, H, j, 1.0f, tab[vi][jj]);  // c.w = h^2 / A
-                            const float hA = tab[vi][jj].c.w;
-#pragma unroll
-                            for (int q = 0; q < S; ++q) {
-                                const int b = sg * S + q;
-                                float yv;
-                                if (P.sym_mode == 8) {  // frame (qq, m): view_g(v), bin_m(j)
-                                    const int N = g.n_views, v = P.view_begin + vg0 + vc + vi;
-                                    const int m = q >> 2, qq = q & 3;
-                                    const int view = ((m ? N - v : v) + qq * (N / 4)) % N;
-                                    const int bin = m ? g.n_det - 1 - j : j;
-                                    yv = (m && (v == 0 || 8 * v == N)) ? 0.0f
-                                                                       : __ldg(P.sino + (size_t)view * g.n_det + bin);
-                                } else if (P.sym_stride > 0) {
-                                    yv = __ldg(P.sino + (size_t)q * P.sym_stride * g.n_det + yo);
-                                } else {
-                                    yv = b < P.batch ? __ldg(P.sino + (size_t)b * sino_plane + yo) : 0.0f;
-                                }
-                                ytab[(vi * BP_NB + jj) * S + q] = yv * hA;
-                            }
                         }
                     }
                 }
@@ -418,8 +508,13 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                 }
             }
             if (bucket >= 0) bp_flush<S>(acc_s, horiz, e0, e1, a0, a1);
-            __syncthreads();
+            // the next pass rebuilds tab (the next chunk's top barrier covers S > 1)
+            if (!STAGE || pass + 1 < npass) __syncthreads();
         }
+    }
+    if constexpr (STAGE) {
+        cp_async_wait_all();
+        __syncthreads();
     }
     const size_t plane = (size_t)g.n * g.n;
     for (int q = 0; q < S; ++q) {
