@@ -472,20 +472,13 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     fprintf(stderr, "bp kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
 #endif
     cudaFreeAsync(hdrs, stream);
-    if (symmode == 8) {
-        const int blocks = (int)std::min<size_t>((plane + 255) / 256, (size_t)sms * 8);
-        cbp::cbp_sym8_reduce_kernel<<<blocks, 256, 0, stream>>>(part, img, g.n, G, accumulate ? 1 : 0);
-        ++g_launches;
-        cudaFreeAsync(part, stream);
-    } else if (sym) {
-        const int blocks = (int)std::min<size_t>((plane + 255) / 256, (size_t)sms * 8);
-        cbp::cbp_sym_reduce_kernel<<<blocks, 256, 0, stream>>>(part, img, g.n, G, accumulate ? 1 : 0);
-        ++g_launches;
-        cudaFreeAsync(part, stream);
-    } else if (G > 1) {
-        const size_t count = plane * batch;
-        const int blocks = (int)std::min<size_t>((count + 255) / 256, (size_t)sms * 8);
-        cbp::cbp_reduce_kernel<<<blocks, 256, 0, stream>>>(part, img, count, G, accumulate ? 1 : 0);
+    if (sym || G > 1) {
+        // symmetric: the G x S frame planes are already in output orientation
+        const size_t count = sym ? plane : plane * batch;
+        const int planes = sym ? G * batch : G;
+        const int blocks = (int)std::min<size_t>((count / 4 + 255) / 256, (size_t)sms * 8);
+        cbp::cbp_reduce_kernel<<<std::max(blocks, 1), 256, 0, stream>>>(part, img, count, planes,
+                                                                        accumulate ? 1 : 0);
         ++g_launches;
         cudaFreeAsync(part, stream);
     }

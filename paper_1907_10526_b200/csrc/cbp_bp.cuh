@@ -290,6 +290,27 @@ __device__ __forceinline__ void bp_flush(bp_acc_t<S>* acc_s, int horiz, int e0, 
 // next, the one after), S == 1 one
 __host__ __device__ constexpr int bp_hdr_bufs(int S) { return S > 1 ? 3 : 1; }
 
+// Symmetry frames on pixel (r, c) of the n x n grid:
+// g = R^q M^m with R(r, c) = (n-1-c, r) (+90 degrees) and M(r, c) = (n-1-r, c).
+__device__ __forceinline__ void frame_fwd(int n, int q, int m, int& r, int& c)
+{
+    if (m) r = n - 1 - r;
+    for (int t = 0; t < q; ++t) {
+        const int nr = n - 1 - c;
+        c = r;
+        r = nr;
+    }
+}
+__device__ __forceinline__ void frame_inv(int n, int q, int m, int& r, int& c)
+{
+    for (int t = 0; t < q; ++t) {  // R^-1 (r, c) = (c, n-1-r)
+        const int nr = c;
+        c = n - 1 - r;
+        r = nr;
+    }
+    if (m) r = n - 1 - r;
+}
+
 // dynamic shared memory of the BP kernel for S slices: entries, headers,
 // (S > 1) two y buffers [2][VC][NB][S], tile accumulators [S][32][33]
 __host__ __device__ constexpr size_t bp_smem_bytes(int S)
@@ -516,72 +537,89 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
         cp_async_wait_all();
         __syncthreads();
     }
-    const size_t plane = (size_t)g.n * g.n;
+    // Write the tile's sums.  With symmetry, slice q holds frame g_q = R^qq M^m
+    // of the image; its values go straight to the output orientation (pixel
+    // g_q(k)), so the partial planes are summed elementwise (cbp_reduce_kernel).
+    // Threads walk the OUTPUT rectangle g_q(tile) row by row (coalesced
+    // stores; the transposed shared-memory reads are conflict-free with the
+    // 33-float row pitch).
+    const int n = g.n;
+    const size_t plane = (size_t)n * n;
+    const int th = min(BP_TILE, n - row0), tw = min(BP_TILE, n - col0);
+    const int fsym = P.sym_mode == 8 ? 8 : (P.sym_stride > 0 ? 4 : 0);
+    constexpr int LD = BP_TILE + 1;
+    __shared__ int4 ep[S][2];  // per slice: (OR, OC, oh, ow), (s0, sc, sr, -)
+    if (tid < S) {
+        const int q = tid;
+        const int qq = fsym ? (q & 3) : 0, m = (fsym == 8 && q >= 4) ? 1 : 0;
+        int ra = row0, ca = col0, rb = row0 + th - 1, cb = col0 + tw - 1;
+        frame_fwd(n, qq, m, ra, ca);
+        frame_fwd(n, qq, m, rb, cb);
+        const int OR = min(ra, rb), OC = min(ca, cb);
+        // tile pixel of output (OR, OC) and its step per output column / row
+        int k0r = OR, k0c = OC, k1r = OR, k1c = OC + 1, k2r = OR + 1, k2c = OC;
+        frame_inv(n, qq, m, k0r, k0c);
+        frame_inv(n, qq, m, k1r, k1c);
+        frame_inv(n, qq, m, k2r, k2c);
+        ep[q][0] = make_int4(OR, OC, abs(ra - rb) + 1, abs(ca - cb) + 1);
+        ep[q][1] = make_int4((k0r - row0) * LD + (k0c - col0), (k1r - k0r) * LD + (k1c - k0c),
+                             (k2r - k0r) * LD + (k2c - k0c), 0);
+    }
+    __syncthreads();
     for (int q = 0; q < S; ++q) {
         const int b = sg * S + q;
         if (b >= P.batch) break;
         float* out = P.out + (P.groups > 1 ? ((size_t)grp * P.batch + b) : (size_t)b) * plane;
-        for (int i = tid; i < BP_TILE * BP_TILE; i += BP_THREADS) {
-            const int r = i / BP_TILE, c = i % BP_TILE;
-            const int row = row0 + r, col = col0 + c;
-            if (row < g.n && col < g.n) {
-                float* o = out + (size_t)row * g.n + col;
-                const float v = (float)acc_s[(q * BP_TILE + r) * (BP_TILE + 1) + c];
-                *o = (P.groups == 1 && P.accumulate) ? *o + v : v;
+        const int4 e0 = ep[q][0], e1 = ep[q][1];
+        const int OR = e0.x, OC = e0.y, oh = e0.z, ow = e0.w, s0 = e1.x, sc = e1.y, sr = e1.z;
+        const bp_acc_t<S>* a = acc_s + q * BP_TILE * LD;
+        const bool acc_out = P.groups == 1 && P.accumulate;
+        if (oh == BP_TILE && ow == BP_TILE && (n & 3) == 0 && !acc_out) {  // float4 stores
+            for (int i = tid; i < BP_TILE * BP_TILE / 4; i += BP_THREADS) {
+                const int r = i / (BP_TILE / 4), c = (i % (BP_TILE / 4)) * 4;
+                const int si = s0 + r * sr + c * sc;
+                const float4 v = make_float4((float)a[si], (float)a[si + sc], (float)a[si + 2 * sc],
+                                             (float)a[si + 3 * sc]);
+                *reinterpret_cast<float4*>(out + (size_t)(OR + r) * n + OC + c) = v;
+            }
+        } else {
+            for (int i = tid; i < BP_TILE * BP_TILE; i += BP_THREADS) {
+                const int r = i / BP_TILE, c = i % BP_TILE;
+                if (r < oh && c < ow) {
+                    float* o = out + (size_t)(OR + r) * n + OC + c;
+                    const float v = (float)a[s0 + r * sr + c * sc];
+                    *o = acc_out ? *o + v : v;
+                }
             }
         }
     }
 }
 
-// symmetric BP: out[k] = (accumulate ? out[k] : 0) + sum_g sum_q part[g][q][R^-q k]
-// (fixed order), R(r, c) = (n-1-c, r) the +90 degree pixel rotation
-__global__ void cbp_sym_reduce_kernel(const float* __restrict__ part, float* __restrict__ out, int n,
-                                      int groups, int accumulate)
-{
-    const size_t plane = (size_t)n * n;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < plane;
-         i += (size_t)gridDim.x * blockDim.x) {
-        const int r = (int)(i / n), c = (int)(i % n);
-        // R^-q (r, c): q = 0 (r, c), 1 (c, n-1-r), 2 (n-1-r, n-1-c), 3 (n-1-c, r)
-        const size_t src[4] = {i, (size_t)c * n + (n - 1 - r), (size_t)(n - 1 - r) * n + (n - 1 - c),
-                               (size_t)(n - 1 - c) * n + r};
-        float s = accumulate ? out[i] : 0.0f;
-        for (int gi = 0; gi < groups; ++gi)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) s += part[((size_t)gi * 4 + q) * plane + src[q]];
-        out[i] = s;
-    }
-}
-
-// dihedral BP: out[k] = (accumulate ? out[k] : 0) + sum_g sum_f part[g][f][g_f^-1 k],
-// g_f = R^q M^m (f = 4 m + q), g_f^-1 k = M^m R^-q k, fixed order
-__global__ void cbp_sym8_reduce_kernel(const float* __restrict__ part, float* __restrict__ out, int n,
-                                       int groups, int accumulate)
-{
-    const size_t plane = (size_t)n * n;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < plane;
-         i += (size_t)gridDim.x * blockDim.x) {
-        const int r = (int)(i / n), c = (int)(i % n);
-        // R^-q (r, c): q = 0 (r, c), 1 (c, n-1-r), 2 (n-1-r, n-1-c), 3 (n-1-c, r); then M: row -> n-1-row
-        const int rq[4] = {r, c, n - 1 - r, n - 1 - c}, cq[4] = {c, n - 1 - r, n - 1 - c, r};
-        float s = accumulate ? out[i] : 0.0f;
-        for (int gi = 0; gi < groups; ++gi)
-#pragma unroll
-            for (int f = 0; f < 8; ++f) {
-                const int q = f & 3;
-                const int rr = f >= 4 ? n - 1 - rq[q] : rq[q];
-                s += part[((size_t)gi * 8 + f) * plane + (size_t)rr * n + cq[q]];
-            }
-        out[i] = s;
-    }
-}
-
-// out[b][p] = (accumulate ? out[b][p] : 0) + sum_g part[g][b][p], fixed order
+// out[p] = (accumulate ? out[p] : 0) + sum_g part[g][p] over `groups` planes
+// of `count` floats, fixed order (deterministic); float4 when aligned
 __global__ void cbp_reduce_kernel(const float* __restrict__ part, float* __restrict__ out,
                                   size_t count, int groups, int accumulate)
 {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
-         i += (size_t)gridDim.x * blockDim.x) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const size_t t0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (((count & 3) | (reinterpret_cast<uintptr_t>(part) & 15) | (reinterpret_cast<uintptr_t>(out) & 15)) == 0) {
+        const size_t c4 = count / 4;
+        const float4* p4 = reinterpret_cast<const float4*>(part);
+        float4* o4 = reinterpret_cast<float4*>(out);
+        for (size_t i = t0; i < c4; i += stride) {
+            float4 s = accumulate ? o4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int gi = 0; gi < groups; ++gi) {
+                const float4 v = __ldg(p4 + (size_t)gi * c4 + i);
+                s.x += v.x;
+                s.y += v.y;
+                s.z += v.z;
+                s.w += v.w;
+            }
+            o4[i] = s;
+        }
+        return;
+    }
+    for (size_t i = t0; i < count; i += stride) {
         float s = accumulate ? out[i] : 0.0f;
         for (int gi = 0; gi < groups; ++gi) s += part[(size_t)gi * count + i];
         out[i] = s;
