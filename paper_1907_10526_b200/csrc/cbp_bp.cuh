@@ -61,6 +61,7 @@ constexpr int BP_THREADS = 256;   // 8 warps x 2 pairs x 2 pixels x 32 lanes = 3
 constexpr int BP_VC = 8;          // views per chunk
 constexpr int BP_NB = 80;         // bins per view per pass (a 32-pixel tile spans <= ~64)
 constexpr int BP_BUCKETS = 32;    // ray directions over [0, pi) for the pair order
+constexpr int BP_RUN_CHUNKS = 4;  // register partial sums span at most 4 chunks (32 views)
 constexpr int BP_PAIRS = BP_TILE * BP_TILE / 2;
 
 struct __align__(16) BPEntry {
@@ -427,6 +428,14 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
             cp_async_commit();
         }
     }
+    // the thread's two pixel pairs (their order depends on the ray-direction
+    // bucket) and their FP32 partial sums, carried across chunks and flushed
+    // to acc_s when the bucket changes, every BP_RUN_CHUNKS chunks and at the end
+    float2 a0[S], a1[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) a0[q] = a1[q] = make_float2(0.f, 0.f);
+    int bucket = -1, horiz = 1, e0 = 0, e1 = 0;
+    float2 dc0, dr0, dc1, dr1;  // pixel offsets of the two pairs (lanes a, b)
     for (int c = 0; c < nchunks; ++c) {
         const int vc = c * BP_VC;
         const int nvc = min(BP_VC, vgn - vc);
@@ -470,15 +479,12 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                 }
             }
             __syncthreads();
-            float2 a0[S], a1[S];
-#pragma unroll
-            for (int q = 0; q < S; ++q) a0[q] = a1[q] = make_float2(0.f, 0.f);
-            int bucket = -1, horiz = 1, e0 = 0, e1 = 0;
-            float2 dc0, dr0, dc1, dr1;  // pixel offsets of the two pairs (lanes a, b)
             for (int vi = 0; vi < nvc; ++vi) {
                 const BPHeader& H = hdr[vi];
                 const int4 hi = *reinterpret_cast<const int4*>(&H.ja);  // ja, jlo, jhi, bucket
-                if (hi.w != bucket) {  // new pair order: hand the pixels back first
+                // new pair order, or FP32 register sums over BP_RUN views: hand the pixels back
+                const bool renew = hi.w != bucket || (vi == 0 && pass == 0 && c > 0 && c % BP_RUN_CHUNKS == 0);
+                if (renew) {
                     if (bucket >= 0) {
                         bp_flush<S>(acc_s, horiz, e0, e1, a0, a1);
                         __syncthreads();
@@ -528,11 +534,11 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                         bp_pair<S>(row, yrow, jl, jh, base, dcp.x, drp.x, a1);
                 }
             }
-            if (bucket >= 0) bp_flush<S>(acc_s, horiz, e0, e1, a0, a1);
             // the next pass rebuilds tab (the next chunk's top barrier covers S > 1)
             if (!STAGE || pass + 1 < npass) __syncthreads();
         }
     }
+    if (bucket >= 0) bp_flush<S>(acc_s, horiz, e0, e1, a0, a1);
     if constexpr (STAGE) {
         cp_async_wait_all();
         __syncthreads();
