@@ -614,7 +614,20 @@ __global__ void cbp_reduce_kernel(const float* __restrict__ part, float* __restr
         float4* o4 = reinterpret_cast<float4*>(out);
         for (size_t i = t0; i < c4; i += stride) {
             float4 s = accumulate ? o4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int gi = 0; gi < groups; ++gi) {
+            int gi = 0;
+            for (; gi + 8 <= groups; gi += 8) {  // 8 loads in flight, summed in plane order
+                float4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldg(p4 + (size_t)(gi + u) * c4 + i);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    s.x += v[u].x;
+                    s.y += v[u].y;
+                    s.z += v[u].z;
+                    s.w += v[u].w;
+                }
+            }
+            for (; gi < groups; ++gi) {
                 const float4 v = __ldg(p4 + (size_t)gi * c4 + i);
                 s.x += v.x;
                 s.y += v.y;
