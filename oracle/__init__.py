@@ -89,6 +89,10 @@ def lib():
                 "orc_set_candidate_margin_scale": (None, [ctypes.c_double]),
                 "orc_count_weights": (ctypes.c_int64, [G, ctypes.c_int32, ctypes.c_int32,
                                                        ctypes.c_int32]),
+                "orc_ref_chord": (ctypes.c_double, [G, ctypes.c_double, ctypes.c_double, _PD]),
+                "orc_ref_weight": (ctypes.c_double, [G, ctypes.c_double, ctypes.c_double, _PD]),
+                "orc_ref_forward": (ctypes.c_int, [G, _PD, _PD, ctypes.c_int32, ctypes.c_int32,
+                                                   ctypes.c_int32, ctypes.c_int32]),
                 "orc_count_weights_per_view": (ctypes.c_int, [G, ctypes.c_int32, ctypes.c_int32,
                                                               ctypes.POINTER(ctypes.c_int64),
                                                               ctypes.c_int32]),
@@ -241,3 +245,28 @@ def count_weights_per_view(geom, view_begin=0, view_count=None, threads=0) -> np
     if rc != 0:
         raise ValueError("orc_count_weights_per_view: invalid arguments")
     return out
+
+
+# ---- row f2: the reference projector ---------------------------
+def ref_chord(geom, theta, s, k):
+    return lib().orc_ref_chord(ctypes.byref(_g(geom)), theta, s, _D2(*k))
+
+
+def ref_weight(geom, theta, s, k):
+    return lib().orc_ref_weight(ctypes.byref(_g(geom)), theta, s, _D2(*k))
+
+
+def ref_forward(geom, image, view_begin=0, view_count=None, threads=0) -> np.ndarray:
+    """y = A_ref c: exact bin-averaged chords (FP64), layout as forward()."""
+    g = _g(geom)
+    img = np.ascontiguousarray(image, dtype=np.float64)
+    squeeze = img.ndim == 2
+    if squeeze:
+        img = img[None]
+    nv = g.n_views - view_begin if view_count is None else view_count
+    out = np.zeros((img.shape[0], nv, g.n_det))
+    rc = lib().orc_ref_forward(ctypes.byref(g), _dp(img), _dp(out), img.shape[0], view_begin, nv,
+                               threads)
+    if rc != 0:
+        raise ValueError("orc_ref_forward: invalid arguments")
+    return out[0] if squeeze else out

@@ -78,6 +78,18 @@ int64_t orc_count_weights(const orc_geometry* g, int32_t v0, int32_t nv, int32_t
 int orc_count_weights_per_view(const orc_geometry* g, int32_t v0, int32_t nv, int64_t* out,
                                int32_t threads);
 
+/* --- row f2: the paper's reference projector "Ref" ------------
+ * orc_ref_chord: exact chord of the ray of detector coordinate s through the
+ *   indicator pixel of side h centred at k (Eq. 10, no blur).
+ * orc_ref_weight: that chord averaged over [s - tau/2, s + tau/2] (adaptive
+ *   Simpson between the projected corners, absolute tolerance 1e-14).
+ * orc_ref_forward: y = A_ref c with these weights (layout as orc_forward;
+ *   zero pixels are skipped, which is exact).                                 */
+double orc_ref_chord(const orc_geometry* g, double theta, double s, const double k[2]);
+double orc_ref_weight(const orc_geometry* g, double theta, double s, const double k[2]);
+int orc_ref_forward(const orc_geometry* g, const double* image, double* sino,
+                    int32_t batch, int32_t v0, int32_t nv, int32_t threads);
+
 #ifdef __cplusplus
 }
 #endif
