@@ -141,6 +141,19 @@ int cbp_cgls_step(float* x, const float* p, float* r, const float* q, const doub
 int cbp_cgls_direction(float* p, const float* s, const double* num, const double* den,
                        int64_t count, void* stream);
 
+/* ---- Row f2: the paper's reference projector "Ref", FP64.
+ *   sino[b][v][j] = sum_k image[b][k] (1/tau) int_{s_j - tau/2}^{s_j + tau/2} chord_k(s) ds
+ * with chord_k(s) the length the ray from the source to detector coordinate s
+ * cuts through the indicator pixel k (Eq. 10: the exact fan-beam transform of
+ * the pixel basis, no blur), integrated by 8-point Gauss-Legendre between the
+ * perspective images of the pixel corners (the integrand is smooth there).
+ * An accuracy reference for the CNSF weights (Eq. 15 errors, Fig. 6-7), not
+ * a hot path: ~100x the cost of cbp_forward.  image FP32 [batch][n][n],
+ * sino FP64 [batch][view_count][n_det] (8-byte aligned); DEVICE pointers
+ * only; stream-ordered.  CBP_EINVAL as cbp_forward, or for host pointers. */
+int cbp_ref_forward(const cbp_geometry_t* g, const float* image, double* sino, int32_t batch,
+                    int32_t view_begin, int32_t view_count, void* stream);
+
 /* Adjoint identity check on the current device (synchronous): draws seeded
  * c, y ~ U[0,1) (splitmix64), runs cbp_forward and cbp_back over all views,
  * and returns |<Ac,y> - <c,A^T y>| / |<Ac,y>| with FP64 inner products in

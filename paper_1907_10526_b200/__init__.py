@@ -24,8 +24,8 @@ CBP_OK, CBP_EINVAL, CBP_ECUDA, CBP_ENOMEM = 0, -1, -2, -3
 # names declared in include/cbp.h
 ABI_FUNCTIONS = ("cbp_validate", "cbp_forward", "cbp_back", "cbp_symmetry_fold",
                  "cbp_forward_orbit", "cbp_back_orbit", "cbp_sart_residual", "cbp_sart_update",
-                 "cbp_fill", "cbp_dot", "cbp_cgls_step", "cbp_cgls_direction", "cbp_adjoint_check",
-                 "cbp_strerror", "cbp_version", "cbp_launch_count")
+                 "cbp_fill", "cbp_dot", "cbp_cgls_step", "cbp_cgls_direction", "cbp_ref_forward",
+                 "cbp_adjoint_check", "cbp_strerror", "cbp_version", "cbp_launch_count")
 
 
 class CbpError(RuntimeError):
@@ -102,6 +102,8 @@ def lib() -> ctypes.CDLL:
         for name in ("cbp_sart_residual", "cbp_sart_update", "cbp_fill", "cbp_dot",
                      "cbp_cgls_step", "cbp_cgls_direction"):
             getattr(L, name).restype = ctypes.c_int
+        L.cbp_ref_forward.argtypes = [G, fp, fp, i32, i32, i32, vp]
+        L.cbp_ref_forward.restype = ctypes.c_int
         L.cbp_adjoint_check.argtypes = [G, ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]
         L.cbp_adjoint_check.restype = ctypes.c_int
         L.cbp_strerror.argtypes = [ctypes.c_int]
@@ -186,6 +188,35 @@ def forward(geom, image, sino=None, view_begin: int = 0, view_count: int | None 
     rc = lib().cbp_forward(ctypes.byref(g), pi, ps, batch, view_begin, nv, st)
     if rc != CBP_OK:
         raise CbpError(rc, "cbp_forward")
+    return sino
+
+
+def ref_forward(geom, image, sino=None, view_begin: int = 0, view_count: int | None = None,
+                stream=None):
+    """Row f2: the paper's reference projector -- exact chords
+    averaged over each bin, FP64 -- for views [view_begin, view_begin + view_count).
+
+    image: [n, n] or [B, n, n] float32 CUDA tensor.  Returns a float64 CUDA
+    tensor [B?, view_count, n_det].
+    """
+    import torch
+    g = _checked(geom)
+    nv = g.n_views - view_begin if view_count is None else view_count
+    squeeze = image.ndim == 2
+    batch = 1 if squeeze else image.shape[0]
+    if tuple(image.shape[-2:]) != (g.n, g.n):
+        raise ValueError(f"image shape {tuple(image.shape)} does not match n={g.n}")
+    if not (isinstance(image, torch.Tensor) and image.is_cuda):
+        raise ValueError("ref_forward takes CUDA tensors")
+    shape = (nv, g.n_det) if squeeze else (batch, nv, g.n_det)
+    if sino is None:
+        sino = torch.empty(shape, dtype=torch.float64, device=image.device)
+    elif tuple(sino.shape) != shape or sino.dtype != torch.float64 or not sino.is_contiguous():
+        raise ValueError(f"sino must be a contiguous float64 tensor of shape {shape}")
+    pi, st = _ptr_and_stream(image, stream)
+    rc = lib().cbp_ref_forward(ctypes.byref(g), pi, sino.data_ptr(), batch, view_begin, nv, st)
+    if rc != CBP_OK:
+        raise CbpError(rc, "cbp_ref_forward")
     return sino
 
 

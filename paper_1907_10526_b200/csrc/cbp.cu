@@ -18,6 +18,7 @@
 #include "cbp_bp.cuh"
 #include "cbp_common.cuh"
 #include "cbp_fp.cuh"
+#include "cbp_ref.cuh"
 #include "cbp_tables.cuh"
 #include "cbp_vec.cuh"
 
@@ -753,7 +754,30 @@ const char* cbp_strerror(int code)
     }
 }
 
-int cbp_version(void) { return 100; }
+// ---- row f2: the reference projector ---------------------------------------
+int cbp_ref_forward(const cbp_geometry_t* g, const float* image, double* sino, int32_t batch,
+                    int32_t view_begin, int32_t view_count, void* stream_)
+{
+    int rc = check_common(g, image, sino, batch, view_begin, view_count);
+    if (rc != CBP_OK) return rc;
+    if (((uintptr_t)sino & 7) || pointer_kind(image) != 1 || pointer_kind(sino) != 1) return CBP_EINVAL;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    cbp::Tables t;
+    if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    cbp::RefParams P;
+    P.g = to_dev(*g);
+    P.t = t;
+    P.img = image;
+    P.sino = sino;
+    P.view_begin = view_begin;
+    P.view_count = view_count;
+    P.batch = batch;
+    dim3 grid((g->n_det + cbp::REF_BLOCK - 1) / cbp::REF_BLOCK, view_count, batch);
+    cbp::cbp_ref_fp_kernel<<<grid, cbp::REF_BLOCK, 0, stream>>>(P);
+    return launched();
+}
+
+int cbp_version(void) { return 110; }
 
 uint64_t cbp_launch_count(void) { return g_launches.load(); }
 
