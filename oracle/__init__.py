@@ -93,6 +93,8 @@ def lib():
                 "orc_ref_weight": (ctypes.c_double, [G, ctypes.c_double, ctypes.c_double, _PD]),
                 "orc_ref_forward": (ctypes.c_int, [G, _PD, _PD, ctypes.c_int32, ctypes.c_int32,
                                                    ctypes.c_int32, ctypes.c_int32]),
+                "orc_ref_back": (ctypes.c_int, [G, _PD, _PD, ctypes.c_int32, ctypes.c_int32,
+                                                ctypes.c_int32, ctypes.c_int32]),
                 "orc_count_weights_per_view": (ctypes.c_int, [G, ctypes.c_int32, ctypes.c_int32,
                                                               ctypes.POINTER(ctypes.c_int64),
                                                               ctypes.c_int32]),
@@ -269,4 +271,19 @@ def ref_forward(geom, image, view_begin=0, view_count=None, threads=0) -> np.nda
                                threads)
     if rc != 0:
         raise ValueError("orc_ref_forward: invalid arguments")
+    return out[0] if squeeze else out
+
+
+def ref_back(geom, sino, view_begin=0, threads=0) -> np.ndarray:
+    """c = A_ref^T y (FP64); sino [nv, n_det] or [B, nv, n_det]."""
+    g = _g(geom)
+    y = np.ascontiguousarray(sino, dtype=np.float64)
+    squeeze = y.ndim == 2
+    if squeeze:
+        y = y[None]
+    out = np.zeros((y.shape[0], g.n, g.n))
+    rc = lib().orc_ref_back(ctypes.byref(g), _dp(y), _dp(out), y.shape[0], view_begin, y.shape[1],
+                            threads)
+    if rc != 0:
+        raise ValueError("orc_ref_back: invalid arguments")
     return out[0] if squeeze else out

@@ -663,3 +663,45 @@ int orc_ref_forward(const orc_geometry* g, const double* image, double* sino, in
     }
     return 0;
 }
+
+/* A_ref^T: image[b][k] = sum_{v,j} sino[b][v][j] W_ref(v, j, k) (the exact
+ * transpose of orc_ref_forward: same weights, same candidate bins). */
+int orc_ref_back(const orc_geometry* g, const double* sino, double* image, int32_t batch,
+                 int32_t v0, int32_t nv, int32_t threads)
+{
+    if (!geometry_ok(g) || !image || !sino || batch < 1 || v0 < 0 || nv < 0 ||
+        v0 + nv > g->n_views)
+        return -1;
+    const int32_t n = g->n, ns = g->n_det;
+    const int nt = nthreads_of(threads);
+    const double hh = 0.5 * g->pixel, c0 = 0.5 * (double)(ns - 1);
+    int64_t px;
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 16)
+    for (px = 0; px < (int64_t)n * n; ++px) {
+        const int32_t row = (int32_t)(px / n), col = (int32_t)(px % n);
+        double k[2];
+        orc_pixel_center(g, row, col, k);
+        for (int32_t b = 0; b < batch; ++b) image[(int64_t)b * n * n + px] = 0.0;
+        for (int32_t vl = 0; vl < nv; ++vl) {
+            double u[2], e[2], p[2];
+            orc_view_frame(g, orc_view_angle(g, v0 + vl), u, e, p);
+            double smin = 1e300, smax = -1e300;
+            for (int c = 0; c < 4; ++c) {
+                const double corner[2] = {k[0] + ((c & 1) ? hh : -hh), k[1] + ((c & 2) ? hh : -hh)};
+                const double sc = perspective_f(g, u, e, p, corner);
+                if (sc < smin) smin = sc;
+                if (sc > smax) smax = sc;
+            }
+            double lo = ceil((smin - 0.5 * g->det_width) / g->det_pitch + c0 - 1.0);
+            double hi = floor((smax + 0.5 * g->det_width) / g->det_pitch + c0 + 1.0);
+            if (lo < 0) lo = 0;
+            if (hi > ns - 1) hi = ns - 1;
+            for (int32_t j = (int32_t)lo; j <= (int32_t)hi; ++j) {
+                const double w = ref_weight_f(g, u, e, p, orc_bin_center(g, j), k);
+                for (int32_t b = 0; b < batch; ++b)
+                    image[(int64_t)b * n * n + px] += sino[((int64_t)b * nv + vl) * ns + j] * w;
+            }
+        }
+    }
+    return 0;
+}

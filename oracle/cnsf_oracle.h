@@ -89,6 +89,9 @@ double orc_ref_chord(const orc_geometry* g, double theta, double s, const double
 double orc_ref_weight(const orc_geometry* g, double theta, double s, const double k[2]);
 int orc_ref_forward(const orc_geometry* g, const double* image, double* sino,
                     int32_t batch, int32_t v0, int32_t nv, int32_t threads);
+/* its transpose: image = A_ref^T sino (same weights)                          */
+int orc_ref_back(const orc_geometry* g, const double* sino, double* image,
+                 int32_t batch, int32_t v0, int32_t nv, int32_t threads);
 
 #ifdef __cplusplus
 }
