@@ -154,6 +154,31 @@ int cbp_cgls_direction(float* p, const float* s, const double* num, const double
 int cbp_ref_forward(const cbp_geometry_t* g, const float* image, double* sino, int32_t batch,
                     int32_t view_begin, int32_t view_count, void* stream);
 
+/* Its exact transpose, FP64 both sides: image[b][k] = sum_{v,j} sino[b][v][j]
+ * W_ref(v, j, k) (overwrites image).  Device pointers only, 8-byte aligned. */
+int cbp_ref_back(const cbp_geometry_t* g, const double* sino, double* image, int32_t batch,
+                 int32_t view_begin, int32_t view_count, void* stream);
+
+/* ---- Row f4: total variation and the steps of ASD-POCS (the
+ * schedule is DESIGN.md ledger #21).  Device pointers; FP32 images
+ * [batch][n][n]; scalars are DEVICE doubles (no host round trip).
+ *   TV(x) = sum sqrt(dx^2 + dy^2 + eps^2), dx, dy forward differences with a
+ *   reflective boundary (ledger #20); differences in FP64.
+ * cbp_tv_value:    *out = TV(x) summed over the batch (deterministic FP64 sum)
+ * cbp_tv_gradient: grad = d TV / d x (its exact analytic gradient)
+ * cbp_diff_norm2:  *out = |a - b|^2 over count elements (FP64)
+ * cbp_tv_step:     x -= (*alpha) sqrt(*dp2) g / sqrt(*gg)  (unchanged if *gg == 0):
+ *                  a normalised descent step of length alpha |data step|
+ * cbp_asd_adapt:   *alpha *= alpha_red if sqrt(*dg2) > r_max sqrt(*dp2)
+ * CBP_EINVAL for null pointers, n < 1, batch < 1, count < 0 or eps < 0.    */
+int cbp_tv_value(const float* x, int32_t n, int32_t batch, double eps, double* out, void* stream);
+int cbp_tv_gradient(const float* x, float* grad, int32_t n, int32_t batch, double eps, void* stream);
+int cbp_diff_norm2(const float* a, const float* b, int64_t count, double* out, void* stream);
+int cbp_tv_step(float* x, const float* g, int64_t count, const double* gg, const double* alpha,
+                const double* dp2, void* stream);
+int cbp_asd_adapt(double* alpha, const double* dp2, const double* dg2, double r_max, double alpha_red,
+                  void* stream);
+
 /* Adjoint identity check on the current device (synchronous): draws seeded
  * c, y ~ U[0,1) (splitmix64), runs cbp_forward and cbp_back over all views,
  * and returns |<Ac,y> - <c,A^T y>| / |<Ac,y>| with FP64 inner products in

@@ -9,8 +9,9 @@ study's CPU cross-check, never by the product path.
   reflective boundary (the difference past the last row / column is 0),
   eps = 1e-8; tv_gradient is its exact analytic gradient.
 * ASD-POCS (Sidky & Pan 2008, cited at P:547; schedule per S:368-375 and
-  DESIGN.md ledger #18): per iteration
-      x_d = max(SART(x, beta), 0);  dp = |x_d - x|
+  DESIGN.md ledger #21): per iteration
+      x_d = SART sweep from x over the ordered view subsets (positivity after
+            each subset);  dp = |x_d - x|
       step = alpha dp;  n_tv times: x <- x - step grad TV(x) / |grad TV(x)|
       dg = |x - x_d|;  if dg > r_max dp: alpha <- alpha alpha_red
       beta <- beta beta_red
@@ -62,6 +63,7 @@ class AsdPocsConfig:
     alpha_red: float = 0.95
     r_max: float = 0.95
     nonneg: bool = True
+    subsets: int = 1
 
 
 def sart_step(x, y, fwd: Callable, back: Callable, rows, cols, beta: float):
@@ -69,16 +71,45 @@ def sart_step(x, y, fwd: Callable, back: Callable, rows, cols, beta: float):
     return x + beta * np.where(cols > 1e-12, back(r) / np.where(cols > 1e-12, cols, 1.0), 0.0)
 
 
+def _order(count):
+    """bit-reversed order for a power of two, else golden-ratio stepping"""
+    if count & (count - 1) == 0:
+        bits = max(1, count.bit_length() - 1)
+        return [int(format(i, f"0{bits}b")[::-1], 2) for i in range(count)] if count > 1 else [0]
+    order, seen, k = [], set(), 0
+    step = max(1, round(count * 0.6180339887))
+    while len(order) < count:
+        while k in seen:
+            k = (k + 1) % count
+        order.append(k)
+        seen.add(k)
+        k = (k + step) % count
+    return order
+
+
 def asd_pocs(y: np.ndarray, n: int, fwd: Callable, back: Callable, cfg: AsdPocsConfig,
              log: list | None = None) -> np.ndarray:
-    rows = fwd(np.ones((n, n)))
-    cols = back(np.ones_like(y))
+    """fwd(c, v0, nv) -> rows v0..v0+nv-1; back(r, v0) -> image (view blocks);
+    with cfg.subsets == 1 they are called with the whole view range."""
+    nviews = y.shape[0]
+    base, rem = divmod(nviews, cfg.subsets)
+    blocks, v = [], 0
+    for i in range(cfg.subsets):
+        m = base + (1 if i < rem else 0)
+        blocks.append((v, m))
+        v += m
+    rows = [fwd(np.ones((n, n)), v0, m) for v0, m in blocks]
+    cols = [back(np.ones((m, y.shape[1])), v0) for v0, m in blocks]
     x = np.zeros((n, n))
     beta, alpha = cfg.beta0, cfg.alpha
     for it in range(cfg.n_iterations):
-        xd = sart_step(x, y, fwd, back, rows, cols, beta)
-        if cfg.nonneg:
-            xd = np.maximum(xd, 0.0)
+        xd = x.copy()
+        for b in _order(len(blocks)):
+            v0, m = blocks[b]
+            xd = sart_step(xd, y[v0:v0 + m], lambda c: fwd(c, v0, m), lambda s: back(s, v0),
+                           rows[b], cols[b], beta)
+            if cfg.nonneg:
+                xd = np.maximum(xd, 0.0)
         dp = float(np.linalg.norm(xd - x))
         step = alpha * dp
         x = xd.copy()

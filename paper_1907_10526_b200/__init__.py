@@ -25,7 +25,9 @@ CBP_OK, CBP_EINVAL, CBP_ECUDA, CBP_ENOMEM = 0, -1, -2, -3
 ABI_FUNCTIONS = ("cbp_validate", "cbp_forward", "cbp_back", "cbp_symmetry_fold",
                  "cbp_forward_orbit", "cbp_back_orbit", "cbp_sart_residual", "cbp_sart_update",
                  "cbp_fill", "cbp_dot", "cbp_cgls_step", "cbp_cgls_direction", "cbp_ref_forward",
-                 "cbp_adjoint_check", "cbp_strerror", "cbp_version", "cbp_launch_count")
+                 "cbp_ref_back", "cbp_tv_value", "cbp_tv_gradient", "cbp_diff_norm2", "cbp_tv_step",
+                 "cbp_asd_adapt", "cbp_adjoint_check", "cbp_strerror", "cbp_version",
+                 "cbp_launch_count")
 
 
 class CbpError(RuntimeError):
@@ -104,6 +106,16 @@ def lib() -> ctypes.CDLL:
             getattr(L, name).restype = ctypes.c_int
         L.cbp_ref_forward.argtypes = [G, fp, fp, i32, i32, i32, vp]
         L.cbp_ref_forward.restype = ctypes.c_int
+        L.cbp_ref_back.argtypes = [G, fp, fp, i32, i32, i32, vp]
+        L.cbp_ref_back.restype = ctypes.c_int
+        f64 = ctypes.c_double
+        L.cbp_tv_value.argtypes = [fp, i32, i32, f64, fp, vp]
+        L.cbp_tv_gradient.argtypes = [fp, fp, i32, i32, f64, vp]
+        L.cbp_diff_norm2.argtypes = [fp, fp, i64, fp, vp]
+        L.cbp_tv_step.argtypes = [fp, fp, i64, fp, fp, fp, vp]
+        L.cbp_asd_adapt.argtypes = [fp, fp, fp, f64, f64, vp]
+        for name in ("cbp_tv_value", "cbp_tv_gradient", "cbp_diff_norm2", "cbp_tv_step", "cbp_asd_adapt"):
+            getattr(L, name).restype = ctypes.c_int
         L.cbp_adjoint_check.argtypes = [G, ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]
         L.cbp_adjoint_check.restype = ctypes.c_int
         L.cbp_strerror.argtypes = [ctypes.c_int]
@@ -333,6 +345,61 @@ def cgls_step(x, p, r, q, num, den):
 
 def cgls_direction(p, s, num, den):
     _call("cbp_cgls_direction", _dev(p), _dev(s), _dev(num), _dev(den), p.numel())
+
+
+def ref_back(geom, sino, image=None, view_begin: int = 0):
+    """Row f2/f4: A_ref^T y, the exact transpose of ref_forward (FP64 in and
+    out, CUDA tensors).  sino [V, n_det] or [B, V, n_det]."""
+    import torch
+    g = _checked(geom)
+    squeeze = sino.ndim == 2
+    batch = 1 if squeeze else sino.shape[0]
+    if sino.dtype != torch.float64 or sino.shape[-1] != g.n_det:
+        raise ValueError("sino must be float64 [B?, V, n_det]")
+    shape = (g.n, g.n) if squeeze else (batch, g.n, g.n)
+    if image is None:
+        image = torch.empty(shape, dtype=torch.float64, device=sino.device)
+    _call_g("cbp_ref_back", g, _dev(sino), _dev(image), batch, view_begin, sino.shape[-2])
+    return image
+
+
+def _call_g(name, g, *args):
+    rc = getattr(lib(), name)(ctypes.byref(g), *args, _stream())
+    if rc != CBP_OK:
+        raise CbpError(rc, name)
+
+
+EPS_TV = 1e-8
+
+
+def tv_value(x, out, eps: float = EPS_TV):
+    """TV(x) (isotropic, forward differences, reflective boundary) summed over
+    the batch, into the device float64 tensor `out` [1]."""
+    n = x.shape[-1]
+    _call("cbp_tv_value", _dev(x), n, x.numel() // (n * n), ctypes.c_double(eps), _dev(out))
+    return out
+
+
+def tv_gradient(x, grad, eps: float = EPS_TV):
+    n = x.shape[-1]
+    _call("cbp_tv_gradient", _dev(x), _dev(grad), n, x.numel() // (n * n), ctypes.c_double(eps))
+    return grad
+
+
+def diff_norm2(a, b, out):
+    _call("cbp_diff_norm2", _dev(a), _dev(b), a.numel(), _dev(out))
+    return out
+
+
+def tv_step(x, g, gg, alpha, dp2):
+    _call("cbp_tv_step", _dev(x), _dev(g), x.numel(), _dev(gg), _dev(alpha), _dev(dp2))
+    return x
+
+
+def asd_adapt(alpha, dp2, dg2, r_max: float, alpha_red: float):
+    _call("cbp_asd_adapt", _dev(alpha), _dev(dp2), _dev(dg2), ctypes.c_double(r_max),
+          ctypes.c_double(alpha_red))
+    return alpha
 
 
 def adjoint_check(geom, seed: int = 0) -> float:

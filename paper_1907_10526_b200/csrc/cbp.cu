@@ -682,6 +682,60 @@ int cbp_dot(const float* a, const float* b, int64_t count, double* out, void* st
     return rc;
 }
 
+// ---- row f4: TV and the ASD-POCS steps ---------------------------------------
+static int sum_reduce(const float* a, const float* b, int n, int64_t count, double eps, int mode,
+                      double* out, cudaStream_t stream)
+{
+    double* part = nullptr;
+    int rc = scratch_alloc((void**)&part, sizeof(double) * cbp::DOT_BLOCKS, stream);
+    if (rc != CBP_OK) return rc;
+    cbp::cbp_sum_partial_kernel<<<cbp::DOT_BLOCKS, cbp::VEC_BLOCK, 0, stream>>>(a, b, n, count, eps, mode,
+                                                                               part);
+    ++g_launches;
+    cbp::cbp_dot_final_kernel<<<1, cbp::VEC_BLOCK, 0, stream>>>(part, cbp::DOT_BLOCKS, out);
+    rc = launched();
+    cudaFreeAsync(part, stream);
+    return rc;
+}
+
+int cbp_tv_value(const float* x, int32_t n, int32_t batch, double eps, double* out, void* stream)
+{
+    if (!x || !out || n < 1 || batch < 1 || !(eps >= 0.0)) return CBP_EINVAL;
+    return sum_reduce(x, nullptr, n, (int64_t)batch * n * n, eps, 0, out, (cudaStream_t)stream);
+}
+
+int cbp_tv_gradient(const float* x, float* grad, int32_t n, int32_t batch, double eps, void* stream)
+{
+    if (!x || !grad || n < 1 || batch < 1 || !(eps >= 0.0)) return CBP_EINVAL;
+    const int64_t count = (int64_t)batch * n * n;
+    cbp::cbp_tv_gradient_kernel<<<vec_grid(count), cbp::VEC_BLOCK, 0, (cudaStream_t)stream>>>(x, grad, n,
+                                                                                              count, eps);
+    return launched();
+}
+
+int cbp_diff_norm2(const float* a, const float* b, int64_t count, double* out, void* stream)
+{
+    if (!a || !b || !out || count < 0) return CBP_EINVAL;
+    return sum_reduce(a, b, 1, count, 0.0, 1, out, (cudaStream_t)stream);
+}
+
+int cbp_tv_step(float* x, const float* g, int64_t count, const double* gg, const double* alpha,
+                const double* dp2, void* stream)
+{
+    if (!x || !g || !gg || !alpha || !dp2 || count < 0) return CBP_EINVAL;
+    cbp::cbp_tv_step_kernel<<<vec_grid(count), cbp::VEC_BLOCK, 0, (cudaStream_t)stream>>>(x, g, count, gg,
+                                                                                          alpha, dp2);
+    return launched();
+}
+
+int cbp_asd_adapt(double* alpha, const double* dp2, const double* dg2, double r_max, double alpha_red,
+                  void* stream)
+{
+    if (!alpha || !dp2 || !dg2) return CBP_EINVAL;
+    cbp::cbp_asd_adapt_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(alpha, dp2, dg2, r_max, alpha_red);
+    return launched();
+}
+
 int cbp_cgls_step(float* x, const float* p, float* r, const float* q, const double* num,
                   const double* den, int64_t nx, int64_t nr, void* stream)
 {
@@ -777,7 +831,30 @@ int cbp_ref_forward(const cbp_geometry_t* g, const float* image, double* sino, i
     return launched();
 }
 
-int cbp_version(void) { return 110; }
+int cbp_ref_back(const cbp_geometry_t* g, const double* sino, double* image, int32_t batch,
+                 int32_t view_begin, int32_t view_count, void* stream_)
+{
+    int rc = check_common(g, sino, image, batch, view_begin, view_count);
+    if (rc != CBP_OK) return rc;
+    if (((uintptr_t)sino & 7) || ((uintptr_t)image & 7) || pointer_kind(image) != 1 || pointer_kind(sino) != 1)
+        return CBP_EINVAL;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    cbp::Tables t;
+    if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    cbp::RefBackParams P;
+    P.g = to_dev(*g);
+    P.t = t;
+    P.sino = sino;
+    P.img = image;
+    P.view_begin = view_begin;
+    P.view_count = view_count;
+    P.batch = batch;
+    dim3 grid((unsigned)(((int64_t)g->n * g->n + cbp::REF_BLOCK - 1) / cbp::REF_BLOCK), batch);
+    cbp::cbp_ref_bp_kernel<<<grid, cbp::REF_BLOCK, 0, stream>>>(P);
+    return launched();
+}
+
+int cbp_version(void) { return 120; }
 
 uint64_t cbp_launch_count(void) { return g_launches.load(); }
 

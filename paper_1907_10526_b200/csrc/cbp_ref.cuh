@@ -180,4 +180,55 @@ __global__ void __launch_bounds__(REF_BLOCK) cbp_ref_fp_kernel(const RefParams P
     P.sino[((size_t)b * P.view_count + vl) * g.n_det + j] = y / g.tau;
 }
 
+// A_ref^T: thread = one pixel of one image; for every view the bins whose
+// interval meets the pixel's projected corners (widened by tau/2 and one bin)
+// -- a superset of the nonzero weights, so this is the exact transpose of
+// cbp_ref_fp_kernel (weights outside the support are exactly 0 there too).
+struct RefBackParams {
+    GeomDev g;
+    Tables t;
+    const double* sino;  // [batch][view_count][n_det]
+    double* img;         // [batch][n][n]
+    int view_begin, view_count, batch;
+};
+
+__global__ void __launch_bounds__(REF_BLOCK) cbp_ref_bp_kernel(const RefBackParams P)
+{
+    const GeomDev& g = P.g;
+    const int n = g.n;
+    const int px = blockIdx.x * REF_BLOCK + threadIdx.x;
+    if (px >= n * n) return;
+    const int b = blockIdx.y;
+    const int row = px / n, col = px % n;
+    const double h = g.h, hh = 0.5 * g.h;
+    const double kx = (col - g.c0) * h, ky = (g.c0 - row) * h;
+    const double* y = P.sino + (size_t)b * P.view_count * g.n_det;
+    double acc = 0.0;
+    for (int vl = 0; vl < P.view_count; ++vl) {
+        const double2 cs = P.t.view_cs[P.view_begin + vl];
+        RefView V;
+        V.ux = cs.x;
+        V.uy = cs.y;
+        V.ex = -cs.y;
+        V.ey = cs.x;
+        V.px = g.sid * cs.x;
+        V.py = g.sid * cs.y;
+        V.dps = g.sdd;
+        V.dso = g.sdd - g.sid;
+        const double s0 = ref_project(V, kx - hh, ky - hh), s1 = ref_project(V, kx + hh, ky - hh);
+        const double s2 = ref_project(V, kx - hh, ky + hh), s3 = ref_project(V, kx + hh, ky + hh);
+        const double smin = fmin(fmin(s0, s1), fmin(s2, s3)), smax = fmax(fmax(s0, s1), fmax(s2, s3));
+        const double ip = 1.0 / g.pitch;
+        const int jlo = max(0, (int)fmax(-1.0, ceil((smin - 0.5 * g.tau) * ip + g.cs - 1.0)));
+        const int jhi = min(g.n_det - 1, (int)fmin((double)g.n_det, floor((smax + 0.5 * g.tau) * ip + g.cs + 1.0)));
+        for (int j = jlo; j <= jhi; ++j) {
+            const double yv = y[(size_t)vl * g.n_det + j];
+            if (yv == 0.0) continue;  // exact
+            const double sj = P.t.bin_d[j].x;
+            acc += yv * ref_weight(V, sj - 0.5 * g.tau, sj + 0.5 * g.tau, kx - hh, kx + hh, ky - hh, ky + hh);
+        }
+    }
+    P.img[(size_t)b * n * n + px] = acc / g.tau;
+}
+
 }  // namespace cbp

@@ -112,4 +112,92 @@ __global__ void cbp_cgls_dir_kernel(float* __restrict__ p, const float* __restri
         p[i] = fmaf(b, p[i], s[i]);
 }
 
+// ---- row f4: total variation and the ASD-POCS steps ------------------------
+// TV(x) = sum sqrt(dx^2 + dy^2 + eps^2), forward differences, reflective
+// boundary (DESIGN.md ledger #20); differences and roots in FP64 (the inputs
+// are FP32, so each difference is exact).
+__device__ __forceinline__ double tv_term_at(const float* x, int n, int r, int c, double eps2, double& dx,
+                                             double& dy)
+{
+    const size_t i = (size_t)r * n + c;
+    const double v = x[i];
+    dx = c + 1 < n ? (double)x[i + 1] - v : 0.0;
+    dy = r + 1 < n ? (double)x[i + n] - v : 0.0;
+    return sqrt(dx * dx + dy * dy + eps2);
+}
+
+// grad[b][r][c] = d TV / d x[b][r][c]
+__global__ void cbp_tv_gradient_kernel(const float* __restrict__ x, float* __restrict__ grad, int n,
+                                       int64_t count, double eps)
+{
+    const double eps2 = eps * eps;
+    const int64_t plane = (int64_t)n * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float* xb = x + (i / plane) * plane;
+        const int r = (int)((i % plane) / n), c = (int)(i % n);
+        double dx, dy;
+        const double m = tv_term_at(xb, n, r, c, eps2, dx, dy);
+        double gsum = -(dx + dy) / m;
+        if (c > 0) {  // left neighbour's term, through its dx
+            const double ml = tv_term_at(xb, n, r, c - 1, eps2, dx, dy);
+            gsum += dx / ml;
+        }
+        if (r > 0) {  // upper neighbour's term, through its dy
+            const double mu = tv_term_at(xb, n, r - 1, c, eps2, dx, dy);
+            gsum += dy / mu;
+        }
+        grad[i] = (float)gsum;
+    }
+}
+
+// FP64 partial sums over a fixed index set per block: mode 0 = TV terms,
+// mode 1 = (a - b)^2
+__global__ void __launch_bounds__(VEC_BLOCK) cbp_sum_partial_kernel(const float* __restrict__ a,
+                                                                    const float* __restrict__ b, int n,
+                                                                    int64_t count, double eps, int mode,
+                                                                    double* __restrict__ part)
+{
+    __shared__ double red[VEC_BLOCK];
+    double s = 0.0;
+    const int64_t plane = (int64_t)n * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (mode == 0) {
+            double dx, dy;
+            s += tv_term_at(a + (i / plane) * plane, n, (int)((i % plane) / n), (int)(i % n), eps * eps, dx, dy);
+        } else {
+            const double d = (double)a[i] - (double)b[i];
+            s += d * d;
+        }
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = VEC_BLOCK / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// x -= alpha sqrt(dp2) g / sqrt(gg)  (a normalised TV descent step of length
+// alpha |data step|); gg == 0 leaves x unchanged
+__global__ void cbp_tv_step_kernel(float* __restrict__ x, const float* __restrict__ g, int64_t count,
+                                   const double* __restrict__ gg, const double* __restrict__ alpha,
+                                   const double* __restrict__ dp2)
+{
+    const double n2 = *gg;
+    const float a = n2 > 0.0 ? (float)(*alpha * sqrt(*dp2) / sqrt(n2)) : 0.0f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = fmaf(-a, g[i], x[i]);
+}
+
+// alpha *= alpha_red when |TV steps| > r_max |data step|
+__global__ void cbp_asd_adapt_kernel(double* alpha, const double* dp2, const double* dg2, double r_max,
+                                     double alpha_red)
+{
+    if (threadIdx.x == 0 && blockIdx.x == 0 && sqrt(*dg2) > r_max * sqrt(*dp2)) *alpha *= alpha_red;
+}
+
 }  // namespace cbp

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     L = ctypes.CDLL(cbp.LIB_PATH)
     for name in _declared_functions():
         assert hasattr(L, name), name
-    assert cbp.version() == 110
+    assert cbp.version() == 120
     assert cbp.strerror(0) == "ok"
     assert "invalid" in cbp.strerror(-1)
     assert cbp.strerror(12345) == "unknown error"

@@ -1,0 +1,115 @@
+"""Row f4 on the GPU: TV kernels, the ASD-POCS steps and the whole loop
+against the numpy FP64 oracle (oracle/tv.py, pinned in test_oracle_tv.py),
+and the reference projector's adjoint (cbp_ref_back) against the oracle's."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle as O
+from oracle import tv as OT
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("kind", ["random", "shepp", "batch"])
+def test_tv_value_and_gradient(torch_cuda, kind):
+    torch = torch_cuda
+    import paper_1907_10526_b200 as cbp
+    if kind == "random":
+        x = W.random_image(67, 1)
+    elif kind == "shepp":
+        x = W.shepp_logan(64)
+    else:
+        x = W.random_image(33, 2, batch=3)
+    xt = torch.from_numpy(x).cuda()
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    cbp.tv_value(xt, out)
+    want = OT.tv_value(x.astype(np.float64))
+    assert out.item() == pytest.approx(want, rel=1e-12)
+    g = cbp.tv_gradient(xt, torch.empty_like(xt)).cpu().numpy()
+    gw = OT.tv_gradient(x.astype(np.float64))
+    # FP64 inside, FP32 output
+    np.testing.assert_allclose(g, gw, rtol=1e-6, atol=1e-6)
+
+
+def test_asd_scalar_steps(torch_cuda):
+    torch = torch_cuda
+    import paper_1907_10526_b200 as cbp
+    d64 = dict(dtype=torch.float64, device="cuda")
+    a = torch.rand(1000, device="cuda")
+    b = torch.rand(1000, device="cuda")
+    out = torch.zeros(1, **d64)
+    cbp.diff_norm2(a, b, out)
+    assert out.item() == pytest.approx(float(((a.double() - b.double()) ** 2).sum()), rel=1e-12)
+    x = a.clone()
+    gg = torch.tensor([4.0], **d64)        # |g| = 2
+    alpha = torch.tensor([0.5], **d64)
+    dp2 = torch.tensor([9.0], **d64)       # |dp| = 3  -> step 1.5, x -= 1.5 g / 2
+    cbp.tv_step(x, b, gg, alpha, dp2)
+    np.testing.assert_allclose(x.cpu().numpy(), (a - 0.75 * b).cpu().numpy(), rtol=1e-6, atol=1e-6)
+    cbp.asd_adapt(alpha, dp2, torch.tensor([10.0], **d64), 1.0, 0.5)   # sqrt(10) > 3: reduce
+    assert alpha.item() == 0.25
+    cbp.asd_adapt(alpha, dp2, torch.tensor([8.0], **d64), 1.0, 0.5)    # sqrt(8) < 3: keep
+    assert alpha.item() == 0.25
+    zero = torch.zeros(1, **d64)
+    x2 = a.clone()
+    cbp.tv_step(x2, b, zero, alpha, dp2)  # |g| = 0: unchanged
+    assert torch.equal(x2, a)
+
+
+def test_ref_back_matches_oracle_and_is_adjoint(torch_cuda):
+    torch = torch_cuda
+    import paper_1907_10526_b200 as cbp
+    g = dict(W.FIG7, n=40, n_views=16, n_det=90)
+    y = W.random_sino(16, 90, 3).astype(np.float64)
+    got = cbp.ref_back(g, torch.from_numpy(y).cuda()).cpu().numpy()
+    want = O.ref_back(g, y)
+    assert np.abs(got - want).max() / np.abs(want).max() < 1e-9
+    c = W.random_image(40, 4)
+    ay = cbp.ref_forward(g, torch.from_numpy(c).cuda()).cpu().numpy()
+    lhs, rhs = float((ay * y).sum()), float((c.astype(np.float64) * got).sum())
+    assert abs(lhs - rhs) / abs(lhs) < 1e-12
+
+
+def _fig10_small():
+    # Fig. 10's scanner, reduced: 64 px of 2 mm, 16 views
+    return dict(n=64, pixel=2.0, n_views=16, n_det=205, det_pitch=1.0, det_width=1.0, sid=200.0,
+                sdd=400.0)
+
+
+@pytest.mark.parametrize("subsets", [1, 4, 16])
+def test_asd_pocs_matches_oracle(torch_cuda, subsets):
+    torch = torch_cuda
+    from paper_1907_10526_b200 import recon
+    g = _fig10_small()
+    truth = W.shepp_logan(64, modified=True)
+    y = O.forward(g, truth).astype(np.float32)
+    cfg = dict(n_iterations=4, beta0=1.0, beta_red=0.99, n_tv=6, alpha=0.2, alpha_red=0.9, r_max=0.9,
+               subsets=subsets)
+    x = recon.asd_pocs(g, torch.from_numpy(y).cuda(), recon.AsdPocsConfig(**cfg)).cpu().numpy()
+    ref = OT.asd_pocs(y.astype(np.float64), 64, lambda c, v0, m: O.forward(g, c, v0, m),
+                      lambda s, v0: O.back(g, s, v0), OT.AsdPocsConfig(**cfg))
+    assert _rel(x, ref) < 2e-3
+
+
+def test_asd_pocs_zero_data(torch_cuda):
+    torch = torch_cuda
+    from paper_1907_10526_b200 import recon
+    g = _fig10_small()
+    y = torch.zeros((16, 205), device="cuda")
+    x = recon.asd_pocs(g, y, recon.AsdPocsConfig(n_iterations=3, n_tv=4))
+    assert float(x.abs().max()) == 0.0

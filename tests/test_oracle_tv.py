@@ -63,8 +63,8 @@ def _small():
 def test_asd_pocs_zero_data_gives_zero():
     g = _small()
     y = np.zeros((12, 40))
-    x = tv.asd_pocs(y, 16, lambda c: oracle.ref_forward(g, c), lambda s: oracle.ref_back(g, s),
-                    tv.AsdPocsConfig(n_iterations=3, n_tv=5))
+    x = tv.asd_pocs(y, 16, lambda c, v0, m: oracle.ref_forward(g, c, v0, m),
+                    lambda s, v0: oracle.ref_back(g, s, v0), tv.AsdPocsConfig(n_iterations=3, n_tv=5, subsets=4))
     assert np.abs(x).max() == 0.0
 
 
@@ -87,3 +87,24 @@ def test_sart_fixed_point_without_tv():
     rows, cols = fwd(np.ones((16, 16))), back(np.ones_like(y))
     x = tv.sart_step(c, y, fwd, back, rows, cols, 1.0)
     np.testing.assert_allclose(x, c, atol=1e-12)
+
+
+def test_ordered_subsets_is_a_permutation_with_jumps():
+    for count in (1, 2, 3, 5, 8, 12, 16):
+        o = tv._order(count)
+        assert sorted(o) == list(range(count))
+    assert tv._order(8) == [0, 4, 2, 6, 1, 5, 3, 7]
+
+
+def test_one_subset_sweep_equals_sart_step():
+    g = _small()
+    rng = np.random.default_rng(6)
+    c = rng.random((16, 16))
+    y = oracle.ref_forward(g, c) * 1.1
+    fwd = lambda x, v0, m: oracle.ref_forward(g, x, v0, m)
+    back = lambda s, v0: oracle.ref_back(g, s, v0)
+    cfg = tv.AsdPocsConfig(n_iterations=1, n_tv=0, nonneg=False, subsets=1)
+    x = tv.asd_pocs(y, 16, fwd, back, cfg)
+    rows, cols = fwd(np.ones((16, 16)), 0, 12), back(np.ones_like(y), 0)
+    want = tv.sart_step(np.zeros((16, 16)), y, lambda z: fwd(z, 0, 12), lambda s: back(s, 0), rows, cols, 1.0)
+    np.testing.assert_allclose(x, want, atol=1e-13)
