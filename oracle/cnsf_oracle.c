@@ -73,7 +73,7 @@ void orc_view_frame(const orc_geometry* g, double theta, double u[2], double e[2
 static void detector_point_f(const orc_geometry* g, const double u[2], const double e[2],
                              double s, double q[2])
 {
-    const double d_so = g->sdd - g->sid;
+    const double d_so = g->kind == 1 ? 0.0 : g->sdd - g->sid;
     q[0] = -d_so * u[0] + s * e[0];
     q[1] = -d_so * u[1] + s * e[1];
 }
@@ -91,6 +91,13 @@ void orc_detector_point(const orc_geometry* g, double theta, double s, double q[
 static void ray_frame_f(const orc_geometry* g, const double u[2], const double e[2],
                         const double p[2], double s, double v[2], double r[2])
 {
+    if (g->kind == 1) { /* parallel beam: every ray runs along -u */
+        v[0] = -u[0];
+        v[1] = -u[1];
+        r[0] = e[0];
+        r[1] = e[1];
+        return;
+    }
     double q[2];
     detector_point_f(g, u, e, s, q);
     const double dx = q[0] - p[0], dy = q[1] - p[1];
@@ -118,6 +125,7 @@ void orc_ray_frame(const orc_geometry* g, double theta, double s, double v[2], d
 static double perspective_f(const orc_geometry* g, const double u[2], const double e[2],
                             const double p[2], const double x[2])
 {
+    if (g->kind == 1) return dot2(x, e); /* parallel: orthogonal projection onto e */
     const double xp[2] = {x[0] - p[0], x[1] - p[1]};
     const double depth = -dot2(xp, u); /* (p - x).u */
     return g->sdd * dot2(xp, e) / depth;
@@ -145,6 +153,9 @@ static double effective_blur_f(const orc_geometry* g, const double u[2], const d
     double qp[2], qm[2];
     detector_point_f(g, u, e, s + 0.5 * tau, qp);
     detector_point_f(g, u, e, s - 0.5 * tau, qm);
+    if (g->kind == 1) /* parallel (Theorem 1): the edges move along u onto the
+                         plane through k, their distance along r is unchanged */
+        return fabs(dot2(qp, r) - dot2(qm, r));
     const double kp[2] = {k[0] - p[0], k[1] - p[1]};
     const double dp[2] = {qp[0] - p[0], qp[1] - p[1]};
     const double dm[2] = {qm[0] - p[0], qm[1] - p[1]};
@@ -237,10 +248,11 @@ static double footprint_f(const orc_geometry* g, const double p[2], const double
 
 double orc_footprint(const orc_geometry* g, double theta, double s, const double k[2])
 {
-    double u[2], e[2], p[2], v[2], r[2];
+    double u[2], e[2], p[2], v[2], r[2], q[2];
     orc_view_frame(g, theta, u, e, p);
     ray_frame_f(g, u, e, p, s, v, r);
-    return footprint_f(g, p, r, k);
+    detector_point_f(g, u, e, s, q);
+    return footprint_f(g, g->kind == 1 ? q : p, r, k);
 }
 
 /* Eq. 14: the blurred fan-beam footprint
@@ -253,7 +265,11 @@ static double weight_f(const orc_geometry* g, const double u[2], const double e[
                        const double k[2])
 {
     const double h = g->pixel;
-    const double pk[2] = {p[0] - k[0], p[1] - k[1]};
+    /* a point of the ray: the source, or (parallel beam) the detector point s e */
+    double q[2];
+    detector_point_f(g, u, e, s, q);
+    const double* ray_pt = g->kind == 1 ? q : p;
+    const double pk[2] = {ray_pt[0] - k[0], ray_pt[1] - k[1]};
     const double x = dot2(r, pk);
     const double tau_eff = effective_blur_f(g, u, e, p, s, v, r, k);
     const double raw[3] = {h * r[0], h * r[1], tau_eff};
@@ -277,6 +293,8 @@ static int geometry_ok(const orc_geometry* g)
 {
     if (!g || g->n < 1 || !(g->pixel > 0) || g->n_views < 1 || g->n_det < 1) return 0;
     if (!(g->det_pitch > 0) || !(g->det_width > 0)) return 0;
+    if (g->kind == 1) return 1; /* parallel beam: no source */
+    if (g->kind != 0) return 0;
     if (!(g->sid > 0) || !(g->sdd >= g->sid)) return 0;
     /* S:249/S:251 (ledger #14): every pixel strictly between source and
      * detector for every view, i.e. the FOV's circumscribed circle strictly
@@ -530,7 +548,12 @@ static double ref_chord_f(const orc_geometry* g, const double u[2], const double
 {
     double q[2];
     detector_point_f(g, u, e, s, q);
-    const double d[2] = {q[0] - p[0], q[1] - p[1]};
+    double d[2] = {q[0] - p[0], q[1] - p[1]};
+    if (g->kind == 1) { /* parallel: the line through q along u */
+        d[0] = u[0];
+        d[1] = u[1];
+        p = q;
+    }
     const double len = sqrt(d[0] * d[0] + d[1] * d[1]);
     const double hh = 0.5 * g->pixel;
     double t0 = -1e300, t1 = 1e300;

@@ -31,6 +31,9 @@ typedef struct orc_geometry {
     double  det_width;  /* tau, bin width used by the blur (Eq. 2)                */
     double  sid;        /* D_po, source to rotation centre                        */
     double  sdd;        /* D_ps, source to detector; D_so = D_ps - D_po           */
+    int32_t kind;       /* 0 = fan beam, flat detector (the paper's case);
+                           1 = parallel beam (Eq. 9-10, row f3): rays along -u through
+                               s e, sid and sdd unused                              */
 } orc_geometry;
 
 /* --- geometry steps (Eq. 4, Eq. 11, Eq. 13) ---------------------- */
