@@ -58,6 +58,11 @@ extern "C" {
 #define CBP_ECUDA  -2  /* CUDA error at launch / copy / allocation of workspace   */
 #define CBP_ENOMEM -3  /* host allocation failure                                 */
 
+/* Scanner kinds (cbp_geometry_t.kind) */
+#define CBP_FAN_FLAT  0  /* fan beam, flat detector: the paper's geometry          */
+#define CBP_PARALLEL  1  /* parallel beam (Eq. 9-10, row f3): the rays of view v run along
+                            -u_v through s e_v; sid and sdd are unused (must be finite)      */
+
 /* Scanner and grid (P:96-106 geometry; P:157-159 image; P:124 and P:416
  * detector).  All lengths in mm.                                            */
 typedef struct cbp_geometry {
@@ -69,13 +74,18 @@ typedef struct cbp_geometry {
     double  det_width;  /* bin width tau > 0 (the detector blur, Eq. 2)                */
     double  sid;        /* D_po, source to rotation centre; n h / sqrt(2) < sid        */
     double  sdd;        /* D_ps, source to detector; sdd >= sid (D_so = sdd - sid)     */
+    int32_t kind;       /* CBP_FAN_FLAT (0) or CBP_PARALLEL (1)                         */
 } cbp_geometry_t;
 
 /* Validate a geometry (no CUDA call).  CBP_EINVAL if n < 1, pixel <= 0,
- * n_views < 1, n_det < 1, det_pitch <= 0, det_width <= 0, sid <= 0,
- * sdd < sid, det_width >= 2 sdd, any value non-finite, or the field of view's
- * circumscribed circle n h / sqrt(2) is not strictly inside the source orbit
- * (every pixel must lie strictly in front of the source). */
+ * n_views < 1, n_det < 1, det_pitch <= 0, det_width <= 0, any value
+ * non-finite, kind unknown, or (fan beam) sid <= 0, sdd < sid,
+ * det_width >= 2 sdd, or the field of view's circumscribed circle
+ * n h / sqrt(2) is not strictly inside the source orbit (every pixel
+ * must lie strictly in front of the source).  In parallel beam W is the
+ * 3-direction box spline M_{[h|sin|, h|cos|, tau]}(s_j - k.e) -- exact
+ * (Theorem 1).  The reference projector (cbp_ref_*) is fan-beam
+ * only. */
 int cbp_validate(const cbp_geometry_t* g);
 
 /* Forward projection y = A c (Eq. 6) for views [view_begin,

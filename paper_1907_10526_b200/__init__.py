@@ -41,7 +41,10 @@ class cbp_geometry_t(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("pixel", ctypes.c_double),
                 ("n_views", ctypes.c_int32), ("n_det", ctypes.c_int32),
                 ("det_pitch", ctypes.c_double), ("det_width", ctypes.c_double),
-                ("sid", ctypes.c_double), ("sdd", ctypes.c_double)]
+                ("sid", ctypes.c_double), ("sdd", ctypes.c_double), ("kind", ctypes.c_int32)]
+
+
+FAN_FLAT, PARALLEL = 0, 1  # cbp_geometry_t.kind
 
 
 @dataclass(frozen=True)
@@ -55,15 +58,16 @@ class Geometry:
     det_width: float
     sid: float
     sdd: float
+    kind: int = FAN_FLAT
 
     @classmethod
     def from_dict(cls, d: dict) -> "Geometry":
-        return cls(**{k: d[k] for k in cls.__dataclass_fields__})
+        return cls(**{k: d[k] for k in cls.__dataclass_fields__ if k in d})
 
     def c_struct(self) -> cbp_geometry_t:
         return cbp_geometry_t(int(self.n), float(self.pixel), int(self.n_views), int(self.n_det),
                               float(self.det_pitch), float(self.det_width), float(self.sid),
-                              float(self.sdd))
+                              float(self.sdd), int(self.kind))
 
     def as_dict(self) -> dict:
         return asdict(self)

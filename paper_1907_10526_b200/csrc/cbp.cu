@@ -39,6 +39,7 @@ cbp::GeomDev to_dev(const cbp_geometry_t& g)
     d.tau = g.det_width;
     d.sid = g.sid;
     d.sdd = g.sdd;
+    d.parallel = g.kind == CBP_PARALLEL ? 1 : 0;
     d.c0 = 0.5 * (double)(g.n - 1);
     d.cs = 0.5 * (double)(g.n_det - 1);
     return d;
@@ -47,6 +48,7 @@ cbp::GeomDev to_dev(const cbp_geometry_t& g)
 // ---- per-(geometry, device) tables --------------------------------------
 struct TableKey {
     int device;
+    int32_t kind;
     int32_t n_views, n_det;
     double pitch, tau, sdd;
     bool operator<(const TableKey& o) const
@@ -71,6 +73,7 @@ int get_tables(const cbp_geometry_t& g, cudaStream_t stream, cbp::Tables& out)
     TableKey key;
     std::memset(&key, 0, sizeof(key));
     key.device = dev;
+    key.kind = g.kind;
     key.n_views = g.n_views;
     key.n_det = g.n_det;
     key.pitch = g.det_pitch;
@@ -232,7 +235,8 @@ int scratch_alloc(void** p, size_t bytes, cudaStream_t stream)
 // tau'_max <= (tau / D_ps) (D_po + n h / sqrt(2))
 int fp_pad_width(const cbp_geometry_t& g)
 {
-    const double taumax = g.det_width / g.sdd * (g.sid + g.n * g.pixel / std::sqrt(2.0));
+    const double taumax = g.kind == CBP_PARALLEL ? g.det_width
+                                                 : g.det_width / g.sdd * (g.sid + g.n * g.pixel / std::sqrt(2.0));
     const double sigq = 1.0 + taumax / (std::sqrt(2.0) * g.pixel);
     return (int)std::floor(2.0 * sigq) + 2;
 }
@@ -506,9 +510,11 @@ int cbp_validate(const cbp_geometry_t* g)
 {
     if (!g) return CBP_EINVAL;
     if (g->n < 1 || g->n_views < 1 || g->n_det < 1) return CBP_EINVAL;
-    if (!finite_pos(g->pixel) || !finite_pos(g->det_pitch) || !finite_pos(g->det_width) ||
-        !finite_pos(g->sid) || !finite_pos(g->sdd))
+    if (!finite_pos(g->pixel) || !finite_pos(g->det_pitch) || !finite_pos(g->det_width))
         return CBP_EINVAL;
+    if (g->kind == CBP_PARALLEL) return std::isfinite(g->sid) && std::isfinite(g->sdd) ? CBP_OK : CBP_EINVAL;
+    if (g->kind != CBP_FAN_FLAT) return CBP_EINVAL;
+    if (!finite_pos(g->sid) || !finite_pos(g->sdd)) return CBP_EINVAL;
     if (g->sdd < g->sid) return CBP_EINVAL;
     if (g->det_width >= 2.0 * g->sdd) return CBP_EINVAL;
     const double radius = 0.5 * (double)g->n * g->pixel * std::sqrt(2.0);
@@ -814,6 +820,7 @@ int cbp_ref_forward(const cbp_geometry_t* g, const float* image, double* sino, i
 {
     int rc = check_common(g, image, sino, batch, view_begin, view_count);
     if (rc != CBP_OK) return rc;
+    if (g->kind != CBP_FAN_FLAT) return CBP_EINVAL;
     if (((uintptr_t)sino & 7) || pointer_kind(image) != 1 || pointer_kind(sino) != 1) return CBP_EINVAL;
     cudaStream_t stream = (cudaStream_t)stream_;
     cbp::Tables t;
@@ -836,6 +843,7 @@ int cbp_ref_back(const cbp_geometry_t* g, const double* sino, double* image, int
 {
     int rc = check_common(g, sino, image, batch, view_begin, view_count);
     if (rc != CBP_OK) return rc;
+    if (g->kind != CBP_FAN_FLAT) return CBP_EINVAL;
     if (((uintptr_t)sino & 7) || ((uintptr_t)image & 7) || pointer_kind(image) != 1 || pointer_kind(sino) != 1)
         return CBP_EINVAL;
     cudaStream_t stream = (cudaStream_t)stream_;

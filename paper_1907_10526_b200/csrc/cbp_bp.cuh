@@ -86,6 +86,39 @@ __device__ void bp_view_header(const GeomDev& g, const Tables& t, int v, double 
     const double cth = cs.x, sth = cs.y;
     const double kau = kax * cth + kay * sth;   // k_a . u
     const double kae = -kax * sth + kay * cth;  // k_a . e
+    if (g.parallel) {  // row f3: P(k) = k.e, linear in (dc, dr); no depth, tau' = tau
+        const double ua = kae / g.pitch + g.cs;
+        const double ja = floor(ua + 0.5);
+        const float h = (float)g.h, ip = (float)(1.0 / g.pitch), fc = (float)cth, fs = (float)sth;
+        const float nx = -h * fs * ip, ny = -h * fc * ip;  // dk = (dc h, -dr h)
+        const float umin = -fabsf(nx) * hcx - fabsf(ny) * hcy, umax = -umin;
+        const float urel = (float)(ua - ja);
+        // |s_j - P(k)| < (A + C + tau)/2, A + C = h (|sin| + |cos|) for every ray of the view
+        const float cW = 0.5f * (h * (fabsf(fs) + fabsf(fc)) + (float)g.tau) * ip * (1.0f + 1e-5f);
+        const float jsh = (float)ja;
+        const float jl = fmaxf(0.0f, floorf(jsh + urel + umin - cW - 0.01f));
+        const float jh = fminf((float)(g.n_det - 1), ceilf(jsh + urel + umax + cW + 0.01f));
+        H.ja = (int)ja;
+        H.jlo = (int)jl;
+        H.jhi = (int)jh;
+        float phi = atan2f(-fs, -fc);  // the rays run along -u
+        if (phi < 0.0f) phi += 3.14159265f;
+        H.bucket = min(BP_BUCKETS - 1, max(0, (int)(phi * (BP_BUCKETS / 3.14159265f))));
+        H.urel = urel;
+        H.nx = nx;
+        H.ny = ny;
+        H.cW = cW;
+        H.dena = 1.0f;
+        H.dx = 0.0f;
+        H.dy = 0.0f;
+        H.npass_f = jl <= jh ? (float)(((int)(jh - jl) + BP_NB) / BP_NB) : 0.0f;
+        H.delta_a = 1.0;  // s'(k_a) = (j - ja) Delta_s - f_a (with 1/L_j = 1 in the tables)
+        H.f_a = kae - (ja - g.cs) * g.pitch;
+        H.cth = cth;
+        H.sth = sth;
+        H.kae = kae;
+        return;
+    }
     const double delta = g.sid - kau;           // depth (p - k_a) . u
     const double Pa = g.sdd * kae / delta;      // Eq. 4
     const double ua = Pa / g.pitch + g.cs;      // continuous bin coordinate
@@ -191,17 +224,17 @@ __device__ void bp_build_entry(const GeomDev& g, const Tables& t, const BPHeader
 {
     const double2 bd = t.bin_d[j];
     const float4 bf = t.bin_f[j];
-    const double invL = bd.y;
-    const double sphi = bd.x * invL, cphi = g.sdd * invL;
+    const double invL = bd.y;  // parallel: 1
+    const double sphi = g.parallel ? 0.0 : bd.x * invL, cphi = g.parallel ? 1.0 : g.sdd * invL;
     const double rxd = sphi * H.cth - cphi * H.sth;  // r_j (Eq. 11)
     const double ryd = cphi * H.cth + sphi * H.sth;
     // s'(k_a) = delta_a (s_j - P(k_a)) / L_j with s_j - P(k_a) = (j - ja) Delta_s - f_a  (FP64)
     const double xa = H.delta_a * ((double)(j - H.ja) * g.pitch - H.f_a) * invL;
     const float rx = (float)rxd, ry = (float)ryd;
     const float da = bf.y * (float)H.delta_a + bf.x * (float)H.kae;  // (k_a - p) . v_j
-    const float h = (float)g.h, gj = bf.z;
+    const float h = (float)g.h, gj = g.parallel ? 0.0f : bf.z;
     const float A = fmaxf(fabsf(rx), fabsf(ry)) * h, C = fminf(fabsf(rx), fabsf(ry)) * h;
-    const float Ba = gj * da;
+    const float Ba = g.parallel ? (float)g.tau : gj * da;  // parallel: tau' = tau, no slopes
     const float tx = -gj * ry * h, ty = -gj * rx * h;  // dtau'/dc, dtau'/dr
     const float zsx = -rx * h + 0.5f * tx, zsy = ry * h + 0.5f * ty;
     E.a = make_float4((float)(xa + 0.5 * ((double)A - (double)C) + 0.5 * (double)Ba), zsx, zsy, Ba);

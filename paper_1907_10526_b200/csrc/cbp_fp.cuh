@@ -398,18 +398,19 @@ __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_f
     const double2 cs = P.t.view_cs[v];
     const double2 bd = P.t.bin_d[j];
     const double cth = cs.x, sth = cs.y, s = bd.x, invL = bd.y;
-    const double sphi = s * invL, cphi = g.sdd * invL;
-    const double rx = sphi * cth - cphi * sth;  // r_j = (D_ps e + s_j u) / L_j
+    const double sphi = g.parallel ? 0.0 : s * invL, cphi = g.parallel ? 1.0 : g.sdd * invL;
+    const double rx = sphi * cth - cphi * sth;  // r_j = (D_ps e + s_j u) / L_j  (parallel: e)
     const double ry = cphi * cth + sphi * sth;
     const double vx = -ry, vy = rx;             // v_j = (-D_ps u + s_j e) / L_j
     const double h = g.h, c0 = g.c0;
-    // s'(row, col) = X00 + col * bcol + row * brow   (r.p = s_j D_po / L_j)
-    const double X00 = s * g.sid * invL + h * c0 * (rx - ry);
+    // s'(row, col) = X00 + col * bcol + row * brow   (r.p = s_j D_po / L_j; parallel: s' = s_j - k.e)
+    const double X00 = (g.parallel ? s : s * g.sid * invL) + h * c0 * (rx - ry);
     const double bcol = -rx * h, brow = ry * h;
-    // d(row, col) = (k - p).v = D00 + col * dcol + row * drow  (p.v = -D_po D_ps / L_j)
-    const double D00 = g.sid * g.sdd * invL + h * c0 * (vy - vx);
-    const double dcol = vx * h, drow = -vy * h;
-    const double gj = (double)P.t.bin_f[j].z;
+    // d(row, col) = (k - p).v = D00 + col * dcol + row * drow  (p.v = -D_po D_ps / L_j);
+    // parallel: tau' = tau everywhere (g_j d = 1 * tau)
+    const double D00 = g.parallel ? g.tau : g.sid * g.sdd * invL + h * c0 * (vy - vx);
+    const double dcol = g.parallel ? 0.0 : vx * h, drow = g.parallel ? 0.0 : -vy * h;
+    const double gj = g.parallel ? 1.0 : (double)P.t.bin_f[j].z;
 
     const bool rows_major = fabs(rx) >= fabs(ry);
     const double a_i = rows_major ? brow : bcol;  // step of s' along the line index

@@ -27,8 +27,13 @@ __global__ void cbp_tables_kernel(GeomDev g, double2* view_cs, double2* bin_d, f
         const double invL = 1.0 / L;
         const double hts = 0.5 * g.tau * s;
         const double gj = g.tau * g.sdd * L2 / (L2 * L2 - hts * hts);
-        bin_d[t] = make_double2(s, invL);
-        bin_f[t] = make_float4((float)(s * invL), (float)(g.sdd * invL), (float)gj, 0.0f);
+        if (g.parallel) {  // every ray is perpendicular to the detector: phi = 0, tau' = tau
+            bin_d[t] = make_double2(s, 1.0);
+            bin_f[t] = make_float4(0.0f, 1.0f, 1.0f, 0.0f);
+        } else {
+            bin_d[t] = make_double2(s, invL);
+            bin_f[t] = make_float4((float)(s * invL), (float)(g.sdd * invL), (float)gj, 0.0f);
+        }
     }
 }
 

@@ -34,8 +34,9 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_struct_layout_matches_header():
-    # int32, (pad), double, int32, int32, double x4  -> 56 bytes on LP64
-    assert ctypes.sizeof(cbp.cbp_geometry_t) == 56
+    # int32, (pad), double, int32, int32, double x4, int32 (pad) -> 64 bytes on LP64
+    assert ctypes.sizeof(cbp.cbp_geometry_t) == 64
+    assert cbp.cbp_geometry_t.kind.offset == 56
     assert cbp.cbp_geometry_t.pixel.offset == 8
     assert cbp.cbp_geometry_t.det_pitch.offset == 24
 
