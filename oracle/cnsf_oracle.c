@@ -73,6 +73,12 @@ void orc_view_frame(const orc_geometry* g, double theta, double u[2], double e[2
 static void detector_point_f(const orc_geometry* g, const double u[2], const double e[2],
                              double s, double q[2])
 {
+    if (g->kind == 2) { /* arc detector: radius D_ps about the source, s = arc length */
+        const double gam = s / g->sdd;
+        q[0] = g->sid * u[0] + g->sdd * (-cos(gam) * u[0] + sin(gam) * e[0]);
+        q[1] = g->sid * u[1] + g->sdd * (-cos(gam) * u[1] + sin(gam) * e[1]);
+        return;
+    }
     const double d_so = g->kind == 1 ? 0.0 : g->sdd - g->sid;
     q[0] = -d_so * u[0] + s * e[0];
     q[1] = -d_so * u[1] + s * e[1];
@@ -128,6 +134,7 @@ static double perspective_f(const orc_geometry* g, const double u[2], const doub
     if (g->kind == 1) return dot2(x, e); /* parallel: orthogonal projection onto e */
     const double xp[2] = {x[0] - p[0], x[1] - p[1]};
     const double depth = -dot2(xp, u); /* (p - x).u */
+    if (g->kind == 2) return g->sdd * atan2(dot2(xp, e), depth); /* arc: D_ps x angle */
     return g->sdd * dot2(xp, e) / depth;
 }
 
@@ -294,7 +301,8 @@ static int geometry_ok(const orc_geometry* g)
     if (!g || g->n < 1 || !(g->pixel > 0) || g->n_views < 1 || g->n_det < 1) return 0;
     if (!(g->det_pitch > 0) || !(g->det_width > 0)) return 0;
     if (g->kind == 1) return 1; /* parallel beam: no source */
-    if (g->kind != 0) return 0;
+    if (g->kind != 0 && g->kind != 2) return 0;
+    if (g->kind == 2 && !(g->det_width < 3.14159 * g->sdd)) return 0;
     if (!(g->sid > 0) || !(g->sdd >= g->sid)) return 0;
     /* S:249/S:251 (ledger #14): every pixel strictly between source and
      * detector for every view, i.e. the FOV's circumscribed circle strictly

@@ -33,7 +33,11 @@ typedef struct orc_geometry {
     double  sdd;        /* D_ps, source to detector; D_so = D_ps - D_po           */
     int32_t kind;       /* 0 = fan beam, flat detector (the paper's case);
                            1 = parallel beam (Eq. 9-10, row f3): rays along -u through
-                               s e, sid and sdd unused                              */
+                               s e, sid and sdd unused;
+                           2 = fan beam, arc detector (row f3): the detector is
+                               the circle of radius D_ps about the source, s is the arc
+                               length (angle s / D_ps from the central ray), det_pitch
+                               and det_width are arc lengths                        */
 } orc_geometry;
 
 /* --- geometry steps (Eq. 4, Eq. 11, Eq. 13) ---------------------- */
