@@ -62,6 +62,10 @@ extern "C" {
 #define CBP_FAN_FLAT  0  /* fan beam, flat detector: the paper's geometry          */
 #define CBP_PARALLEL  1  /* parallel beam (Eq. 9-10, row f3): the rays of view v run along
                             -u_v through s e_v; sid and sdd are unused (must be finite)      */
+#define CBP_FAN_ARC   2  /* fan beam, arc (equiangular) detector (row f3): the detector
+                            is the circle of radius sdd about the source, s is arc length
+                            (angle s/sdd from the central ray); det_pitch and det_width are
+                            arc lengths; every bin must lie within +-90 degrees            */
 
 /* Scanner and grid (P:96-106 geometry; P:157-159 image; P:124 and P:416
  * detector).  All lengths in mm.                                            */
@@ -74,7 +78,7 @@ typedef struct cbp_geometry {
     double  det_width;  /* bin width tau > 0 (the detector blur, Eq. 2)                */
     double  sid;        /* D_po, source to rotation centre; n h / sqrt(2) < sid        */
     double  sdd;        /* D_ps, source to detector; sdd >= sid (D_so = sdd - sid)     */
-    int32_t kind;       /* CBP_FAN_FLAT (0) or CBP_PARALLEL (1)                         */
+    int32_t kind;       /* CBP_FAN_FLAT (0), CBP_PARALLEL (1) or CBP_FAN_ARC (2)        */
 } cbp_geometry_t;
 
 /* Validate a geometry (no CUDA call).  CBP_EINVAL if n < 1, pixel <= 0,
@@ -84,8 +88,9 @@ typedef struct cbp_geometry {
  * n h / sqrt(2) is not strictly inside the source orbit (every pixel
  * must lie strictly in front of the source).  In parallel beam W is the
  * 3-direction box spline M_{[h|sin|, h|cos|, tau]}(s_j - k.e) -- exact
- * (Theorem 1).  The reference projector (cbp_ref_*) is fan-beam
- * only. */
+ * (Theorem 1).  On the arc the bin of ray angle gamma subtends
+ * tau/sdd at the source, tau'(k) = 2 d tan(tau / (2 sdd)).  The reference
+ * projector (cbp_ref_*) takes the flat detector only. */
 int cbp_validate(const cbp_geometry_t* g);
 
 /* Forward projection y = A c (Eq. 6) for views [view_begin,

@@ -44,7 +44,7 @@ class cbp_geometry_t(ctypes.Structure):
                 ("sid", ctypes.c_double), ("sdd", ctypes.c_double), ("kind", ctypes.c_int32)]
 
 
-FAN_FLAT, PARALLEL = 0, 1  # cbp_geometry_t.kind
+FAN_FLAT, PARALLEL, FAN_ARC = 0, 1, 2  # cbp_geometry_t.kind
 
 
 @dataclass(frozen=True)

@@ -40,6 +40,7 @@ cbp::GeomDev to_dev(const cbp_geometry_t& g)
     d.sid = g.sid;
     d.sdd = g.sdd;
     d.parallel = g.kind == CBP_PARALLEL ? 1 : 0;
+    d.arc = g.kind == CBP_FAN_ARC ? 1 : 0;
     d.c0 = 0.5 * (double)(g.n - 1);
     d.cs = 0.5 * (double)(g.n_det - 1);
     return d;
@@ -235,8 +236,9 @@ int scratch_alloc(void** p, size_t bytes, cudaStream_t stream)
 // tau'_max <= (tau / D_ps) (D_po + n h / sqrt(2))
 int fp_pad_width(const cbp_geometry_t& g)
 {
+    const double gmax = g.kind == CBP_FAN_ARC ? 2.0 * std::tan(0.5 * g.det_width / g.sdd) : g.det_width / g.sdd;
     const double taumax = g.kind == CBP_PARALLEL ? g.det_width
-                                                 : g.det_width / g.sdd * (g.sid + g.n * g.pixel / std::sqrt(2.0));
+                                                 : gmax * (g.sid + g.n * g.pixel / std::sqrt(2.0));
     const double sigq = 1.0 + taumax / (std::sqrt(2.0) * g.pixel);
     return (int)std::floor(2.0 * sigq) + 2;
 }
@@ -513,8 +515,12 @@ int cbp_validate(const cbp_geometry_t* g)
     if (!finite_pos(g->pixel) || !finite_pos(g->det_pitch) || !finite_pos(g->det_width))
         return CBP_EINVAL;
     if (g->kind == CBP_PARALLEL) return std::isfinite(g->sid) && std::isfinite(g->sdd) ? CBP_OK : CBP_EINVAL;
-    if (g->kind != CBP_FAN_FLAT) return CBP_EINVAL;
+    if (g->kind != CBP_FAN_FLAT && g->kind != CBP_FAN_ARC) return CBP_EINVAL;
     if (!finite_pos(g->sid) || !finite_pos(g->sdd)) return CBP_EINVAL;
+    // arc: every bin (and its blur) strictly inside +-90 degrees of the central ray
+    if (g->kind == CBP_FAN_ARC &&
+        !((0.5 * (g->n_det - 1) * g->det_pitch + 0.5 * g->det_width) / g->sdd < 0.5 * 3.14159265358979))
+        return CBP_EINVAL;
     if (g->sdd < g->sid) return CBP_EINVAL;
     if (g->det_width >= 2.0 * g->sdd) return CBP_EINVAL;
     const double radius = 0.5 * (double)g->n * g->pixel * std::sqrt(2.0);

@@ -139,11 +139,53 @@ __device__ void bp_view_header(const GeomDev& g, const Tables& t, int v, double 
         umin = fminf(umin, du);
         umax = fmaxf(umax, du);
     }
+    if (g.arc) {  // row f3, arc detector: bin coordinate gamma(k) / dgam with tan gamma = k_e / delta
+        const double ta = kae / delta, gam_a = atan(ta), dgam = g.pitch / g.sdd;
+        const double uaa = gam_a / dgam + g.cs, jaa = floor(uaa + 0.5);
+        // linearise atan over the tile: gamma - gamma_a ~ (t - t_a) / (1 + t_a^2); the flat map
+        // (P - P_a) / Delta_s = D_ps (t - t_a) / Delta_s, so the slopes scale by 1 / (1 + t_a^2)
+        const float sc = (float)(1.0 / (1.0 + ta * ta));
+        const float dt = fmaxf(fabsf(umin), fabsf(umax)) * (float)(g.pitch / g.sdd);  // max |t - t_a|
+        const float E = 0.5f * 0.65f * dt * dt / (float)dgam * 1.1f + 1e-4f;  // |atan''| <= 0.65, in bins
+        const float Rt = sqrtf((hcx + 0.5f) * (hcx + 0.5f) + (hcy + 0.5f) * (hcy + 0.5f)) * h;
+        const float dmin = fd - fabsf(dx) * (hcx + 0.5f) - fabsf(dy) * (hcy + 0.5f);
+        const double dist_a = sqrt(delta * delta + kae * kae);
+        const float sigma = 0.5f * (h * 1.41421356f + (float)(2.0 * tan(0.5 * g.tau / g.sdd)) * ((float)dist_a + Rt));
+        // |gamma - gamma(k)| < asin(sigma / |k - p|) <= 1.01 sigma / delta(k); den = delta(k) <= fd + Rt
+        const float cW = 1.01f * sigma / (float)dgam + E * (fd + Rt);
+        const float urel = (float)(uaa - jaa);
+        const float jsh = (float)jaa;
+        const float jl = fmaxf(0.0f, floorf(jsh + urel + umin * sc - cW / dmin - 0.01f));
+        const float jh = fminf((float)(g.n_det - 1), ceilf(jsh + urel + umax * sc + cW / dmin + 0.01f));
+        H.ja = (int)jaa;
+        H.jlo = (int)jl;
+        H.jhi = (int)jh;
+        float phi = atan2f((float)(kay - g.sid * sth), (float)(kax - g.sid * cth));
+        if (phi < 0.0f) phi += 3.14159265f;
+        H.bucket = min(BP_BUCKETS - 1, max(0, (int)(phi * (BP_BUCKETS / 3.14159265f))));
+        H.urel = urel;
+        H.nx = nx * sc;
+        H.ny = ny * sc;
+        H.cW = cW;
+        H.dena = fd;
+        H.dx = dx;
+        H.dy = dy;
+        H.npass_f = jl <= jh ? (float)(((int)(jh - jl) + BP_NB) / BP_NB) : 0.0f;
+        H.delta_a = delta;  // depth; s'(k_a) = |p - k_a| sin(gamma_j - gamma_a) in bp_build_entry
+        H.f_a = gam_a - (jaa - g.cs) * dgam;
+        H.cth = cth;
+        H.sth = sth;
+        H.kae = kae;
+        return;
+    }
     const float urel = (float)(ua - ja);
     // |s_j - P(k)| < sigma_j L_j / delta_k  <=>  W != 0   (s' = delta (s_j - P) / L_j),
     // sigma_j = (A + C + tau') / 2 <= (h (|sin psi| + |cos psi|) + tau'_max) / 2
     const float Rt = sqrtf((hcx + 0.5f) * (hcx + 0.5f) + (hcy + 0.5f) * (hcy + 0.5f)) * h;
-    const float dmin = fd - Rt;  // > 0: every pixel is inside the FOV circle < sid
+    // least depth over the tile's pixels (depth is affine: extremes at the corners); > 0
+    // because every pixel is inside the FOV circle < sid.  (fd - Rt, the circumscribed
+    // circle, is far too low for a ragged tile near the source.)
+    const float dmin = fd - fabsf(dx) * (hcx + 0.5f) - fabsf(dy) * (hcy + 0.5f);
     const float px = (float)(g.sid * cth - kax), py = (float)(g.sid * sth - kay);
     const float taumax = (float)(g.tau / g.sdd) * (sqrtf(px * px + py * py) + Rt);  // g_j <= tau/D_ps
     const float sedge = (float)(g.cs * g.pitch);
@@ -159,7 +201,10 @@ __device__ void bp_view_header(const GeomDev& g, const Tables& t, int v, double 
         Lmax = fmaxf(L1, L2);
         const float sp1 = (s1 * fc - sdd * fs) / L1, cp1 = (sdd * fc + s1 * fs) / L1;
         const float sp2 = (s2 * fc - sdd * fs) / L2, cp2 = (sdd * fc + s2 * fs) / L2;
-        const bool peak = (fabsf(sp1) > fabsf(cp1)) != (fabsf(sp2) > fabsf(cp2));
+        // a diagonal (|sin| = |cos|) lies between the two end rays: one crossing flips the
+        // dominant axis; two need an angular span >= 90 degrees (cos(span) <= 0)
+        const bool peak = ((fabsf(sp1) > fabsf(cp1)) != (fabsf(sp2) > fabsf(cp2))) ||
+                          (sp1 * sp2 + cp1 * cp2 < 0.01f);
         const float fmx = peak ? 1.41421356f
                                : fmaxf(fabsf(sp1) + fabsf(cp1), fabsf(sp2) + fabsf(cp2));
         cW = 0.5f * (h * fmx + taumax) * Lmax * ip * (1.0f + 1e-5f);
@@ -229,7 +274,9 @@ __device__ void bp_build_entry(const GeomDev& g, const Tables& t, const BPHeader
     const double rxd = sphi * H.cth - cphi * H.sth;  // r_j (Eq. 11)
     const double ryd = cphi * H.cth + sphi * H.sth;
     // s'(k_a) = delta_a (s_j - P(k_a)) / L_j with s_j - P(k_a) = (j - ja) Delta_s - f_a  (FP64)
-    const double xa = H.delta_a * ((double)(j - H.ja) * g.pitch - H.f_a) * invL;
+    const double xa = g.arc ? sqrt(H.delta_a * H.delta_a + H.kae * H.kae) *
+                                  sin((double)(j - H.ja) * (g.pitch / g.sdd) - H.f_a)
+                            : H.delta_a * ((double)(j - H.ja) * g.pitch - H.f_a) * invL;
     const float rx = (float)rxd, ry = (float)ryd;
     const float da = bf.y * (float)H.delta_a + bf.x * (float)H.kae;  // (k_a - p) . v_j
     const float h = (float)g.h, gj = g.parallel ? 0.0f : bf.z;

@@ -30,6 +30,7 @@ namespace cbp {
 struct GeomDev {
     int n, n_views, n_det;
     int parallel;  // kind == CBP_PARALLEL (row f3): rays along -u, s' = s_j - k.e, tau' = tau
+    int arc;       // kind == CBP_FAN_ARC (row f3): bin j is the ray at angle (j - cs) pitch / sdd
     double h, pitch, tau, sid, sdd;
     double c0;  // (n - 1) / 2: pixel-centre offset (ledger #13)
     double cs;  // (n_det - 1) / 2: bin-centre offset (ledger #10)

@@ -27,7 +27,14 @@ __global__ void cbp_tables_kernel(GeomDev g, double2* view_cs, double2* bin_d, f
         const double invL = 1.0 / L;
         const double hts = 0.5 * g.tau * s;
         const double gj = g.tau * g.sdd * L2 / (L2 * L2 - hts * hts);
-        if (g.parallel) {  // every ray is perpendicular to the detector: phi = 0, tau' = tau
+        if (g.arc) {  // the arc ray at gamma is the flat ray at s = D_ps tan(gamma);
+                      // its bin subtends tau / D_ps: g_j = 2 tan(tau / (2 D_ps))
+            const double gam = ((double)t - g.cs) * g.pitch / g.sdd;
+            double sg, cg;
+            sincos(gam, &sg, &cg);
+            bin_d[t] = make_double2(g.sdd * sg / cg, cg / g.sdd);
+            bin_f[t] = make_float4((float)sg, (float)cg, (float)(2.0 * tan(0.5 * g.tau / g.sdd)), 0.0f);
+        } else if (g.parallel) {  // every ray is perpendicular to the detector: phi = 0, tau' = tau
             bin_d[t] = make_double2(s, 1.0);
             bin_f[t] = make_float4(0.0f, 1.0f, 1.0f, 0.0f);
         } else {

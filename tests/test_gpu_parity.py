@@ -333,3 +333,16 @@ def test_symmetry_ragged_odd_grid(torch_cuda):
     _assert_parity(_fp(torch_cuda, g, img), O.forward(g, img), "FP ragged sym8")
     y = W.random_sino(g["n_views"], g["n_det"], 109)
     _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), "BP ragged sym8")
+
+
+@pytest.mark.parametrize("batch", [1, 5])
+def test_close_source_ragged_tiles(torch_cuda, batch):
+    """Regression: a ragged 5-column tile next to a close source (FOV radius 34
+    of sid 40 mm) -- its circumscribed circle reaches behind the source, so the
+    BP tile range must use the least pixel depth, not anchor depth - radius."""
+    g = dict(n=37, n_views=30, n_det=101, pixel=1.3, det_pitch=1.87, det_width=1.1, sid=40.0, sdd=90.0)
+    imgs = W.random_image(37, 7, batch=batch)
+    _assert_parity(_fp(torch_cuda, g, imgs), O.forward(g, imgs), "FP close source")
+    y = W.random_sino(30, 101, 8, batch=batch)
+    _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), "BP close source")
+    assert cbp.adjoint_check(g, seed=2) <= 1e-5
