@@ -383,28 +383,29 @@ int launch_fp(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, f
 }
 
 // Number of view groups the BP splits the views into (one CTA per tile,
-// view group and slice group).  The grid should fill whole waves of the
-// resident CTA slots (the last wave of a ragged grid runs mostly idle) and
-// have >= 4 waves for dynamic load balance; each group has >= 8 views and the
-// partial images (G per slice, summed by cbp_reduce_kernel) are capped at
-// 32 / slice_groups per slice.
+// view group and slice group).  Each group costs a CTA's fixed overhead
+// (accumulator setup, the S-plane epilogue) and a partial image set that
+// cbp_reduce_kernel must read back, so the BP takes the FEWEST groups that
+// still give >= 3 waves of the resident CTA slots (dynamic scheduling then
+// balances the tail); small problems take as many groups as allowed.
+// Measured on the B200 at config 2 (256 tiles, 91 base views, 296 slots):
+// G = 3/4/5/6/8/12 -> BP 0.220/0.206/0.213/0.219/0.224/0.257 ms; the earlier
+// whole-wave score picked 8.  Each group has >= 8 views and the partial
+// images are capped at 32 / slice_groups per slice.
 int bp_groups(const cbp_geometry_t& g, int32_t slice_groups, int32_t nv, int slots)
 {
+    static const int Gforce = getenv("CBP_BP_GROUPS") ? atoi(getenv("CBP_BP_GROUPS")) : 0;  // tuning knob
+    if (Gforce > 0) return std::max(1, std::min(Gforce, (int)nv));
     const int tiles = ((g.n + cbp::BP_TILE - 1) / cbp::BP_TILE) * ((g.n + cbp::BP_TILE - 1) / cbp::BP_TILE);
     const int gmax = std::max(1, std::min(std::min(nv / 8, 64), 32 / std::max(1, (int)slice_groups)));
-    int best = 1;
-    double best_score = -1.0;
-    for (int G = 1; G <= gmax; ++G) {
+    int G = 1;
+    for (; G <= gmax; ++G) {
         const int vpg = (nv + G - 1) / G;
         const int Geff = (nv + vpg - 1) / vpg;
-        const double waves = (double)tiles * Geff * slice_groups / slots;
-        const double score = std::min(1.0, waves / 4.0) * waves / std::ceil(waves);
-        if (score > best_score + 1e-9) {
-            best_score = score;
-            best = Geff;
-        }
+        if ((double)tiles * Geff * slice_groups >= 3.0 * slots) return Geff;
     }
-    return best;
+    const int vpg = (nv + gmax - 1) / gmax;
+    return (nv + vpg - 1) / vpg;
 }
 
 template <int S>
