@@ -17,7 +17,8 @@ import os
 from dataclasses import dataclass, asdict
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcbp.so")
+# CBP_LIB_PATH: load another build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("CBP_LIB_PATH") or os.path.join(_HERE, "libcbp.so")
 
 CBP_OK, CBP_EINVAL, CBP_ECUDA, CBP_ENOMEM = 0, -1, -2, -3
 
