@@ -106,6 +106,13 @@ int cbp_forward(const cbp_geometry_t* g, const float* image, float* sino, int32_
 int cbp_back(const cbp_geometry_t* g, const float* sino, float* image, int32_t batch,
              int32_t view_begin, int32_t view_count, int32_t accumulate, void* stream);
 
+/* The normal operator out = A^T A image over all views (one FP+BP pair, the
+ * benchmark's unit): the sinogram A c lives in an internal device buffer
+ * and never crosses to the host.  Host or device pointers as cbp_forward
+ * (host pointers: the call synchronises `stream`).  Overwrites out.  Errors
+ * as cbp_forward. */
+int cbp_normal(const cbp_geometry_t* g, const float* image, float* out, int32_t batch, void* stream);
+
 /* Rotational symmetry.  Rotating the whole scanner by 90
  * degrees maps view v to view v + n_views/4, keeps every detector coordinate
  * and permutes the square pixel grid, so W(v + n_views/4, j, k) = W(v, j, R^-1 k)

@@ -23,7 +23,7 @@ LIB_PATH = os.environ.get("CBP_LIB_PATH") or os.path.join(_HERE, "libcbp.so")
 CBP_OK, CBP_EINVAL, CBP_ECUDA, CBP_ENOMEM = 0, -1, -2, -3
 
 # names declared in include/cbp.h
-ABI_FUNCTIONS = ("cbp_validate", "cbp_forward", "cbp_back", "cbp_symmetry_fold",
+ABI_FUNCTIONS = ("cbp_validate", "cbp_forward", "cbp_back", "cbp_normal", "cbp_symmetry_fold",
                  "cbp_forward_orbit", "cbp_back_orbit", "cbp_sart_residual", "cbp_sart_update",
                  "cbp_fill", "cbp_dot", "cbp_cgls_step", "cbp_cgls_direction", "cbp_ref_forward",
                  "cbp_ref_back", "cbp_tv_value", "cbp_tv_gradient", "cbp_diff_norm2", "cbp_tv_step",
@@ -93,6 +93,8 @@ def lib() -> ctypes.CDLL:
         L.cbp_forward.restype = ctypes.c_int
         L.cbp_back.argtypes = [G, fp, fp, i32, i32, i32, i32, vp]
         L.cbp_back.restype = ctypes.c_int
+        L.cbp_normal.argtypes = [G, fp, fp, i32, vp]
+        L.cbp_normal.restype = ctypes.c_int
         L.cbp_symmetry_fold.argtypes = [G, i32, i32, i32]
         L.cbp_symmetry_fold.restype = ctypes.c_int
         L.cbp_forward_orbit.argtypes = [G, fp, fp, i32, i32, vp]
@@ -206,6 +208,27 @@ def forward(geom, image, sino=None, view_begin: int = 0, view_count: int | None 
     if rc != CBP_OK:
         raise CbpError(rc, "cbp_forward")
     return sino
+
+
+def normal(geom, image, out=None, stream=None):
+    """out = A^T A image over all views (one FP+BP pair; the sinogram stays on
+    the device).  image [n, n] or [B, n, n] float32: CUDA tensor, CPU tensor or
+    numpy (host buffers: synchronous)."""
+    g = _checked(geom)
+    squeeze = image.ndim == 2
+    batch = 1 if squeeze else image.shape[0]
+    if tuple(image.shape[-2:]) != (g.n, g.n):
+        raise ValueError(f"image shape {tuple(image.shape)} does not match n={g.n}")
+    if out is None:
+        out = _empty_like(image, tuple(image.shape))
+    elif tuple(out.shape) != tuple(image.shape):
+        raise ValueError("out must have the image's shape")
+    pi, st = _ptr_and_stream(image, stream)
+    po, _ = _ptr_and_stream(out, stream)
+    rc = lib().cbp_normal(ctypes.byref(g), pi, po, batch, st)
+    if rc != CBP_OK:
+        raise CbpError(rc, "cbp_normal")
+    return out
 
 
 def ref_forward(geom, image, sino=None, view_begin: int = 0, view_count: int | None = None,

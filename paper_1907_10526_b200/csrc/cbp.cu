@@ -596,6 +596,46 @@ int cbp_back(const cbp_geometry_t* g, const float* sino, float* image, int32_t b
     return cudaStreamSynchronize(stream) == cudaSuccess ? CBP_OK : CBP_ECUDA;
 }
 
+int cbp_normal(const cbp_geometry_t* g, const float* image, float* out, int32_t batch, void* stream_)
+{
+    int rc = check_common(g, image, out, batch, 0, g ? g->n_views : 0);
+    if (rc != CBP_OK) return rc;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    cbp::Tables t;
+    if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    const int ki = pointer_kind(image), ko = pointer_kind(out);
+    if (ki < 0 || ko < 0) return CBP_EINVAL;
+    const size_t ib = sizeof(float) * (size_t)batch * g->n * g->n;
+    float* sino = nullptr;  // A c stays on the device
+    if ((rc = scratch_alloc((void**)&sino, sizeof(float) * (size_t)batch * g->n_views * g->n_det, stream)) !=
+        CBP_OK)
+        return rc;
+    std::unique_lock<std::mutex> lock(g_ws_mu, std::defer_lock);
+    void *di = (void*)image, *dout = (void*)out;
+    if (ki == 0 || ko == 0) {  // host buffers: stage through the device workspace
+        lock.lock();
+        int dev = 0;
+        cudaGetDevice(&dev);
+        Workspace& w = g_ws[dev];
+        if ((ki == 0 && (rc = ws_get(w, 0, ib, &di)) != CBP_OK) || (ko == 0 && (rc = ws_get(w, 1, ib, &dout)) != CBP_OK)) {
+            cudaFreeAsync(sino, stream);
+            return rc;
+        }
+        if (ki == 0 && cudaMemcpyAsync(di, image, ib, cudaMemcpyHostToDevice, stream) != cudaSuccess) {
+            cudaFreeAsync(sino, stream);
+            return CBP_ECUDA;
+        }
+    }
+    rc = launch_fp(*g, t, (const float*)di, sino, batch, 0, g->n_views, stream);
+    if (rc == CBP_OK) rc = launch_bp(*g, t, sino, (float*)dout, batch, 0, g->n_views, 0, stream);
+    cudaFreeAsync(sino, stream);
+    if (rc != CBP_OK) return rc;
+    if (ko == 0 && cudaMemcpyAsync(out, dout, ib, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+        return CBP_ECUDA;
+    if (ki == 0 || ko == 0) return cudaStreamSynchronize(stream) == cudaSuccess ? CBP_OK : CBP_ECUDA;
+    return CBP_OK;
+}
+
 int cbp_symmetry_fold(const cbp_geometry_t* g, int32_t batch, int32_t view_begin,
                       int32_t view_count)
 {

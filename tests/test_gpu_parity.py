@@ -346,3 +346,21 @@ def test_close_source_ragged_tiles(torch_cuda, batch):
     y = W.random_sino(30, 101, 8, batch=batch)
     _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), "BP close source")
     assert cbp.adjoint_check(g, seed=2) <= 1e-5
+
+
+@pytest.mark.parametrize("cfg,batch", [("1", 1), ("1", 3), ("2", 1)])
+def test_normal_operator(torch_cuda, cfg, batch):
+    """cbp_normal = A^T A over all views, device and host buffers, equals
+    back(forward(.)) of the same library (and, at config 1, the oracle's)."""
+    torch = torch_cuda
+    g = W.geometry(cfg)
+    img = W.random_image(g["n"], 21, batch=None if batch == 1 else batch)
+    d = torch.from_numpy(img).cuda()
+    got = cbp.normal(g, d)
+    want = cbp.back(g, cbp.forward(g, d))
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    host = cbp.normal(g, torch.from_numpy(img).pin_memory())
+    assert torch.equal(host, want.cpu())
+    if cfg == "1":
+        _assert_parity(host.numpy(), O.back(g, O.forward(g, img)), "normal cfg1")
