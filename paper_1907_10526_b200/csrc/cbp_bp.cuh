@@ -347,6 +347,56 @@ __device__ __forceinline__ void bp_pair(const BPEntry* row, const float* yrow, i
 
 // per-tile accumulators: FP64 for S <= 2, FP32 for S >= 4 (shared-memory
 // budget; each term is already a partial over a run of views)
+// one loop for both of a lane's pixel pairs (see cbp_bp_kernel)
+template <int S>
+constexpr bool BP_UNION = S == 8;
+
+// two pixel pairs over the same entries [jl, jh] (one set of shared loads,
+// two independent weight chains)
+template <int S>
+__device__ __forceinline__ void bp_pair2(const BPEntry* row, const float* yrow, int jl, int jh, int base,
+                                         float dc0, float dr0, float dc1, float dr1, float2 (&a0)[S],
+                                         float2 (&a1)[S])
+{
+    if (jh < jl) return;
+    CBP_CHECK(jl >= base && jh - base < BP_NB, "bp_pair2 jl=%d jh=%d base=%d\n", jl, jh, base);
+    const int cnt = jh - jl + 1;
+    const BPEntry* e = row + (jl - base);
+    const float* ys = yrow + (jl - base) * S;
+    for (int k = 0; k < cnt; ++k, ++e, ys += S) {
+        if constexpr (S == 1) {
+            const float yw = e->c.w;
+            const float2 w0 = bp_weight(e, dc0, dr0), w1 = bp_weight(e, dc1, dr1);
+            a0[0] = __ffma2_rn(make_float2(yw, yw), w0, a0[0]);
+            a1[0] = __ffma2_rn(make_float2(yw, yw), w1, a1[0]);
+        } else {
+            const float hA = e->c.w;
+            const float2 w0 = __fmul2_rn(bp_weight(e, dc0, dr0), make_float2(hA, hA));
+            const float2 w1 = __fmul2_rn(bp_weight(e, dc1, dr1), make_float2(hA, hA));
+            if constexpr (S == 2) {
+                const float2 y2 = *reinterpret_cast<const float2*>(ys);
+                a0[0] = __ffma2_rn(make_float2(y2.x, y2.x), w0, a0[0]);
+                a0[1] = __ffma2_rn(make_float2(y2.y, y2.y), w0, a0[1]);
+                a1[0] = __ffma2_rn(make_float2(y2.x, y2.x), w1, a1[0]);
+                a1[1] = __ffma2_rn(make_float2(y2.y, y2.y), w1, a1[1]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < S; q += 4) {
+                    const float4 y4 = *reinterpret_cast<const float4*>(ys + q);
+                    a0[q] = __ffma2_rn(make_float2(y4.x, y4.x), w0, a0[q]);
+                    a0[q + 1] = __ffma2_rn(make_float2(y4.y, y4.y), w0, a0[q + 1]);
+                    a0[q + 2] = __ffma2_rn(make_float2(y4.z, y4.z), w0, a0[q + 2]);
+                    a0[q + 3] = __ffma2_rn(make_float2(y4.w, y4.w), w0, a0[q + 3]);
+                    a1[q] = __ffma2_rn(make_float2(y4.x, y4.x), w1, a1[q]);
+                    a1[q + 1] = __ffma2_rn(make_float2(y4.y, y4.y), w1, a1[q + 1]);
+                    a1[q + 2] = __ffma2_rn(make_float2(y4.z, y4.z), w1, a1[q + 2]);
+                    a1[q + 3] = __ffma2_rn(make_float2(y4.w, y4.w), w1, a1[q + 3]);
+                }
+            }
+        }
+    }
+}
+
 template <int S>
 using bp_acc_t = typename std::conditional<(S >= 4), float, double>::type;
 
@@ -571,10 +621,16 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                     }
                     bucket = hi.w;
                     horiz = bucket_horiz(bucket);
-                    const uint16_t* order = P.pairs + bucket * BP_PAIRS + (tid >> 5) * 64 + (tid & 31);
+                    // the lane's two pairs are neighbours in the lateral order: nearly the
+                    // same bins, so one loop over the union of their ranges serves both
+                    // (only at S = 8, measured: S = 4 spills under its 3-CTA register
+                    // budget, S = 1 is 3% slower; they keep two loops with pairs 32 apart)
+                    constexpr int PSTEP = BP_UNION<S> ? 1 : 32;
+                    const uint16_t* order = P.pairs + bucket * BP_PAIRS + (tid >> 5) * 64 +
+                                            (BP_UNION<S> ? 2 * (tid & 31) : (tid & 31));
                     CBP_CHECK(bucket >= 0 && bucket < BP_BUCKETS, "bucket %d\n", bucket);
                     e0 = __ldg(order);
-                    e1 = __ldg(order + 32);
+                    e1 = __ldg(order + PSTEP);
                     const float sx = horiz ? 1.0f : 0.0f, sy = 1.0f - sx;  // pair step (dc, dr)
                     const float c0 = (float)(e0 & 31) - hcx, r0 = (float)(e0 >> 5) - hcy;
                     const float c1 = (float)(e1 & 31) - hcx, r1 = (float)(e1 >> 5) - hcy;
@@ -590,6 +646,7 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                 const float4 hf = *reinterpret_cast<const float4*>(&H.urel);  // urel, nx, ny, cW
                 const float4 hd = *reinterpret_cast<const float4*>(&H.dena);  // dena, dx, dy, -
                 const int jmax = min(hi.z, base + BP_NB - 1);
+                int jl2 = 1 << 30, jh2 = -(1 << 30);
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
                     const float2 dcp = p ? dc1 : dc0, drp = p ? dr1 : dr0;
@@ -608,11 +665,18 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                     const float hi2 = fmaxf(fminf(fmaxf(u.x + w.x, u.y + w.y), 1e6f), -1e6f);
                     const int jl = max(hi.x + __float2int_rd(lo) + 1, base);
                     const int jh = min(hi.x + __float2int_ru(hi2) - 1, jmax);
-                    if (p == 0)
+                    if constexpr (BP_UNION<S>) {
+                        jl2 = min(jl2, jl);
+                        jh2 = max(jh2, jh);
+                    } else if (p == 0) {
                         bp_pair<S>(row, yrow, jl, jh, base, dcp.x, drp.x, a0);
-                    else
+                    } else {
                         bp_pair<S>(row, yrow, jl, jh, base, dcp.x, drp.x, a1);
+                    }
                 }
+                // both pairs over the union (weights outside a pixel's support are exactly 0)
+                if constexpr (BP_UNION<S>)
+                    bp_pair2<S>(row, yrow, jl2, jh2, base, dc0.x, dr0.x, dc1.x, dr1.x, a0, a1);
             }
             // the next pass rebuilds tab (the next chunk's top barrier covers S > 1)
             if (!STAGE || pass + 1 < npass) __syncthreads();
