@@ -46,6 +46,15 @@ struct FPParams {
     // 8: the full dihedral symmetry (S = 8, cbp_pad_sym8_kernel) over base
     // views [0, n_views/8], output the natural [n_views][n_det] sinogram
     int sym_mode;
+    // > 1: each ray's lines are split into `splits` parts walked by different
+    // CTAs (blockIdx.z = group * splits + part).  Every warp stores its FP64
+    // partial totals to `part`, then counts itself in `counter` (one per warp
+    // item, zeroed before the launch); the last arriving part sums all parts in
+    // part order and writes the output once: deterministic.  Used when the grid
+    // would otherwise be short of ~6 waves (the ragged last wave dominated).
+    int splits;
+    double* part;  // [warp item][splits][S][32]
+    int* counter;  // [warp item]
 };
 
 constexpr int FP_BLOCK = 128;
@@ -382,7 +391,7 @@ __device__ void fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, in
     }
 }
 
-template <int S>
+template <int S, bool SPLIT>
 __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_fp_kernel(const FPParams P)
 {
     const GeomDev& g = P.g;
@@ -390,7 +399,9 @@ __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_f
     const bool valid = jr < g.n_det;
     const int j = valid ? jr : g.n_det - 1;
     const int vl = blockIdx.y;
-    const int grp = blockIdx.z;  // slices grp S .. grp S + S - 1
+    const int splits = SPLIT ? P.splits : 1;
+    const int grp = blockIdx.z / splits;  // slices grp S .. grp S + S - 1
+    const int half = SPLIT ? blockIdx.z % splits : 0;
     const int v = P.view_begin + vl;
     const int n = g.n;
 
@@ -458,10 +469,18 @@ __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_f
 #pragma unroll
     for (int q = 0; q < S; ++q)
         acc[q * FP_BLOCK] = Kw > P.P ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;  // pad too thin: NaN
-    if (wlo <= whi && Kw <= P.P) {
+    int i0 = wlo, i1 = whi;
+    if (SPLIT) {  // this CTA's part of the warp's lines: even lengths, because the walk
+                         // takes lines in pairs (an odd range reads one line past its end --
+                         // harmless past whi, not inside the next part)
+        const int L = 2 * ((whi - wlo + 2 * splits) / (2 * splits));
+        i0 = wlo + half * L;
+        i1 = half == splits - 1 ? whi : min(whi, i0 + L - 1);
+    }
+    if (i0 <= i1 && Kw <= P.P) {
         FPRay R;
-        // lower support edge on line i: q*(i) - sig_q, as 32.32 fixed point from line wlo
-        const int64_t E0 = (int64_t)llrint((Q0 + (double)wlo * m - sig_q) * 0x1p32);
+        // lower support edge on line i: q*(i) - sig_q, as 32.32 fixed point from line i0
+        const int64_t E0 = (int64_t)llrint((Q0 + (double)i0 * m - sig_q) * 0x1p32);
         const int64_t Mfx = (int64_t)llrint(m * 0x1p32);
         R.flo = (uint32_t)(uint64_t)E0;
         R.fhi = (int32_t)(E0 >> 32);
@@ -491,31 +510,56 @@ __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_f
         const int mab_t = gj * dmax * (1.0 + 1e-6) < A ? 1 : (gj * dmin * (1.0 - 1e-6) > A ? 2 : 0);
         const int mab = __all_sync(0xffffffffu, mab_t == 1) ? 1 : (__all_sync(0xffffffffu, mab_t == 2) ? 2 : 0);
         switch (Kw) {
-            case 1: fp_walk_k<1, S>(R, mab, wlo, whi, n, P.np, P.P, acc); break;
-            case 2: fp_walk_k<2, S>(R, mab, wlo, whi, n, P.np, P.P, acc); break;
-            case 3: fp_walk_k<3, S>(R, mab, wlo, whi, n, P.np, P.P, acc); break;
-            case 4: fp_walk_k<4, S>(R, mab, wlo, whi, n, P.np, P.P, acc); break;
-            case 5: fp_walk_k<5, S>(R, mab, wlo, whi, n, P.np, P.P, acc); break;
-            case 6: fp_walk_k<6, S>(R, mab, wlo, whi, n, P.np, P.P, acc); break;
-            default: fp_walk_generic<S>(R, Kw, wlo, whi, n, P.np, P.P, acc); break;
+            case 1: fp_walk_k<1, S>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 2: fp_walk_k<2, S>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 3: fp_walk_k<3, S>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 4: fp_walk_k<4, S>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 5: fp_walk_k<5, S>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 6: fp_walk_k<6, S>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            default: fp_walk_generic<S>(R, Kw, i0, i1, n, P.np, P.P, acc); break;
         }
 #pragma unroll
         for (int q = 0; q < S; ++q) acc[q * FP_BLOCK] *= h * h / A;  // W = (h^2 / A) num / B
+    }
+    if (SPLIT) {  // combine the parts: the last one to arrive sums them in order
+        const int lane = threadIdx.x & 31;
+        const size_t item = (((size_t)grp * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * (FP_BLOCK / 32) +
+                            (threadIdx.x >> 5);
+        double* mine = P.part + (item * splits + half) * (S * 32) + lane;
+#pragma unroll
+        for (int q = 0; q < S; ++q) __stcg(mine + q * 32, acc[q * FP_BLOCK]);
+        __threadfence();
+        __syncwarp();
+        int arrived = 0;
+        if (lane == 0) arrived = atomicAdd(P.counter + item, 1);
+        arrived = __shfl_sync(0xffffffffu, arrived, 0);
+        if (arrived != splits - 1) return;  // another part finishes this item
+        __threadfence();
+        const double* all = P.part + item * splits * (S * 32) + lane;
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+            double t = 0.0;
+            for (int pp = 0; pp < splits; ++pp) t += __ldcg(all + (pp * S + q) * 32);
+            acc[q * FP_BLOCK] = t;
+        }
     }
     if (valid)
 #pragma unroll
         for (int q = 0; q < S; ++q) {
             const int b = grp * S + q;
+            float* dst = nullptr;
             if (P.sym_mode == 8) {
                 const int N = g.n_views, m = q >> 2, qq = q & 3;
                 if (m && (v == 0 || 8 * v == N)) continue;  // mirrored frame repeats a rotation
                 const int view = ((m ? N - v : v) + qq * (N / 4)) % N;
                 const int bin = m ? g.n_det - 1 - j : j;
-                P.sino[(size_t)view * g.n_det + bin] = (float)acc[q * FP_BLOCK];
-            } else if (P.sym_stride > 0)
-                P.sino[((size_t)vl + (size_t)q * P.sym_stride) * g.n_det + j] = (float)acc[q * FP_BLOCK];
-            else if (b < P.batch)
-                P.sino[((size_t)b * P.view_count + vl) * g.n_det + j] = (float)acc[q * FP_BLOCK];
+                dst = P.sino + (size_t)view * g.n_det + bin;
+            } else if (P.sym_stride > 0) {
+                dst = P.sino + ((size_t)vl + (size_t)q * P.sym_stride) * g.n_det + j;
+            } else if (b < P.batch) {
+                dst = P.sino + ((size_t)b * P.view_count + vl) * g.n_det + j;
+            }
+            if (dst) *dst = (float)acc[q * FP_BLOCK];
         }
 }
 
