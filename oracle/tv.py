@@ -64,6 +64,7 @@ class AsdPocsConfig:
     r_max: float = 0.95
     nonneg: bool = True
     subsets: int = 1
+    eps_tv: float = EPS_TV
 
 
 def sart_step(x, y, fwd: Callable, back: Callable, rows, cols, beta: float):
@@ -114,7 +115,7 @@ def asd_pocs(y: np.ndarray, n: int, fwd: Callable, back: Callable, cfg: AsdPocsC
         step = alpha * dp
         x = xd.copy()
         for _ in range(cfg.n_tv):
-            g = tv_gradient(x)
+            g = tv_gradient(x, cfg.eps_tv)
             gn = float(np.linalg.norm(g))
             if gn > 0.0:
                 x = x - step * g / gn

@@ -140,6 +140,7 @@ class AsdPocsConfig:
     r_max: float = 0.95
     nonneg: bool = True
     subsets: int = 1  # ordered subsets of contiguous views (> 1: one device)
+    eps_tv: float = 1e-8  # TV smoothing (ledger #20)
 
 
 def subset_order(count: int) -> list[int]:
@@ -222,7 +223,7 @@ def asd_pocs(geom, y_full: torch.Tensor, cfg: AsdPocsConfig, group=None, ops=Non
         cbp.diff_norm2(xd, x, dp2)
         x.copy_(xd)
         for _ in range(cfg.n_tv):  # the TV steepest-descent steps
-            cbp.tv_gradient(x, grad)
+            cbp.tv_gradient(x, grad, cfg.eps_tv)
             cbp.dot(grad, grad, gg)
             cbp.tv_step(x, grad, gg, alpha, dp2)
         cbp.diff_norm2(x, xd, dg2)
