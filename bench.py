@@ -303,9 +303,11 @@ def main():
     # views (symmetry) or slices (batch) per weight evaluation, FP and BP
     sym = 4 if orbit else cbp.symmetry_fold(g, batch, sh.begin, sh.count)
     fp_mirror = bool(os.environ.get("CBP_FP_MIRROR"))
-    folds = {"fp": sym if (sym != 8 or fp_mirror) else 4, "bp": sym}
-    if sym == 1:
-        folds = {k: (4 if batch >= 4 else (2 if batch >= 2 else 1)) for k in folds}
+    slices = 4 if batch >= 4 else (2 if batch >= 2 else 1)
+    if batch > 1:  # FP: weights shared by the batch's slices; BP: symmetry per image
+        folds = {"fp": slices, "bp": sym if sym > 1 else slices}
+    else:
+        folds = {"fp": sym if (sym != 8 or fp_mirror) else 4, "bp": sym}
     units = nw * batch if nw else None
     props = torch.cuda.get_device_properties(dev)
     peaks = measured_peaks()

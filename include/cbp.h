@@ -120,9 +120,11 @@ int cbp_normal(const cbp_geometry_t* g, const float* image, float* out, int32_t 
  * therefore serves 4 views.  With the mirror (x, y) -> (x, -y), which maps
  * view v to n_views - v, bin j to n_det-1-j and (row, col) to (n-1-row, col),
  * one weight serves 8 views when n_views % 8 == 0.  cbp_forward / cbp_back
- * use this automatically for a single image (batch == 1) over the full view
- * range; cbp_symmetry_fold returns the views per weight evaluation (8, 4 or
- * 1; CBP_EINVAL for an invalid geometry).  The environment variables
+ * use this automatically over the full view range: the FP for a single image
+ * (the 4 rotations; a batch shares each weight across 4 images instead), the
+ * BP for a single image and, image by image, for a batch.
+ * cbp_symmetry_fold returns the BP's views per weight evaluation (8, 4 or 1;
+ * CBP_EINVAL for an invalid geometry).  The environment variables
  * CBP_NO_SYMMETRY (all) and CBP_NO_MIRROR (the mirror) disable it. */
 int cbp_symmetry_fold(const cbp_geometry_t* g, int32_t batch, int32_t view_begin,
                       int32_t view_count);

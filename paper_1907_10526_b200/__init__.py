@@ -288,7 +288,7 @@ def back(geom, sino, image=None, view_begin: int = 0, accumulate: bool = False, 
 
 
 def symmetry_fold(geom, batch: int = 1, view_begin: int = 0, view_count: int | None = None) -> int:
-    """4 if the call would use the 90-degree rotational symmetry (include/cbp.h), else 1."""
+    """views per BP weight evaluation: 8 (dihedral), 4 (rotations) or 1 (include/cbp.h)."""
     g = _checked(geom)
     nv = g.n_views - view_begin if view_count is None else view_count
     return lib().cbp_symmetry_fold(ctypes.byref(g), batch, view_begin, nv)

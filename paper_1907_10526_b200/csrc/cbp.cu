@@ -457,7 +457,7 @@ int bp_groups(const cbp_geometry_t& g, int32_t slice_groups, int32_t nv, int slo
 template <int S>
 int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
                 int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream,
-                int symmode = 0)
+                int symmode = 0, int images = 1)
 {
     // symmetric: 4 "slices" (the 4 rotated frames) of one image over the base
     // views [v0, v0 + nv), sinogram [4][nv][n_det]; or 8 frames (rotations
@@ -467,7 +467,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int SG = (batch + S - 1) / S;
+    const int SG = sym ? images : (batch + S - 1) / S;
     const size_t smem = cbp::bp_smem_bytes(S);
     static std::once_flag attr[64];
     static int per_sm[64];
@@ -485,7 +485,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     const size_t plane = (size_t)g.n * g.n;
     float* part = nullptr;
     if (G > 1 || sym) {
-        int rc = scratch_alloc((void**)&part, sizeof(float) * plane * batch * G, stream);
+        int rc = scratch_alloc((void**)&part, sizeof(float) * plane * batch * G * (sym ? images : 1), stream);
         if (rc != CBP_OK) return rc;
     }
     cbp::BPParams P;
@@ -509,6 +509,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     P.out = (G > 1 || sym) ? part : img;
     P.sym_stride = symmode == 4 ? nv : 0;
     P.sym_mode = symmode;
+    P.images = sym ? images : 1;
     P.view_begin = v0;
     P.view_count = nv;
     P.groups = (G > 1 || sym) ? G : 1;
@@ -530,9 +531,10 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
         // symmetric: the G x S frame planes are already in output orientation
         const size_t count = sym ? plane : plane * batch;
         const int planes = sym ? G * batch : G;
-        const int blocks = (int)std::min<size_t>((count / 4 + 255) / 256, (size_t)sms * 8);
-        cbp::cbp_reduce_kernel<<<std::max(blocks, 1), 256, 0, stream>>>(part, img, count, planes,
-                                                                        accumulate ? 1 : 0);
+        const int outs = sym ? images : 1;  // symmetric batch: one reduction per image
+        const int blocks = (int)std::min<size_t>((count / 4 + 255) / 256, (size_t)sms * 8 / outs + 1);
+        cbp::cbp_reduce_kernel<<<dim3(std::max(blocks, 1), outs), 256, 0, stream>>>(part, img, count, planes,
+                                                                                   accumulate ? 1 : 0);
         ++g_launches;
         cudaFreeAsync(part, stream);
     }
@@ -544,6 +546,8 @@ int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, 
 {
     if (use_sym8(g, batch, v0, nv))
         return launch_bp_s<8>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8);
+    if (batch > 1 && use_sym8(g, 1, v0, nv))  // a batch: the 8 frames of each image
+        return launch_bp_s<8>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8, batch);
     if (use_sym4(g, batch, v0, nv))
         return launch_bp_s<4>(g, t, sino, img, batch, 0, g.n_views / 4, accumulate, stream, 4);
     if (batch >= 4) return launch_bp_s<4>(g, t, sino, img, batch, v0, nv, accumulate, stream);
@@ -686,7 +690,8 @@ int cbp_symmetry_fold(const cbp_geometry_t* g, int32_t batch, int32_t view_begin
                       int32_t view_count)
 {
     if (cbp_validate(g) != CBP_OK) return CBP_EINVAL;
-    return use_sym8(*g, batch, view_begin, view_count) ? 8 : (use_sym4(*g, batch, view_begin, view_count) ? 4 : 1);
+    if (use_sym8(*g, 1, view_begin, view_count)) return 8;  // the BP of any batch (per image)
+    return use_sym4(*g, batch, view_begin, view_count) ? 4 : 1;
 }
 
 static int check_orbit(const cbp_geometry_t* g, const void* a, const void* b, int32_t base_begin,

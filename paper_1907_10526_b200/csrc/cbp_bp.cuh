@@ -49,11 +49,14 @@ struct BPParams {
     int accumulate;     // groups == 1 only
     // > 0: 4-fold rotational symmetry: slice q reads sinogram rows
     // vl + q sym_stride of batch 0 and accumulates the image in the frame
-    // rotated by q (combined by cbp_sym_reduce_kernel)
+    // rotated by q (written in output orientation, summed by cbp_reduce_kernel)
     int sym_stride;
     // 8: dihedral symmetry, S = 8 frames g = R^q M^m over base views
-    // [0, n_views/8] of the natural sinogram (see cbp_pad_sym8_kernel)
+    // [0, n_views/8] of the natural sinogram; with `images` > 1 slice group sg
+    // is image sg of a batch ([images][n_views][n_det] in, partial planes
+    // [images][groups][8] out)
     int sym_mode;
+    int images;
 };
 
 constexpr int BP_TILE = 32;       // pixels per tile side
@@ -488,10 +491,11 @@ __device__ __forceinline__ void bp_y_load(const BPParams& P, int vl0, int nvc, i
     int dir = 1;
     if (P.sym_mode == 8) {  // frame (qq, m) of base view v: view_g(v), bin_m(j)
         const int N = g.n_views, v = P.view_begin + vl, m = q >> 2, qq = q & 3;
+        const size_t img = blockIdx.z / P.groups;  // image of the batch (slice group)
         int view = (m ? N - v : v) + qq * (N / 4);
         if (view >= N) view -= N;  // 0 <= v <= N/8
         if (!(m && (v == 0 || 8 * v == N))) {  // else the mirrored frame repeats a rotation: y = 0
-            src = P.sino + (size_t)view * g.n_det + (m ? g.n_det - 1 - j0 : j0);
+            src = P.sino + (img * N + view) * g.n_det + (m ? g.n_det - 1 - j0 : j0);
             dir = m ? -1 : 1;
         }
     } else if (P.sym_stride > 0) {
@@ -717,9 +721,12 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
     }
     __syncthreads();
     for (int q = 0; q < S; ++q) {
-        const int b = sg * S + q;
+        const int b = fsym ? q : sg * S + q;
         if (b >= P.batch) break;
-        float* out = P.out + (P.groups > 1 ? ((size_t)grp * P.batch + b) : (size_t)b) * plane;
+        // symmetric frames: plane (sg groups + grp) frames + q; batch: (grp batch + b)
+        const size_t pi = fsym ? ((size_t)sg * P.groups + grp) * P.batch + q
+                               : (P.groups > 1 ? (size_t)grp * P.batch + b : (size_t)b);
+        float* out = P.out + pi * plane;
         const int4 e0 = ep[q][0], e1 = ep[q][1];
         const int OR = e0.x, OC = e0.y, oh = e0.z, ow = e0.w, s0 = e1.x, sc = e1.y, sr = e1.z;
         const bp_acc_t<S>* a = acc_s + q * BP_TILE * LD;
@@ -747,9 +754,13 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
 
 // out[p] = (accumulate ? out[p] : 0) + sum_g part[g][p] over `groups` planes
 // of `count` floats, fixed order (deterministic); float4 when aligned
+// (blockIdx.y selects one of gridDim.y independent outputs: part + y groups count,
+// out + y count)
 __global__ void cbp_reduce_kernel(const float* __restrict__ part, float* __restrict__ out,
                                   size_t count, int groups, int accumulate)
 {
+    part += (size_t)blockIdx.y * groups * count;
+    out += (size_t)blockIdx.y * count;
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     const size_t t0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (((count & 3) | (reinterpret_cast<uintptr_t>(part) & 15) | (reinterpret_cast<uintptr_t>(out) & 15)) == 0) {

@@ -364,3 +364,18 @@ def test_normal_operator(torch_cuda, cfg, batch):
     assert torch.equal(host, want.cpu())
     if cfg == "1":
         _assert_parity(host.numpy(), O.back(g, O.forward(g, img)), "normal cfg1")
+
+
+@pytest.mark.parametrize("batch,n_views", [(3, 88), (5, 360)])
+def test_batched_bp_uses_per_image_dihedral_symmetry(torch_cuda, batch, n_views):
+    """A batch over a full scan with n_views % 8 == 0: the BP runs the 8 frames
+    of each image (partial planes [images][groups][8]); parity per image."""
+    g = dict(W.geometry("1"), n_views=n_views)
+    assert cbp.symmetry_fold(g, batch) == 8
+    y = W.random_sino(n_views, g["n_det"], 31, batch=batch)
+    _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), f"BP batch {batch} sym8")
+    imgs = W.random_image(g["n"], 32, batch=batch)
+    _assert_parity(_fp(torch_cuda, g, imgs), O.forward(g, imgs), f"FP batch {batch}")
+    lhs = float(np.sum(_fp(torch_cuda, g, imgs).astype(np.float64) * y))
+    rhs = float(np.sum(imgs.astype(np.float64) * _bp(torch_cuda, g, y)))
+    assert abs(lhs - rhs) / abs(lhs) <= 1e-5
