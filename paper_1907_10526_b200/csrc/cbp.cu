@@ -454,6 +454,77 @@ int bp_groups(const cbp_geometry_t& g, int32_t slice_groups, int32_t nv, int slo
     return (nv + vpg - 1) / vpg;
 }
 
+// ---- BP tile-view headers: they depend only on the geometry and the view
+// range, so they are computed once and cached per device (up to 16 MB each,
+// 256 MB in all; larger sets are recomputed per call into stream scratch)
+struct HdrKey {
+    int device;
+    int32_t n, n_views, n_det, kind, v0, nv;
+    double pixel, pitch, tau, sid, sdd;
+    bool operator<(const HdrKey& o) const { return std::memcmp(this, &o, sizeof(HdrKey)) < 0; }
+};
+std::mutex g_hdr_mu;
+std::map<HdrKey, cbp::BPHeader*> g_hdrs;
+size_t g_hdr_bytes = 0;
+
+// *out: the headers of (g, [v0, v0 + nv)); *owned: the caller must free them
+// (stream-ordered) after use
+int get_headers(const cbp_geometry_t& g, const cbp::Tables& t, int32_t v0, int32_t nv, cudaStream_t stream,
+                const cbp::BPHeader** out, cbp::BPHeader** owned)
+{
+    const int tiles = (g.n + cbp::BP_TILE - 1) / cbp::BP_TILE;
+    const size_t bytes = sizeof(cbp::BPHeader) * tiles * tiles * nv;
+    const dim3 grid(tiles * tiles, (nv + 127) / 128);
+    *owned = nullptr;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return CBP_ECUDA;
+    HdrKey key;
+    std::memset(&key, 0, sizeof(key));
+    key.device = dev;
+    key.n = g.n;
+    key.n_views = g.n_views;
+    key.n_det = g.n_det;
+    key.kind = g.kind;
+    key.v0 = v0;
+    key.nv = nv;
+    key.pixel = g.pixel;
+    key.pitch = g.det_pitch;
+    key.tau = g.det_width;
+    key.sid = g.sid;
+    key.sdd = g.sdd;
+    {
+        std::lock_guard<std::mutex> lock(g_hdr_mu);
+        auto it = g_hdrs.find(key);
+        if (it != g_hdrs.end()) {
+            *out = it->second;
+            return CBP_OK;
+        }
+        if (bytes <= (16u << 20) && g_hdr_bytes + bytes <= (256u << 20)) {
+            cbp::BPHeader* d = nullptr;
+            if (cudaMalloc(&d, bytes) != cudaSuccess) {
+                cudaGetLastError();
+                return CBP_ECUDA;
+            }
+            cbp::cbp_bp_header_kernel<<<grid, 128, 0, stream>>>(to_dev(g), t, v0, nv, tiles, d);
+            ++g_launches;
+            // shared across streams: finish building before publishing
+            if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(stream) != cudaSuccess) {
+                cudaFree(d);
+                return CBP_ECUDA;
+            }
+            g_hdrs.emplace(key, d);
+            g_hdr_bytes += bytes;
+            *out = d;
+            return CBP_OK;
+        }
+    }
+    if (scratch_alloc((void**)owned, bytes, stream) != CBP_OK) return CBP_ECUDA;
+    cbp::cbp_bp_header_kernel<<<grid, 128, 0, stream>>>(to_dev(g), t, v0, nv, tiles, *owned);
+    ++g_launches;
+    *out = *owned;
+    return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+}
+
 template <int S>
 int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
                 int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream,
@@ -494,14 +565,12 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
         return CBP_ECUDA;
     }
     const int tiles = (g.n + cbp::BP_TILE - 1) / cbp::BP_TILE;
-    cbp::BPHeader* hdrs = nullptr;
-    if (scratch_alloc((void**)&hdrs, sizeof(cbp::BPHeader) * tiles * tiles * nv, stream) != CBP_OK) {
+    const cbp::BPHeader* hdrs = nullptr;
+    cbp::BPHeader* hdrs_owned = nullptr;
+    if (get_headers(g, t, v0, nv, stream, &hdrs, &hdrs_owned) != CBP_OK) {
         if (part) cudaFreeAsync(part, stream);
         return CBP_ECUDA;
     }
-    cbp::cbp_bp_header_kernel<<<dim3(tiles * tiles, (nv + 127) / 128), 128, 0, stream>>>(
-        to_dev(g), t, v0, nv, tiles, hdrs);
-    ++g_launches;
     P.hdrs = hdrs;
     P.g = to_dev(g);
     P.t = t;
@@ -526,7 +595,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
 #ifdef CBP_DEBUG_CHECKS
     fprintf(stderr, "bp kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
 #endif
-    cudaFreeAsync(hdrs, stream);
+    if (hdrs_owned) cudaFreeAsync(hdrs_owned, stream);
     if (sym || G > 1) {
         // symmetric: the G x S frame planes are already in output orientation
         const size_t count = sym ? plane : plane * batch;
