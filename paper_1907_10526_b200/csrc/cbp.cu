@@ -243,10 +243,10 @@ int fp_pad_width(const cbp_geometry_t& g)
     return (int)std::floor(2.0 * sigq) + 2;
 }
 
-// FP launch with the line split when the grid is short of ~3 waves (see
-// FPParams::splits); zeroes the output first when it accumulates
+// FP launch: PARTS warps per ray (cbp_fp_kernel) when the plain grid is
+// short of ~6 waves of resident CTAs
 template <int S>
-int launch_fp_kernel(cbp::FPParams& Pm, dim3 grid, size_t out_floats, cudaStream_t stream)
+int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stream)
 {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -255,44 +255,28 @@ int launch_fp_kernel(cbp::FPParams& Pm, dim3 grid, size_t out_floats, cudaStream
     static int per_sm[64];
     std::call_once(once[dev & 63], [dev] {
         int k = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_fp_kernel<S, false>, cbp::FP_BLOCK, 0) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_fp_kernel<S, 1>, cbp::FP_BLOCK, 0) !=
                 cudaSuccess || k < 1)
             k = 1;
         per_sm[dev & 63] = k;
     });
-    static const int force = getenv("CBP_FP_SPLITS") ? atoi(getenv("CBP_FP_SPLITS")) : 0;  // tuning knob
-    const int64_t ctas = (int64_t)grid.x * grid.y * grid.z;
+    static const int force = getenv("CBP_FP_PARTS") ? atoi(getenv("CBP_FP_PARTS")) : 0;  // tuning knob
     const int64_t slots = (int64_t)sms * per_sm[dev & 63];
-    // parts per ray: enough for ~6 waves (measured at config 2: 1 / 2 / 3 / 4 / 6
-    // parts -> 0.239 / 0.218 / 0.211 / 0.209 / 0.212 ms), at most 4
-    int splits = 1;
-    while (splits < 4 && ctas * splits < 6 * slots) ++splits;
-    Pm.splits = force >= 1 ? std::min(force, 16) : splits;
-    Pm.part = nullptr;
-    Pm.counter = nullptr;
-    void* scratch = nullptr;
-    if (Pm.splits > 1) {
-        const size_t items = (size_t)ctas * (cbp::FP_BLOCK / 32);
-        const size_t pbytes = sizeof(double) * items * Pm.splits * S * 32;
-        int rc = scratch_alloc(&scratch, pbytes + sizeof(int) * items, stream);
-        if (rc != CBP_OK) return rc;
-        Pm.part = (double*)scratch;
-        Pm.counter = (int*)((char*)scratch + pbytes);
-        if (cudaMemsetAsync(Pm.counter, 0, sizeof(int) * items, stream) != cudaSuccess) {
-            cudaFreeAsync(scratch, stream);
-            return CBP_ECUDA;
-        }
-        grid.z *= Pm.splits;
-    }
-    (void)out_floats;
-    if (Pm.splits > 1)
-        cbp::cbp_fp_kernel<S, true><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
+    auto ctas = [&](int parts) {
+        return (int64_t)((Pm.g.n_det + cbp::FP_BLOCK / parts - 1) / (cbp::FP_BLOCK / parts)) * views * groups;
+    };
+    int parts = 1;
+    while (parts < 4 && ctas(parts) < 6 * slots) parts *= 2;
+    if (force == 1 || force == 2 || force == 4) parts = force;
+    const dim3 grid((unsigned)(ctas(parts) / ((int64_t)views * groups)), views, groups);
+    if (parts == 4)
+        cbp::cbp_fp_kernel<S, 4><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
+    else if (parts == 2)
+        cbp::cbp_fp_kernel<S, 2><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
     else
-        cbp::cbp_fp_kernel<S, false><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
+        cbp::cbp_fp_kernel<S, 1><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
     ++g_launches;
-    const int rc = cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
-    if (scratch) cudaFreeAsync(scratch, stream);
-    return rc;
+    return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
 }
 
 template <int S>
@@ -324,8 +308,7 @@ int launch_fp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* img,
     Pm.batch = batch;
     Pm.sym_stride = 0;
     Pm.sym_mode = 0;
-    dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, nv, G);
-    rc = launch_fp_kernel<S>(Pm, grid, (size_t)batch * nv * g.n_det, stream);
+    rc = launch_fp_kernel<S>(Pm, nv, G, stream);
     cudaFreeAsync(pad, stream);
     return rc;
 }
@@ -366,8 +349,7 @@ int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     Pm.batch = 4;
     Pm.sym_stride = base_count;
     Pm.sym_mode = 4;
-    dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, base_count, 1);
-    rc = launch_fp_kernel<4>(Pm, grid, (size_t)4 * base_count * g.n_det, stream);
+    rc = launch_fp_kernel<4>(Pm, base_count, 1, stream);
     cudaFreeAsync(pad, stream);
     return rc;
 }
@@ -406,8 +388,7 @@ int launch_fp_sym8(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     Pm.batch = 8;
     Pm.sym_stride = 0;
     Pm.sym_mode = 8;
-    dim3 grid((g.n_det + cbp::FP_BLOCK - 1) / cbp::FP_BLOCK, g.n_views / 8 + 1, 1);
-    rc = launch_fp_kernel<8>(Pm, grid, (size_t)g.n_views * g.n_det, stream);
+    rc = launch_fp_kernel<8>(Pm, g.n_views / 8 + 1, 1, stream);
     cudaFreeAsync(pad, stream);
     return rc;
 }

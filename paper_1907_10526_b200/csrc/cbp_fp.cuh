@@ -46,15 +46,7 @@ struct FPParams {
     // 8: the full dihedral symmetry (S = 8, cbp_pad_sym8_kernel) over base
     // views [0, n_views/8], output the natural [n_views][n_det] sinogram
     int sym_mode;
-    // > 1: each ray's lines are split into `splits` parts walked by different
-    // CTAs (blockIdx.z = group * splits + part).  Every warp stores its FP64
-    // partial totals to `part`, then counts itself in `counter` (one per warp
-    // item, zeroed before the launch); the last arriving part sums all parts in
-    // part order and writes the output once: deterministic.  Used when the grid
-    // would otherwise be short of ~6 waves (the ragged last wave dominated).
-    int splits;
-    double* part;  // [warp item][splits][S][32]
-    int* counter;  // [warp item]
+    // (the line split is the kernel's PARTS template parameter, see cbp_fp_kernel)
 };
 
 constexpr int FP_BLOCK = 128;
@@ -391,17 +383,22 @@ __device__ void fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, in
     }
 }
 
-template <int S, bool SPLIT>
+// PARTS (1, 2, 4) warps of a CTA share the same 32 rays and walk disjoint
+// parts of their lines; the parts' FP64 totals are summed in part order in
+// shared memory (deterministic).  A CTA covers 128 / PARTS bins.  PARTS > 1
+// when the grid would otherwise be short of ~6 waves: the ragged last wave
+// of a 1.6-wave grid cost ~25 %.
+template <int S, int PARTS>
 __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_fp_kernel(const FPParams P)
 {
     const GeomDev& g = P.g;
-    const int jr = blockIdx.x * FP_BLOCK + threadIdx.x;
+    constexpr int BINS = FP_BLOCK / PARTS;  // bins per CTA
+    const int warp = threadIdx.x >> 5, part = warp % PARTS;
+    const int jr = blockIdx.x * BINS + (warp / PARTS) * 32 + (threadIdx.x & 31);
     const bool valid = jr < g.n_det;
     const int j = valid ? jr : g.n_det - 1;
     const int vl = blockIdx.y;
-    const int splits = SPLIT ? P.splits : 1;
-    const int grp = blockIdx.z / splits;  // slices grp S .. grp S + S - 1
-    const int half = SPLIT ? blockIdx.z % splits : 0;
+    const int grp = blockIdx.z;  // slices grp S .. grp S + S - 1
     const int v = P.view_begin + vl;
     const int n = g.n;
 
@@ -470,12 +467,12 @@ __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_f
     for (int q = 0; q < S; ++q)
         acc[q * FP_BLOCK] = Kw > P.P ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;  // pad too thin: NaN
     int i0 = wlo, i1 = whi;
-    if (SPLIT) {  // this CTA's part of the warp's lines: even lengths, because the walk
-                         // takes lines in pairs (an odd range reads one line past its end --
-                         // harmless past whi, not inside the next part)
-        const int L = 2 * ((whi - wlo + 2 * splits) / (2 * splits));
-        i0 = wlo + half * L;
-        i1 = half == splits - 1 ? whi : min(whi, i0 + L - 1);
+    if (PARTS > 1) {  // this warp's part of the lines: even lengths, because the walk takes
+                      // lines in pairs (an odd range reads one line past its end -- harmless
+                      // past whi, not inside the next part)
+        const int L = 2 * ((whi - wlo + 2 * PARTS) / (2 * PARTS));
+        i0 = wlo + part * L;
+        i1 = part == PARTS - 1 ? whi : min(whi, i0 + L - 1);
     }
     if (i0 <= i1 && Kw <= P.P) {
         FPRay R;
@@ -521,25 +518,14 @@ __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_f
 #pragma unroll
         for (int q = 0; q < S; ++q) acc[q * FP_BLOCK] *= h * h / A;  // W = (h^2 / A) num / B
     }
-    if (SPLIT) {  // combine the parts: the last one to arrive sums them in order
-        const int lane = threadIdx.x & 31;
-        const size_t item = (((size_t)grp * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * (FP_BLOCK / 32) +
-                            (threadIdx.x >> 5);
-        double* mine = P.part + (item * splits + half) * (S * 32) + lane;
-#pragma unroll
-        for (int q = 0; q < S; ++q) __stcg(mine + q * 32, acc[q * FP_BLOCK]);
-        __threadfence();
-        __syncwarp();
-        int arrived = 0;
-        if (lane == 0) arrived = atomicAdd(P.counter + item, 1);
-        arrived = __shfl_sync(0xffffffffu, arrived, 0);
-        if (arrived != splits - 1) return;  // another part finishes this item
-        __threadfence();
-        const double* all = P.part + item * splits * (S * 32) + lane;
+    if (PARTS > 1) {  // sum the parts in part order; the first part's warp writes
+        __syncthreads();
+        if (part != 0) return;
 #pragma unroll
         for (int q = 0; q < S; ++q) {
-            double t = 0.0;
-            for (int pp = 0; pp < splits; ++pp) t += __ldcg(all + (pp * S + q) * 32);
+            double t = acc[q * FP_BLOCK];
+#pragma unroll
+            for (int pp = 1; pp < PARTS; ++pp) t += acc[q * FP_BLOCK + pp * 32];
             acc[q * FP_BLOCK] = t;
         }
     }
