@@ -430,18 +430,20 @@ __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_f
     dmax = fmax(dmax, D00 + (n - 1) * dcol);
     dmax = fmax(dmax, D00 + (n - 1) * drow);
     dmax = fmax(dmax, D00 + (n - 1) * (dcol + drow));
-    const double sig_q = 0.5 * (A + C + gj * dmax) / A;  // support half-width in pixels
+    const double inv_bq = 1.0 / b_q, inv_A = fabs(inv_bq);  // one FP64 division for both
+    const double sig_q = 0.5 * (A + C + gj * dmax) * inv_A;  // support half-width in pixels
     int K = (int)floor(2.0 * sig_q) + 1;                // candidates per line
 
     // ray crossing of line i: q*(i) = Q0 + i m; lines whose window meets [0, n)
-    const double Q0 = -X00 / b_q, m = -a_i / b_q;
+    const double Q0 = -X00 * inv_bq, m = -a_i * inv_bq;
     int ilo, ihi;
     if (fabs(m) < 1e-15) {
         const bool hit = Q0 > -sig_q && Q0 < (n - 1) + sig_q;
         ilo = hit ? 0 : n;
         ihi = hit ? n - 1 : -1;
     } else {
-        double a = (-sig_q - Q0) / m, c = ((n - 1) + sig_q - Q0) / m;
+        const double inv_m = 1.0 / m;
+        double a = (-sig_q - Q0) * inv_m, c = ((n - 1) + sig_q - Q0) * inv_m;
         if (a > c) {
             const double tmp = a;
             a = c;
@@ -516,7 +518,7 @@ __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_f
             default: fp_walk_generic<S>(R, Kw, i0, i1, n, P.np, P.P, acc); break;
         }
 #pragma unroll
-        for (int q = 0; q < S; ++q) acc[q * FP_BLOCK] *= h * h / A;  // W = (h^2 / A) num / B
+        for (int q = 0; q < S; ++q) acc[q * FP_BLOCK] *= h * h * inv_A;  // W = (h^2 / A) num / B
     }
     if (PARTS > 1) {  // sum the parts in part order; the first part's warp writes
         __syncthreads();
