@@ -109,3 +109,14 @@ def test_arc_rejected_by_reference_projector_and_validated(torch_cuda):
         cbp.ref_forward(_arc(), torch.zeros((64, 64), device="cuda"))
     with pytest.raises(cbp.CbpError):  # bins beyond 90 degrees
         cbp.forward(_arc(n_det=600), torch.zeros((64, 64), device="cuda"))
+
+
+@pytest.mark.parametrize("kind", [cbp.PARALLEL, cbp.FAN_ARC])
+def test_variant_batch_full_scan(torch_cuda, kind):
+    # a batch over a full scan (n_views % 8 == 0): batched FP, per-image
+    # dihedral BP, for the parallel beam and the arc detector
+    g = _par(n_views=88) if kind == cbp.PARALLEL else _arc(n_views=88)
+    imgs = W.random_image(64, 41, batch=3)
+    _assert_parity(_fp(torch_cuda, g, imgs), O.forward(g, imgs), f"FP batch kind {kind}")
+    y = W.random_sino(88, g["n_det"], 42, batch=3)
+    _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), f"BP batch kind {kind}")
