@@ -90,7 +90,7 @@ typedef struct cbp_geometry {
  * 3-direction box spline M_{[h|sin|, h|cos|, tau]}(s_j - k.e) -- exact
  * (Theorem 1).  On the arc the bin of ray angle gamma subtends
  * tau/sdd at the source, tau'(k) = 2 d tan(tau / (2 sdd)).  The reference
- * projector (cbp_ref_*) takes the flat detector only. */
+ * projector (cbp_ref_*) takes every kind. */
 int cbp_validate(const cbp_geometry_t* g);
 
 /* Forward projection y = A c (Eq. 6) for views [view_begin,

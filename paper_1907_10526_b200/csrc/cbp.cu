@@ -968,7 +968,6 @@ int cbp_ref_forward(const cbp_geometry_t* g, const float* image, double* sino, i
 {
     int rc = check_common(g, image, sino, batch, view_begin, view_count);
     if (rc != CBP_OK) return rc;
-    if (g->kind != CBP_FAN_FLAT) return CBP_EINVAL;
     if (((uintptr_t)sino & 7) || pointer_kind(image) != 1 || pointer_kind(sino) != 1) return CBP_EINVAL;
     cudaStream_t stream = (cudaStream_t)stream_;
     cbp::Tables t;
@@ -991,7 +990,6 @@ int cbp_ref_back(const cbp_geometry_t* g, const double* sino, double* image, int
 {
     int rc = check_common(g, sino, image, batch, view_begin, view_count);
     if (rc != CBP_OK) return rc;
-    if (g->kind != CBP_FAN_FLAT) return CBP_EINVAL;
     if (((uintptr_t)sino & 7) || ((uintptr_t)image & 7) || pointer_kind(image) != 1 || pointer_kind(sino) != 1)
         return CBP_EINVAL;
     cudaStream_t stream = (cudaStream_t)stream_;

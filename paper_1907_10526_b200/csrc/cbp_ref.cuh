@@ -73,14 +73,62 @@ __device__ __forceinline__ double ref_chord(double px, double py, double dx, dou
 }
 
 struct RefView {
-    double ux, uy, ex, ey, px, py, dps, dso;
+    double ux, uy, ex, ey, px, py, dps;
+    int parallel, arc;  // geometry kind (row f3)
 };
 
-// detector coordinate of the ray through x (Eq. 4): D_ps (x - p).e / ((p - x).u)
+__device__ __forceinline__ RefView ref_view(const GeomDev& g, double2 cs)
+{
+    RefView V;
+    V.ux = cs.x;
+    V.uy = cs.y;
+    V.ex = -cs.y;
+    V.ey = cs.x;
+    V.px = g.sid * cs.x;
+    V.py = g.sid * cs.y;
+    V.dps = g.sdd;
+    V.parallel = g.parallel;
+    V.arc = g.arc;
+    return V;
+}
+
+// the ray of detector coordinate s: a point on it, its direction, |direction|
+//   flat: from the source to -D_so u + s e;  arc: from the source at angle
+//   s / D_ps (radius D_ps);  parallel: through s e along -u (sign irrelevant)
+__device__ __forceinline__ void ref_ray(const RefView& V, double s, double& ox, double& oy, double& dx,
+                                        double& dy, double& len)
+{
+    if (V.parallel) {
+        ox = s * V.ex;
+        oy = s * V.ey;
+        dx = V.ux;
+        dy = V.uy;
+        len = 1.0;
+    } else if (V.arc) {
+        double sg, cg;
+        sincos(s / V.dps, &sg, &cg);
+        ox = V.px;
+        oy = V.py;
+        dx = V.dps * (-cg * V.ux + sg * V.ex);
+        dy = V.dps * (-cg * V.uy + sg * V.ey);
+        len = V.dps;
+    } else {
+        ox = V.px;
+        oy = V.py;
+        dx = -V.dps * V.ux + s * V.ex;
+        dy = -V.dps * V.uy + s * V.ey;
+        len = sqrt(V.dps * V.dps + s * s);
+    }
+}
+
+// detector coordinate of the ray through x: Eq. 4 on the flat detector,
+// D_ps x angle on the arc, x.e in parallel beam
 __device__ __forceinline__ double ref_project(const RefView& V, double x, double y)
 {
+    if (V.parallel) return x * V.ex + y * V.ey;
     const double ax = x - V.px, ay = y - V.py;
-    return V.dps * (ax * V.ex + ay * V.ey) / -(ax * V.ux + ay * V.uy);
+    const double lat = ax * V.ex + ay * V.ey, dep = -(ax * V.ux + ay * V.uy);
+    return V.arc ? V.dps * atan2(lat, dep) : V.dps * lat / dep;
 }
 
 // (1/tau) int_a^b chord(s) ds for the pixel box [x0, x1] x [y0, y1]
@@ -108,10 +156,9 @@ __device__ double ref_weight(const RefView& V, double a, double b, double x0, do
             double part = 0.0;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const double s = mid + half * gl8_x(i);
-                // d = q(s) - p = -D_ps u + s e,  |d| = sqrt(D_ps^2 + s^2)
-                const double dx = -V.dps * V.ux + s * V.ex, dy = -V.dps * V.uy + s * V.ey;
-                part += gl8_w(i) * ref_chord(V.px, V.py, dx, dy, sqrt(V.dps * V.dps + s * s), x0, x1, y0, y1);
+                double ox, oy, dx, dy, len;
+                ref_ray(V, mid + half * gl8_x(i), ox, oy, dx, dy, len);
+                part += gl8_w(i) * ref_chord(ox, oy, dx, dy, len, x0, x1, y0, y1);
             }
             sum += part * half;
             lo = hi;
@@ -127,31 +174,26 @@ __global__ void __launch_bounds__(REF_BLOCK) cbp_ref_fp_kernel(const RefParams P
     if (j >= g.n_det) return;
     const int vl = blockIdx.y, b = blockIdx.z;
     const int n = g.n;
-    const double2 cs = P.t.view_cs[P.view_begin + vl];
-    RefView V;
-    V.ux = cs.x;
-    V.uy = cs.y;
-    V.ex = -cs.y;
-    V.ey = cs.x;
-    V.px = g.sid * cs.x;
-    V.py = g.sid * cs.y;
-    V.dps = g.sdd;
-    V.dso = g.sdd - g.sid;
-    const double sj = P.t.bin_d[j].x;
+    const RefView V = ref_view(g, P.t.view_cs[P.view_begin + vl]);
+    const double sj = ((double)j - g.cs) * g.pitch;  // bin centre (arc length on the arc)
     const double a = sj - 0.5 * g.tau, bb = sj + 0.5 * g.tau;
     const double h = g.h, hh = 0.5 * g.h, c0 = g.c0;
     // central ray: walk rows (y const) if it is closer to the y axis
-    const double dcx = -V.dps * V.ux + sj * V.ex, dcy = -V.dps * V.uy + sj * V.ey;
+    double ocx, ocy, dcx, dcy, lc_;
+    ref_ray(V, sj, ocx, ocy, dcx, dcy, lc_);
     const bool rows = fabs(dcy) >= fabs(dcx);
-    // edge rays of the bin
-    const double dax = -V.dps * V.ux + a * V.ex, day = -V.dps * V.uy + a * V.ey;
-    const double dbx = -V.dps * V.ux + bb * V.ex, dby = -V.dps * V.uy + bb * V.ey;
+    // edge rays of the bin (each its own point and direction)
+    double oax, oay, dax, day, oex, oey, dbx, dby, ln;
+    ref_ray(V, a, oax, oay, dax, day, ln);
+    ref_ray(V, bb, oex, oey, dbx, dby, ln);
     // slope of the edge rays along the walk (NaN-free only if the wedge
     // contains no ray parallel to the lines: else every pixel of a line is a candidate)
     const double da = rows ? day : dax, db = rows ? dby : dbx;
     const bool bounded = (da > 0.0 && db > 0.0) || (da < 0.0 && db < 0.0);
     const double ma = rows ? dax / day : day / dax, mb = rows ? dbx / dby : dby / dbx;
-    const double pl = rows ? V.py : V.px, pq = rows ? V.px : V.py;  // source: line coord, along-line coord
+    // each edge ray's point: line coordinate, along-line coordinate
+    const double pla = rows ? oay : oax, pqa = rows ? oax : oay;
+    const double plb = rows ? oey : oex, pqb = rows ? oex : oey;
     const float* img = P.img + (size_t)b * n * n;
     double y = 0.0;
     for (int i = 0; i < n; ++i) {
@@ -159,8 +201,8 @@ __global__ void __launch_bounds__(REF_BLOCK) cbp_ref_fp_kernel(const RefParams P
         const double lc = rows ? (c0 - i) * h : (i - c0) * h;
         int q0 = 0, q1 = n - 1;
         if (bounded) {
-            const double e0 = lc - hh - pl, e1 = lc + hh - pl;
-            const double xa0 = pq + e0 * ma, xa1 = pq + e1 * ma, xb0 = pq + e0 * mb, xb1 = pq + e1 * mb;
+            const double xa0 = pqa + (lc - hh - pla) * ma, xa1 = pqa + (lc + hh - pla) * ma;
+            const double xb0 = pqb + (lc - hh - plb) * mb, xb1 = pqb + (lc + hh - plb) * mb;
             const double lo = fmin(fmin(xa0, xa1), fmin(xb0, xb1)), hi = fmax(fmax(xa0, xa1), fmax(xb0, xb1));
             // along-line pixel index of coordinate x: rows -> col = x/h + c0, columns -> row = c0 - y/h
             double ilo = rows ? lo / h + c0 : c0 - hi / h, ihi = rows ? hi / h + c0 : c0 - lo / h;
@@ -205,16 +247,7 @@ __global__ void __launch_bounds__(REF_BLOCK) cbp_ref_bp_kernel(const RefBackPara
     const double* y = P.sino + (size_t)b * P.view_count * g.n_det;
     double acc = 0.0;
     for (int vl = 0; vl < P.view_count; ++vl) {
-        const double2 cs = P.t.view_cs[P.view_begin + vl];
-        RefView V;
-        V.ux = cs.x;
-        V.uy = cs.y;
-        V.ex = -cs.y;
-        V.ey = cs.x;
-        V.px = g.sid * cs.x;
-        V.py = g.sid * cs.y;
-        V.dps = g.sdd;
-        V.dso = g.sdd - g.sid;
+        const RefView V = ref_view(g, P.t.view_cs[P.view_begin + vl]);
         const double s0 = ref_project(V, kx - hh, ky - hh), s1 = ref_project(V, kx + hh, ky - hh);
         const double s2 = ref_project(V, kx - hh, ky + hh), s3 = ref_project(V, kx + hh, ky + hh);
         const double smin = fmin(fmin(s0, s1), fmin(s2, s3)), smax = fmax(fmax(s0, s1), fmax(s2, s3));
@@ -224,7 +257,7 @@ __global__ void __launch_bounds__(REF_BLOCK) cbp_ref_bp_kernel(const RefBackPara
         for (int j = jlo; j <= jhi; ++j) {
             const double yv = y[(size_t)vl * g.n_det + j];
             if (yv == 0.0) continue;  // exact
-            const double sj = P.t.bin_d[j].x;
+            const double sj = ((double)j - g.cs) * g.pitch;
             acc += yv * ref_weight(V, sj - 0.5 * g.tau, sj + 0.5 * g.tau, kx - hh, kx + hh, ky - hh, ky + hh);
         }
     }

@@ -57,10 +57,25 @@ def test_parallel_is_exact_theorem1(torch_cuda):
     _assert_parity(_fp(torch_cuda, g, img), O.ref_forward(g, img), "FP par vs exact")
 
 
-def test_parallel_rejected_by_reference_projector(torch_cuda):
+def _ref_parity(torch, g, img, what):
+    got = cbp.ref_forward(g, torch.from_numpy(img).cuda()).cpu().numpy()
+    want = O.ref_forward(g, img.astype(np.float64))
+    assert np.abs(got - want).max() / np.abs(want).max() < 1e-9, what
+    y = W.random_sino(g["n_views"], g["n_det"], 9).astype(np.float64)
+    gb = cbp.ref_back(g, torch.from_numpy(y).cuda()).cpu().numpy()
+    wb = O.ref_back(g, y)
+    assert np.abs(gb - wb).max() / np.abs(wb).max() < 1e-9, what
+
+
+def test_parallel_reference_projector(torch_cuda):
+    # the GPU reference pair in parallel geometry against the oracle's, and
+    # Theorem 1 once more: the FP32 CNSF projector equals it to FP32 rounding
     torch = torch_cuda
-    with pytest.raises(cbp.CbpError):
-        cbp.ref_forward(_par(), torch.zeros((64, 64), device="cuda"))
+    g = _par(n=32, n_views=12, n_det=64)
+    img = W.random_image(32, 13)
+    _ref_parity(torch, g, img, "ref parallel")
+    ref = cbp.ref_forward(g, torch.from_numpy(img).cuda()).cpu().numpy()
+    _assert_parity(_fp(torch, g, img), ref, "CNSF parallel vs GPU ref")
 
 
 # ------------------------------------------------------------ arc detector
@@ -103,10 +118,10 @@ def test_arc_config2_scale_sampled(torch_cuda):
     _assert_parity(c[rows, cols], O.back_pixels(g, s, rows, cols), "BP arc cfg2 sampled")
 
 
-def test_arc_rejected_by_reference_projector_and_validated(torch_cuda):
+def test_arc_reference_projector_and_validation(torch_cuda):
     torch = torch_cuda
-    with pytest.raises(cbp.CbpError):
-        cbp.ref_forward(_arc(), torch.zeros((64, 64), device="cuda"))
+    g = _arc(n=32, n_views=12, n_det=80, sid=60.0, sdd=120.0)
+    _ref_parity(torch, g, W.random_image(32, 14), "ref arc")
     with pytest.raises(cbp.CbpError):  # bins beyond 90 degrees
         cbp.forward(_arc(n_det=600), torch.zeros((64, 64), device="cuda"))
 

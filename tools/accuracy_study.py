@@ -88,6 +88,15 @@ def main():
                    "max_rel_to_peak": float(err.max() / np.abs(r).max()),
                    "rel_l2": float(np.linalg.norm(y - r) / np.linalg.norm(r)),
                    "cnsf_seconds": tc, "ref_seconds": tr}
+    # row f3 variants in the Fig. 6 setting: parallel beam (exact by Theorem 1:
+    # only FP32 rounding remains) and the arc detector (D_ps = 400 mm)
+    for name, extra in (("fig6a_parallel", dict(kind=cbp.PARALLEL)),
+                        ("fig6a_arc", dict(kind=cbp.FAN_ARC))):
+        g = dict(W.FIG6, **extra)
+        y, r, _, _ = pair(g, np.ones((1, 1)), views=(0, 90))
+        e, peak = per_angle(y, r)
+        res[name] = {"geometry": g, "angles_deg": list(range(90)), "max_error_mm": e.tolist(),
+                     "worst": float(e.max()), "mean": float(e.mean()), "peak_mm": float(peak.max())}
     with open(out, "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps({k: ({kk: vv for kk, vv in v.items() if kk in ("worst", "mean", "max_error_mm", "max_rel_to_peak", "rel_l2", "ref_seconds")} if isinstance(v, dict) else v) for k, v in res.items()}))
