@@ -219,19 +219,21 @@ def main():
     g = W.geometry(args.config)
     n, ns = g["n"], g["n_det"]
     batch = W.BATCH[args.config]
-    # view shard of this rank: the 4 rotated copies of a block of base views
-    # when the 90-degree symmetry applies (one image, n_views % 4 == 0), else a
-    # contiguous block
-    sh = make_shard(g["n_views"], rank, world, batch)
+    # view shard of this rank: the orbits of a block of base views under the
+    # 8 frames (one image, n_views % 8 == 0: the BP keeps one weight per 8
+    # views on every rank), else the 4 rotated copies of a block of base views
+    # (n_views % 4 == 0), else a contiguous block
+    sh = make_shard(g["n_views"], rank, world, batch, dihedral=True)
     views = sh.views()
     nv = len(views)
     orbit = sh.mode == "orbit"
+    dihedral = sh.mode == "dihedral"
 
     host_img = W.shepp_logan(n) if batch == 1 else W.jittered_batch(n, batch, seed=7)
     img = torch.from_numpy(host_img).to(dev)
     bshape = () if batch == 1 else (batch,)
-    sshape = (4, sh.count, ns) if orbit else bshape + (nv, ns)
-    sino = torch.empty(sshape, dtype=torch.float32, device=dev)
+    sshape = (4, sh.count, ns) if orbit else ((g["n_views"], ns) if dihedral else bshape + (nv, ns))
+    sino = torch.zeros(sshape, dtype=torch.float32, device=dev)
     out = torch.empty(bshape + (n, n), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -239,12 +241,16 @@ def main():
     def fwd(image, y):
         if orbit:
             cbp.forward_orbit(g, image, sh.begin, sh.count, sino=y, stream=stream)
+        elif dihedral:
+            cbp.forward_dihedral(g, image, sh.begin, sh.count, sino=y, stream=stream)
         else:
             cbp.forward(g, image, y, view_begin=sh.begin, view_count=sh.count, stream=stream)
 
     def bwd(y, image):
         if orbit:
             cbp.back_orbit(g, y, sh.begin, image=image, stream=stream)
+        elif dihedral:
+            cbp.back_dihedral(g, y, sh.begin, sh.count, image=image, stream=stream)
         else:
             cbp.back(g, y, image, view_begin=sh.begin, stream=stream)
 
@@ -301,7 +307,7 @@ def main():
     counts = weight_counts(args.config)
     nw = int(sum(counts[v] for v in views)) if counts else None
     # views (symmetry) or slices (batch) per weight evaluation, FP and BP
-    sym = 4 if orbit else cbp.symmetry_fold(g, batch, sh.begin, sh.count)
+    sym = 4 if orbit else (8 if dihedral else cbp.symmetry_fold(g, batch, sh.begin, sh.count))
     fp_mirror = bool(os.environ.get("CBP_FP_MIRROR"))
     slices = 4 if batch >= 4 else (2 if batch >= 2 else 1)
     if batch > 1:  # FP: weights shared by the batch's slices; BP: symmetry per image
@@ -383,7 +389,8 @@ def main():
                "d2h_bytes_per_step": 4 * batch * n * n,
                "path": "cbp_normal (A^T A) on pinned host buffers (library staging; the sinogram "
                        "stays on the device)" if world == 1
-               else "pinned H2D/D2H + cbp_forward_orbit/cbp_back_orbit + NCCL all_reduce"}
+               else f"pinned H2D/D2H + {sh.mode} shards (cbp_forward_{sh.mode}/cbp_back_{sh.mode} or view "
+                    f"ranges) + NCCL all_reduce"}
         if world == 1:  # informational: the sinogram also crosses PCIe both ways
             for _ in range(3):
                 e2e_sino_step()
@@ -412,7 +419,8 @@ def main():
                        "n_det": ns, "pixel_mm": g["pixel"], "det_pitch_mm": g["det_pitch"],
                        "sid_mm": g["sid"], "sdd_mm": g["sdd"], "batch": batch,
                        "parallelism": (f"views/{world}" if world > 1 else "single")
-                       + (" (4-fold rotational symmetry)" if orbit else ""),
+                       + (" (4-fold rotational symmetry)" if orbit else "")
+                       + (" (8-fold dihedral symmetry)" if dihedral else ""),
                        "l2": "flushed between steps (256 MiB write, outside the timed events)"},
             "roofline": roof,
             "kernels": kernels,

@@ -141,6 +141,20 @@ int cbp_forward_orbit(const cbp_geometry_t* g, const float* image, float* sino,
 int cbp_back_orbit(const cbp_geometry_t* g, const float* sino, float* image,
                    int32_t base_begin, int32_t base_count, int32_t accumulate, void* stream);
 
+/* Dihedral shards (n_views % 8 == 0): base views b in [base_begin,
+ * base_begin + base_count) within [0, n_views/8]; the shard's views are
+ * their orbits {view_g(b) : g = R^q M^m} (8 views per base view, 4 for
+ * b = 0 and b = n_views/8), so shards of a partition of [0, n_views/8] cover
+ * every view once and each keeps one weight per 8 views.  sino is the
+ * NATURAL [n_views][n_det] layout: cbp_forward_dihedral writes the shard's
+ * rows only, cbp_back_dihedral reads them only (overwrites image, or adds
+ * to it when accumulate != 0).  Device pointers only, 4-byte aligned;
+ * CBP_EINVAL otherwise. */
+int cbp_forward_dihedral(const cbp_geometry_t* g, const float* image, float* sino,
+                         int32_t base_begin, int32_t base_count, void* stream);
+int cbp_back_dihedral(const cbp_geometry_t* g, const float* sino, float* image,
+                      int32_t base_begin, int32_t base_count, int32_t accumulate, void* stream);
+
 /* ---- Row f1: building blocks of the iterative loops (SART, CGLS) around
  * the projector.  Device pointers, FP32 vectors of `count` elements,
  * stream-ordered; CBP_EINVAL for null pointers or negative counts.

@@ -24,7 +24,8 @@ CBP_OK, CBP_EINVAL, CBP_ECUDA, CBP_ENOMEM = 0, -1, -2, -3
 
 # names declared in include/cbp.h
 ABI_FUNCTIONS = ("cbp_validate", "cbp_forward", "cbp_back", "cbp_normal", "cbp_symmetry_fold",
-                 "cbp_forward_orbit", "cbp_back_orbit", "cbp_sart_residual", "cbp_sart_update",
+                 "cbp_forward_orbit", "cbp_back_orbit", "cbp_forward_dihedral", "cbp_back_dihedral",
+                 "cbp_sart_residual", "cbp_sart_update",
                  "cbp_fill", "cbp_dot", "cbp_cgls_step", "cbp_cgls_direction", "cbp_ref_forward",
                  "cbp_ref_back", "cbp_tv_value", "cbp_tv_gradient", "cbp_diff_norm2", "cbp_tv_step",
                  "cbp_asd_adapt", "cbp_adjoint_check", "cbp_strerror", "cbp_version",
@@ -100,6 +101,10 @@ def lib() -> ctypes.CDLL:
         L.cbp_forward_orbit.argtypes = [G, fp, fp, i32, i32, vp]
         L.cbp_forward_orbit.restype = ctypes.c_int
         L.cbp_back_orbit.argtypes = [G, fp, fp, i32, i32, i32, vp]
+        L.cbp_forward_dihedral.argtypes = [G, fp, fp, i32, i32, vp]
+        L.cbp_forward_dihedral.restype = ctypes.c_int
+        L.cbp_back_dihedral.argtypes = [G, fp, fp, i32, i32, i32, vp]
+        L.cbp_back_dihedral.restype = ctypes.c_int
         L.cbp_back_orbit.restype = ctypes.c_int
         i64 = ctypes.c_int64
         L.cbp_sart_residual.argtypes = [fp, fp, fp, fp, i64, vp]
@@ -373,6 +378,46 @@ def cgls_step(x, p, r, q, num, den):
 
 def cgls_direction(p, s, num, den):
     _call("cbp_cgls_direction", _dev(p), _dev(s), _dev(num), _dev(den), p.numel())
+
+
+def dihedral_views(n_views: int, base_begin: int, base_count: int):
+    """the views of a dihedral shard (sorted): the orbits of its base views"""
+    N = n_views
+    out = set()
+    for v in range(base_begin, base_begin + base_count):
+        for m in (0, 1):
+            for q in range(4):
+                out.add(((N - v if m else v) + q * (N // 4)) % N)
+    return sorted(out)
+
+
+def forward_dihedral(geom, image, base_begin: int, base_count: int, sino=None, stream=None):
+    """This dihedral shard's rows of y = A c in a natural [n_views, n_det]
+    sinogram (zero-filled when allocated here; other rows untouched)."""
+    import torch
+    g = _checked(geom)
+    if sino is None:
+        sino = torch.zeros((g.n_views, g.n_det), dtype=torch.float32, device=image.device)
+    pi, st = _ptr_and_stream(image, stream)
+    ps, _ = _ptr_and_stream(sino, stream)
+    rc = lib().cbp_forward_dihedral(ctypes.byref(g), pi, ps, base_begin, base_count, st)
+    if rc != CBP_OK:
+        raise CbpError(rc, "cbp_forward_dihedral")
+    return sino
+
+
+def back_dihedral(geom, sino, base_begin: int, base_count: int, image=None, accumulate: bool = False,
+                  stream=None):
+    """The partial adjoint over a dihedral shard's views (natural sinogram)."""
+    g = _checked(geom)
+    if image is None:
+        image = _empty_like(sino, (g.n, g.n))
+    ps, st = _ptr_and_stream(sino, stream)
+    pi, _ = _ptr_and_stream(image, stream)
+    rc = lib().cbp_back_dihedral(ctypes.byref(g), ps, pi, base_begin, base_count, 1 if accumulate else 0, st)
+    if rc != CBP_OK:
+        raise CbpError(rc, "cbp_back_dihedral")
+    return image
 
 
 def ref_back(geom, sino, image=None, view_begin: int = 0):

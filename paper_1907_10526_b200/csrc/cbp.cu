@@ -323,8 +323,10 @@ bool use_sym4(const cbp_geometry_t& g, int32_t batch, int32_t v0, int32_t nv)
 
 // sino holds [4][base_count][n_det]: row q base_count + b is view
 // base_begin + b + q n_views / 4
+// stride 0: sino is the orbit layout [4][base_count][n_det]; stride n_views/4:
+// sino is the natural [n_views][n_det] layout (rows base_begin + i + q n_views/4)
 int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
-                   int32_t base_begin, int32_t base_count, cudaStream_t stream)
+                   int32_t base_begin, int32_t base_count, cudaStream_t stream, int32_t stride = 0)
 {
     const int P = fp_pad_width(g);
     const int np = g.n + 2 * P;
@@ -343,11 +345,11 @@ int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     Pm.padT = padT;
     Pm.np = np;
     Pm.P = P;
-    Pm.sino = sino;
+    Pm.sino = stride ? sino + (size_t)base_begin * g.n_det : sino;
     Pm.view_begin = base_begin;
     Pm.view_count = base_count;
     Pm.batch = 4;
-    Pm.sym_stride = base_count;
+    Pm.sym_stride = stride ? stride : base_count;
     Pm.sym_mode = 4;
     rc = launch_fp_kernel<4>(Pm, base_count, 1, stream);
     cudaFreeAsync(pad, stream);
@@ -775,6 +777,46 @@ int cbp_back_orbit(const cbp_geometry_t* g, const float* sino, float* image, int
     cbp::Tables t;
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
     return launch_bp_s<4>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 4);
+}
+
+// ---- dihedral shards (views sharded over GPUs keeping the 8-fold symmetry)
+static int check_dihedral(const cbp_geometry_t* g, const void* a, const void* b, int32_t base_begin,
+                          int32_t base_count)
+{
+    if (cbp_validate(g) != CBP_OK || g->n_views % 8 != 0) return CBP_EINVAL;
+    if (!a || !b || base_count < 1 || base_begin < 0 || (int64_t)base_begin + base_count > g->n_views / 8 + 1)
+        return CBP_EINVAL;
+    if (((uintptr_t)a & 3) || ((uintptr_t)b & 3)) return CBP_EINVAL;
+    if (pointer_kind(a) != 1 || pointer_kind(b) != 1) return CBP_EINVAL;
+    return CBP_OK;
+}
+
+int cbp_forward_dihedral(const cbp_geometry_t* g, const float* image, float* sino, int32_t base_begin,
+                         int32_t base_count, void* stream_)
+{
+    int rc = check_dihedral(g, image, sino, base_begin, base_count);
+    if (rc != CBP_OK) return rc;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    cbp::Tables t;
+    if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    const int N = g->n_views, q = N / 4, e = N / 8;
+    // the 4 rotations of the base block, then those of its mirror images
+    // N/4 - v (v = 0 and v = N/8 are their own mirror orbits)
+    if ((rc = launch_fp_sym4(*g, t, image, sino, base_begin, base_count, stream, q)) != CBP_OK) return rc;
+    const int lo = std::max(base_begin, 1), hi = std::min(base_begin + base_count, e);  // [lo, hi)
+    if (hi > lo) rc = launch_fp_sym4(*g, t, image, sino, q - hi + 1, hi - lo, stream, q);
+    return rc;
+}
+
+int cbp_back_dihedral(const cbp_geometry_t* g, const float* sino, float* image, int32_t base_begin,
+                      int32_t base_count, int32_t accumulate, void* stream_)
+{
+    int rc = check_dihedral(g, sino, image, base_begin, base_count);
+    if (rc != CBP_OK) return rc;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    cbp::Tables t;
+    if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    return launch_bp_s<8>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 8);
 }
 
 // ---- row f1: SART / CGLS building blocks ---------------------------------

@@ -7,13 +7,19 @@ each rank back-projects its views into a partial image and the partials are
 summed with one collective (all_reduce, or reduce to one rank) -- the only
 exchange step of the path.
 
-Two shard shapes (``Shard.mode``):
+Three shard shapes (``Shard.mode``):
 
 * ``"orbit"`` (one image, n_views % 4 == 0): the n_views/4 base views are
   split in contiguous blocks and each rank takes the 4 rotated copies of its
   block, views {b + q n_views/4}; the library's 90-degree rotational symmetry
   then computes each weight once for 4 views (``forward_orbit`` /
   ``back_orbit``, local sinogram [4, nb, n_det]);
+* ``"dihedral"`` (one image, n_views % 8 == 0, requested with
+  ``dihedral=True``): the n_views/8 + 1 base views of the 8-fold symmetry
+  are split in contiguous blocks and each rank takes their orbits under
+  the rotations and the mirror (``forward_dihedral`` / ``back_dihedral``,
+  local sinogram = the natural [n_views, n_det] with this rank's rows),
+  so every rank's BP keeps one weight per 8 views;
 * ``"block"`` (otherwise): a contiguous block of views (local sinogram
   [B?, nv, n_det]).
 
@@ -43,23 +49,29 @@ def view_shard(n_views: int, rank: int, world: int) -> tuple[int, int]:
 
 @dataclass(frozen=True)
 class Shard:
-    mode: str    # "orbit" or "block"
+    mode: str    # "orbit", "dihedral" or "block"
     begin: int   # first base view (orbit) or first view (block)
     count: int   # base views (orbit) or views (block)
     n_views: int
 
     def views(self) -> np.ndarray:
-        """global view index of each local sinogram row"""
+        """global view index of each local sinogram row (dihedral: the rows of
+        the natural sinogram this shard owns, sorted)"""
         if self.mode == "block":
             return np.arange(self.begin, self.begin + self.count)
+        if self.mode == "dihedral":
+            return np.asarray(_cbp.dihedral_views(self.n_views, self.begin, self.count))
         m = self.n_views // 4
         return np.concatenate([np.arange(self.begin, self.begin + self.count) + q * m
                                for q in range(4)])
 
 
-def make_shard(n_views: int, rank: int, world: int, batch: int = 1) -> Shard:
+def make_shard(n_views: int, rank: int, world: int, batch: int = 1, dihedral: bool = False) -> Shard:
     if world == 1:  # the whole scan: the library picks its widest symmetry itself
         return Shard("block", 0, n_views, n_views)
+    if dihedral and batch == 1 and n_views % 8 == 0 and n_views // 8 + 1 >= world:
+        b0, nb = view_shard(n_views // 8 + 1, rank, world)
+        return Shard("dihedral", b0, nb, n_views)
     if batch == 1 and n_views % 4 == 0 and n_views // 4 >= world:
         b0, nb = view_shard(n_views // 4, rank, world)
         return Shard("orbit", b0, nb, n_views)
@@ -79,21 +91,27 @@ def _n_views(geom):
 
 
 def forward_sharded(geom, image, group=None, forward: Callable = _cbp.forward,
-                    forward_orbit: Callable = _cbp.forward_orbit, stream=None):
+                    forward_orbit: Callable = _cbp.forward_orbit,
+                    forward_dihedral: Callable = _cbp.forward_dihedral, dihedral: bool = False,
+                    stream=None):
     """This rank's part of y = A c: returns (local sinogram, Shard).  No
-    communication.  Row i of the local sinogram is view shard.views()[i]."""
+    communication.  Row i of the local sinogram is view shard.views()[i]
+    (dihedral: the natural sinogram, rows shard.views() filled)."""
     rank, world = _rank_world(group)
     batch = 1 if image.ndim == 2 else image.shape[0]
-    sh = make_shard(_n_views(geom), rank, world, batch)
+    sh = make_shard(_n_views(geom), rank, world, batch, dihedral)
     if sh.count == 0:
         return None, sh
     if sh.mode == "orbit":
         return forward_orbit(geom, image, sh.begin, sh.count, stream=stream), sh
+    if sh.mode == "dihedral":
+        return forward_dihedral(geom, image, sh.begin, sh.count, stream=stream), sh
     return forward(geom, image, view_begin=sh.begin, view_count=sh.count, stream=stream), sh
 
 
 def back_sharded(geom, sino_local, shard: Shard, image=None, group=None, dst: Optional[int] = None,
-                 back: Callable = _cbp.back, back_orbit: Callable = _cbp.back_orbit, stream=None):
+                 back: Callable = _cbp.back, back_orbit: Callable = _cbp.back_orbit,
+                 back_dihedral: Callable = _cbp.back_dihedral, stream=None):
     """c = sum_g A_g^T y_g: back-projects this rank's views, then sums the
     partial images over the group (all_reduce, or reduce to `dst`)."""
     import torch
@@ -102,6 +120,8 @@ def back_sharded(geom, sino_local, shard: Shard, image=None, group=None, dst: Op
     if shard.count > 0:
         if shard.mode == "orbit":
             image = back_orbit(geom, sino_local, shard.begin, image=image, stream=stream)
+        elif shard.mode == "dihedral":
+            image = back_dihedral(geom, sino_local, shard.begin, shard.count, image=image, stream=stream)
         else:
             image = back(geom, sino_local, image, view_begin=shard.begin, stream=stream)
     elif image is not None:
@@ -117,9 +137,9 @@ def back_sharded(geom, sino_local, shard: Shard, image=None, group=None, dst: Op
     return image
 
 
-def normal_sharded(geom, image, group=None, stream=None, **fns):
+def normal_sharded(geom, image, group=None, stream=None, dihedral: bool = False, **fns):
     """A^T A c over the group (one FP+BP pair, the benchmark's step)."""
-    fwd = {k: v for k, v in fns.items() if k in ("forward", "forward_orbit")}
-    bwd = {k: v for k, v in fns.items() if k in ("back", "back_orbit")}
-    y, sh = forward_sharded(geom, image, group=group, stream=stream, **fwd)
+    fwd = {k: v for k, v in fns.items() if k in ("forward", "forward_orbit", "forward_dihedral")}
+    bwd = {k: v for k, v in fns.items() if k in ("back", "back_orbit", "back_dihedral")}
+    y, sh = forward_sharded(geom, image, group=group, stream=stream, dihedral=dihedral, **fwd)
     return back_sharded(geom, y, sh, group=group, stream=stream, **bwd)

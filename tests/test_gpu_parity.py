@@ -379,3 +379,29 @@ def test_batched_bp_uses_per_image_dihedral_symmetry(torch_cuda, batch, n_views)
     lhs = float(np.sum(_fp(torch_cuda, g, imgs).astype(np.float64) * y))
     rhs = float(np.sum(imgs.astype(np.float64) * _bp(torch_cuda, g, y)))
     assert abs(lhs - rhs) / abs(lhs) <= 1e-5
+
+
+@pytest.mark.parametrize("n_views,world", [(88, 2), (88, 3), (720, 8)])
+def test_dihedral_shards_sum_to_full(torch_cuda, n_views, world):
+    """Dihedral shards (one GPU, shards run one after another): each shard's
+    FP rows are the full FP's rows, and the partial BPs sum to the full BP."""
+    from paper_1907_10526_b200 import sharded
+    torch = torch_cuda
+    g = dict(W.geometry("1"), n_views=n_views) if n_views == 88 else W.geometry("2")
+    img = torch.from_numpy(W.random_image(g["n"], 51)).cuda()
+    full_y = cbp.forward(g, img)
+    y_rand = torch.from_numpy(W.random_sino(g["n_views"], g["n_det"], 52)).cuda()
+    full_c = cbp.back(g, y_rand)
+    total = torch.zeros_like(full_c)
+    seen = []
+    for r in range(world):
+        sh = sharded.make_shard(g["n_views"], r, world, dihedral=True)
+        assert sh.mode == "dihedral"
+        rows = torch.as_tensor(sh.views(), device="cuda")
+        y = cbp.forward_dihedral(g, img, sh.begin, sh.count)
+        _assert_parity(y[rows].cpu().numpy(), full_y[rows].cpu().numpy(), f"FP dihedral shard {r}")
+        total += cbp.back_dihedral(g, y_rand, sh.begin, sh.count)
+        seen += sh.views().tolist()
+    assert sorted(seen) == list(range(g["n_views"]))
+    torch.cuda.synchronize()
+    _assert_parity(total.cpu().numpy(), full_c.cpu().numpy(), "BP dihedral shards")

@@ -115,3 +115,81 @@ def test_sharded_forward_back_gloo(n_views):
         np.testing.assert_array_equal(yl, full_y[views])  # FP shards are exact rows
         np.testing.assert_allclose(c, full_c, rtol=1e-12, atol=1e-9)  # all_reduce
     np.testing.assert_allclose(res[0][4], full_c, rtol=1e-12, atol=1e-9)  # reduce to rank 0
+
+
+# ------------------------------------------------------- dihedral shards
+def _d4_orbit(n_views, v):
+    """views of base view v under the 8 frames R^q M^m,
+    written out independently of the package"""
+    N = n_views
+    return {((N - v if m else v) + q * (N // 4)) % N for m in (0, 1) for q in range(4)}
+
+
+@pytest.mark.parametrize("n_views,world", [(720, 8), (720, 3), (88, 2), (16, 3), (8, 2)])
+def test_dihedral_shards_cover_every_view_once(n_views, world):
+    shards = [sharded.make_shard(n_views, r, world, dihedral=True) for r in range(world)]
+    assert {s.mode for s in shards} == {"dihedral"}
+    views = np.concatenate([s.views() for s in shards])
+    assert sorted(views.tolist()) == list(range(n_views))  # a partition of the scan
+    for s in shards:
+        want = set()
+        for v in range(s.begin, s.begin + s.count):
+            want |= _d4_orbit(n_views, v)
+        assert set(s.views().tolist()) == want
+    # batches and non-multiples of 8 fall back to orbit / block shards
+    assert sharded.make_shard(n_views, 0, world, batch=2, dihedral=True).mode == "block"
+    assert sharded.make_shard(92, 0, 2, dihedral=True).mode == "orbit"
+
+
+def _orc_forward_dihedral(geom, image, base_begin, base_count, sino=None, stream=None):
+    N = geom["n_views"]
+    y = np.zeros((N, geom["n_det"]))
+    for v in sorted(set().union(*[_d4_orbit(N, b) for b in range(base_begin, base_begin + base_count)])):
+        y[v] = O.forward(geom, image.numpy(), v, 1, threads=2)[0]
+    return torch.from_numpy(y)
+
+
+def _orc_back_dihedral(geom, sino, base_begin, base_count, image=None, accumulate=False, stream=None):
+    N = geom["n_views"]
+    views = sorted(set().union(*[_d4_orbit(N, b) for b in range(base_begin, base_begin + base_count)]))
+    c = sum(O.back(geom, sino[v:v + 1].numpy(), v, threads=2) for v in views)
+    c = torch.from_numpy(c)
+    if image is None:
+        return c
+    image.copy_(c)
+    return image
+
+
+def _worker_dihedral(rank, world, port, geom, img, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        y, sh = sharded.forward_sharded(geom, torch.from_numpy(img), dihedral=True,
+                                        forward_dihedral=_orc_forward_dihedral)
+        c = sharded.back_sharded(geom, y, sh, back_dihedral=_orc_back_dihedral)
+        q.put((rank, sh.views(), y.numpy()[sh.views()], c.numpy(), sh.mode))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_dihedral_gloo():
+    world, n_views = 2, 16
+    geom = dict(W._fan(16, n_views, 32))
+    img = W.shepp_logan(16).astype(np.float64)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_dihedral, args=(r, world, port, geom, img, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=120) for _ in range(world)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full_y = O.forward(geom, img)
+    full_c = O.back(geom, full_y)
+    assert sorted(np.concatenate([r[1] for r in res]).tolist()) == list(range(n_views))
+    for rank, views, yl, c, mode in res:
+        assert mode == "dihedral"
+        np.testing.assert_array_equal(yl, full_y[views])
+        np.testing.assert_allclose(c, full_c, rtol=1e-12, atol=1e-9)
