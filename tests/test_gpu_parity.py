@@ -95,7 +95,7 @@ def test_adjoint_config1(torch_cuda):
 
 
 # ---------------------------------------------- full sizes (sampled oracle)
-@pytest.mark.parametrize("cfg,stride", [("2", 45), ("3", 180)])
+@pytest.mark.parametrize("cfg,stride", [("2", 45), ("3", 180), ("5", 719)])
 def test_forward_full_size_sampled_views(torch_cuda, cfg, stride):
     g = W.geometry(cfg)
     img = W.shepp_logan(g["n"])
@@ -109,7 +109,7 @@ def test_forward_full_size_sampled_views(torch_cuda, cfg, stride):
                        f"FP cfg{cfg} rand v{v}")
 
 
-@pytest.mark.parametrize("cfg,npix", [("2", 96), ("3", 24)])
+@pytest.mark.parametrize("cfg,npix", [("2", 96), ("3", 24), ("5", 8)])
 def test_back_full_size_sampled_pixels(torch_cuda, cfg, npix):
     g = W.geometry(cfg)
     y = W.random_sino(g["n_views"], g["n_det"], 103)
