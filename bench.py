@@ -209,7 +209,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1907_10526_b200 as cbp
-    from paper_1907_10526_b200.sharded import make_shard
+    from paper_1907_10526_b200.sharded import make_shard, view_shard
 
     assert args.warmup >= 3, "at least 3 warm-up steps"
     torch.cuda.set_device(local)
@@ -223,15 +223,25 @@ def main():
     # 8 frames (one image, n_views % 8 == 0: the BP keeps one weight per 8
     # views on every rank), else the 4 rotated copies of a block of base views
     # (n_views % 4 == 0), else a contiguous block
-    sh = make_shard(g["n_views"], rank, world, batch, dihedral=True)
+    # A batch (config 4) shards SLICES instead: each rank projects its slices
+    # over all views (replicas of the single-GPU path, no communication;
+    # SURVEY 8(e)).
+    slice_shard = batch > 1 and world > 1
+    total_batch = batch
+    s0 = 0
+    if slice_shard:
+        s0, batch = view_shard(total_batch, rank, world)
+        sh = make_shard(g["n_views"], 0, 1)
+    else:
+        sh = make_shard(g["n_views"], rank, world, batch, dihedral=True)
     views = sh.views()
     nv = len(views)
     orbit = sh.mode == "orbit"
     dihedral = sh.mode == "dihedral"
 
-    host_img = W.shepp_logan(n) if batch == 1 else W.jittered_batch(n, batch, seed=7)
-    img = torch.from_numpy(host_img).to(dev)
-    bshape = () if batch == 1 else (batch,)
+    host_img = W.shepp_logan(n) if total_batch == 1 else W.jittered_batch(n, total_batch, seed=7)[s0:s0 + batch]
+    img = torch.from_numpy(np.ascontiguousarray(host_img)).to(dev)
+    bshape = () if total_batch == 1 else (batch,)
     sshape = (4, sh.count, ns) if orbit else ((g["n_views"], ns) if dihedral else bshape + (nv, ns))
     sino = torch.zeros(sshape, dtype=torch.float32, device=dev)
     out = torch.empty(bshape + (n, n), dtype=torch.float32, device=dev)
@@ -263,7 +273,7 @@ def main():
         bwd(sino, out)
         if ev:
             ev[2].record(stream)
-        if world > 1:
+        if world > 1 and not slice_shard:
             dist.all_reduce(out)
         if ev:
             ev[3].record(stream)
@@ -298,7 +308,7 @@ def main():
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     total_ms = float(tot.item())
-    value = args.steps * batch / (total_ms * 1e-3)  # FP+BP pairs (one per slice) per second
+    value = args.steps * total_batch / (total_ms * 1e-3)  # FP+BP pairs (one per slice, all ranks) per second
 
     # ---- roofline of the dominant kernel (ALU / FP32-pipe bound)
     # units = nonzero (view, bin, pixel) weights of this rank's views x slices;
@@ -362,7 +372,8 @@ def main():
                 d_img.copy_(h_img, non_blocking=True)  # H2D image
                 fwd(d_img, sino)
                 bwd(sino, d_out)
-                dist.all_reduce(d_out)
+                if not slice_shard:
+                    dist.all_reduce(d_out)
                 h_out.copy_(d_out)  # D2H image
                 torch.cuda.synchronize()
 
@@ -384,7 +395,7 @@ def main():
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": ke * batch / (float(et.item()) * 1e-3), "unit": "pairs/s",
+        e2e = {"value": ke * total_batch / (float(et.item()) * 1e-3), "unit": "pairs/s",
                "h2d_bytes_per_step": 4 * batch * n * n,
                "d2h_bytes_per_step": 4 * batch * n * n,
                "path": "cbp_normal (A^T A) on pinned host buffers (library staging; the sinogram "
@@ -417,8 +428,9 @@ def main():
             "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config], "n": n, "n_views": g["n_views"],
                        "n_det": ns, "pixel_mm": g["pixel"], "det_pitch_mm": g["det_pitch"],
-                       "sid_mm": g["sid"], "sdd_mm": g["sdd"], "batch": batch,
-                       "parallelism": (f"views/{world}" if world > 1 else "single")
+                       "sid_mm": g["sid"], "sdd_mm": g["sdd"], "batch": total_batch,
+                       "parallelism": (f"slices/{world}" if slice_shard else
+                                       (f"views/{world}" if world > 1 else "single"))
                        + (" (4-fold rotational symmetry)" if orbit else "")
                        + (" (8-fold dihedral symmetry)" if dihedral else ""),
                        "l2": "flushed between steps (256 MiB write, outside the timed events)"},
