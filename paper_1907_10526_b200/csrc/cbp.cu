@@ -243,8 +243,9 @@ int fp_pad_width(const cbp_geometry_t& g)
     return (int)std::floor(2.0 * sigq) + 2;
 }
 
-// FP launch: PARTS warps per ray (cbp_fp_kernel) when the plain grid is
-// short of ~6 waves of resident CTAs
+// FP launch: PARTS warps per ray (cbp_fp_kernel) while the grid is short of
+// ~16 waves of resident CTAs (config 2: 1.6 waves -> parts 4, FP -17 %;
+// config 3: 6.5 waves -> parts 4, -4 %; config 4 / 5: enough waves)
 template <int S>
 int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stream)
 {
@@ -266,7 +267,7 @@ int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stre
         return (int64_t)((Pm.g.n_det + cbp::FP_BLOCK / parts - 1) / (cbp::FP_BLOCK / parts)) * views * groups;
     };
     int parts = 1;
-    while (parts < 4 && ctas(parts) < 6 * slots) parts *= 2;
+    while (parts < 4 && ctas(parts) < 16 * slots) parts *= 2;  // config 3 (6.5 waves): parts 4 -4 %
     if (force == 1 || force == 2 || force == 4) parts = force;
     const dim3 grid((unsigned)(ctas(parts) / ((int64_t)views * groups)), views, groups);
     if (parts == 4)

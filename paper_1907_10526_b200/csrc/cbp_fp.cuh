@@ -386,7 +386,7 @@ __device__ void fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, in
 // PARTS (1, 2, 4) warps of a CTA share the same 32 rays and walk disjoint
 // parts of their lines; the parts' FP64 totals are summed in part order in
 // shared memory (deterministic).  A CTA covers 128 / PARTS bins.  PARTS > 1
-// when the grid would otherwise be short of ~6 waves: the ragged last wave
+// when the grid would otherwise be short of ~16 waves: the ragged last wave
 // of a 1.6-wave grid cost ~25 %.
 template <int S, int PARTS>
 __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_fp_kernel(const FPParams P)
