@@ -38,6 +38,7 @@ WORKLOADS = {
     "2": "config2: 512x512 Shepp-Logan, 720 views, 1024 bins, SID 500 / SDD 1000 mm",
     "3": "config3: 1024x1024 Shepp-Logan, 1440 views, 2048 bins, SID 500 / SDD 1000 mm",
     "4": "config4: batch of 64 512x512 jittered Shepp-Logan slices, 720 views, 1024 bins",
+    "5": "config5: 2048x2048 Shepp-Logan, 2880 views, 4096 bins (one pair of the SART/CGLS loop)",
 }
 
 

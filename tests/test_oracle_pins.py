@@ -460,3 +460,15 @@ def test_support_density_matches_survey():
     g = W.geometry("1")
     cnt = O.count_weights(g)
     assert cnt / (g["n"] ** 2 * g["n_views"]) == pytest.approx(2.7016, abs=2e-4)
+
+
+def test_weight_counts_are_invariant_on_dihedral_orbits():
+    # scripts/gen_weight_counts.py counts only the base views of configs 3 and
+    # 5 and fills the rest from their orbits; pin that the per-view counts are
+    # equal on every orbit (config-1 scanner with 88 views)
+    g = dict(W.geometry("1"), n_views=88)
+    per_view = O.count_weights_per_view(g)
+    N = 88
+    for v in range(N // 8 + 1):
+        orbit = {((N - v if m else v) + q * (N // 4)) % N for m in (0, 1) for q in range(4)}
+        assert len({int(per_view[o]) for o in orbit}) == 1, v
