@@ -46,14 +46,16 @@ class Geometry(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("pixel", ctypes.c_double),
                 ("n_views", ctypes.c_int32), ("n_det", ctypes.c_int32),
                 ("det_pitch", ctypes.c_double), ("det_width", ctypes.c_double),
-                ("sid", ctypes.c_double), ("sdd", ctypes.c_double), ("kind", ctypes.c_int32)]
+                ("sid", ctypes.c_double), ("sdd", ctypes.c_double), ("kind", ctypes.c_int32),
+                ("model", ctypes.c_int32)]
 
     @classmethod
     def from_dict(cls, d: dict) -> "Geometry":
-        # kind: 0 fan beam / flat detector (default), 1 parallel beam
+        # kind: 0 fan beam / flat detector (default), 1 parallel beam, 2 arc detector;
+        # model: 0 the paper's CNSF weight (default), 1 the magnified-footprint variant
         return cls(int(d["n"]), float(d["pixel"]), int(d["n_views"]), int(d["n_det"]),
                    float(d["det_pitch"]), float(d["det_width"]), float(d.get("sid", 0.0)),
-                   float(d.get("sdd", 0.0)), int(d.get("kind", 0)))
+                   float(d.get("sdd", 0.0)), int(d.get("kind", 0)), int(d.get("model", 0)))
 
 
 _D2 = ctypes.c_double * 2

@@ -267,10 +267,55 @@ double orc_footprint(const orc_geometry* g, double theta, double s, const double
  * i.e. the 3-direction box spline M_{[zeta1, zeta2, tau']} at s' = r.(p - k),
  * with tau' from Eq. 13.  Unit-mass blur (averaging over the bin, ledger #3)
  * and the h^2 indicator factor (ledger #4). */
+/* Row f3, the magnified-footprint variant (model 1).  The detector
+ * coordinate of a point x is P(x) (Eq. 4; the arc's angle x D_ps; parallel:
+ * x.e).  Linearising P at the pixel centre k maps the pixel's edge vectors
+ * xi1 = (h, 0), xi2 = (0, h) to detector lengths zeta_i = grad P(k) . xi_i,
+ * so the pixel's projection is a 2-direction box spline in s around P(k);
+ * convolved with the detector cell (width tau, unit mass) it is the
+ * 3-direction box spline M_{|zeta1|, |zeta2|, tau}(s - P(k)).  Its mass is the
+ * pixel's detector-integrated chord length: integral chord ds = integral over
+ * the pixel of (ds / d(angle)) / |x - p| dA (ds / d(angle) = L^2 / D_ps on the
+ * flat detector, D_ps on the arc; 1 in parallel beam), taken at the centre. */
+static double weight_mag_f(const orc_geometry* g, const double u[2], const double e[2],
+                           const double p[2], double s, const double k[2])
+{
+    const double h = g->pixel;
+    double sk, grad[2], scale;
+    if (g->kind == 1) {
+        sk = dot2(k, e);
+        grad[0] = e[0];
+        grad[1] = e[1];
+        scale = 1.0;
+    } else {
+        const double kp[2] = {k[0] - p[0], k[1] - p[1]};
+        const double dep = -dot2(kp, u), lat = dot2(kp, e);  /* depth, lateral offset */
+        const double rk = sqrt(dep * dep + lat * lat);          /* |k - p| */
+        if (g->kind == 2) {
+            sk = g->sdd * atan2(lat, dep);
+            const double f = g->sdd / (dep * dep + lat * lat);
+            grad[0] = f * (dep * e[0] + lat * u[0]);
+            grad[1] = f * (dep * e[1] + lat * u[1]);
+            scale = g->sdd / rk;
+        } else {
+            sk = g->sdd * lat / dep;
+            const double f = g->sdd / (dep * dep);
+            grad[0] = f * (dep * e[0] + lat * u[0]);
+            grad[1] = f * (dep * e[1] + lat * u[1]);
+            scale = (g->sdd * g->sdd + sk * sk) / (g->sdd * rk);
+        }
+    }
+    const double raw[3] = {h * grad[0], h * grad[1], g->det_width};
+    double a[3];
+    const int m = orc_canonicalize(3, raw, ORC_EPS_REL * h, a);
+    return h * h * scale * orc_box_spline(m, a, s - sk);
+}
+
 static double weight_f(const orc_geometry* g, const double u[2], const double e[2],
                        const double p[2], double s, const double v[2], const double r[2],
                        const double k[2])
 {
+    if (g->model == 1) return weight_mag_f(g, u, e, p, s, k);
     const double h = g->pixel;
     /* a point of the ray: the source, or (parallel beam) the detector point s e */
     double q[2];
@@ -300,6 +345,7 @@ static int geometry_ok(const orc_geometry* g)
 {
     if (!g || g->n < 1 || !(g->pixel > 0) || g->n_views < 1 || g->n_det < 1) return 0;
     if (!(g->det_pitch > 0) || !(g->det_width > 0)) return 0;
+    if (g->model != 0 && g->model != 1) return 0;
     if (g->kind == 1) return 1; /* parallel beam: no source */
     if (g->kind != 0 && g->kind != 2) return 0;
     if (g->kind == 2 && !(g->det_width < 3.14159 * g->sdd)) return 0;

@@ -38,6 +38,12 @@ typedef struct orc_geometry {
                                the circle of radius D_ps about the source, s is the arc
                                length (angle s / D_ps from the central ray), det_pitch
                                and det_width are arc lengths                        */
+    int32_t model;      /* 0 = the paper's CNSF weight (Eq. 14, per bin ray, effective
+                               blur in the object plane);
+                           1 = the magnified-footprint variant (row f3, BASELINE.json's
+                               prose): the pixel's box-spline footprint mapped onto the
+                               detector by the perspective map linearised at the pixel
+                               centre, convolved with the detector cell            */
 } orc_geometry;
 
 /* --- geometry steps (Eq. 4, Eq. 11, Eq. 13) ---------------------- */
