@@ -67,6 +67,20 @@ extern "C" {
                             (angle s/sdd from the central ray); det_pitch and det_width are
                             arc lengths; every bin must lie within +-90 degrees            */
 
+/* Weight models (cbp_geometry_t.model) */
+#define CBP_MODEL_CNSF 0  /* the paper's CNSF weight: per bin ray, Eq. 11-14 with the effective
+                             blur tau' of Eq. 13                               */
+#define CBP_MODEL_MAG  1  /* row f3, the magnified-footprint variant: the pixel's box-spline
+                             footprint mapped onto the detector by the perspective map (Eq. 4,
+                             P:144-152) linearised at the pixel centre -- zeta_i = h dP/dx_i(k)
+                             -- convolved with the detector cell: W = h^2 m(k)
+                             M_{|zeta1|,|zeta2|,tau}(s_j - P(k)), m(k) the pixel's
+                             detector-integrated chord length per unit area at its centre
+                             ((D_ps^2 + P^2)/(D_ps |k - p|) flat, D_ps/|k - p| arc, 1 parallel).
+                             One footprint per (view, pixel) shared by its bins; no view
+                             symmetry is used (cbp_symmetry_fold returns 1); the FP64
+                             reference projector is the same for both models.            */
+
 /* Scanner and grid (P:96-106 geometry; P:157-159 image; P:124 and P:416
  * detector).  All lengths in mm.                                            */
 typedef struct cbp_geometry {
@@ -79,11 +93,12 @@ typedef struct cbp_geometry {
     double  sid;        /* D_po, source to rotation centre; n h / sqrt(2) < sid        */
     double  sdd;        /* D_ps, source to detector; sdd >= sid (D_so = sdd - sid)     */
     int32_t kind;       /* CBP_FAN_FLAT (0), CBP_PARALLEL (1) or CBP_FAN_ARC (2)        */
+    int32_t model;      /* weight model: CBP_MODEL_CNSF (0, the paper's) or CBP_MODEL_MAG (1) */
 } cbp_geometry_t;
 
 /* Validate a geometry (no CUDA call).  CBP_EINVAL if n < 1, pixel <= 0,
  * n_views < 1, n_det < 1, det_pitch <= 0, det_width <= 0, any value
- * non-finite, kind unknown, or (fan beam) sid <= 0, sdd < sid,
+ * non-finite, kind or model unknown, or (fan beam) sid <= 0, sdd < sid,
  * det_width >= 2 sdd, or the field of view's circumscribed circle
  * n h / sqrt(2) is not strictly inside the source orbit (every pixel
  * must lie strictly in front of the source).  In parallel beam W is the

@@ -43,10 +43,12 @@ class cbp_geometry_t(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("pixel", ctypes.c_double),
                 ("n_views", ctypes.c_int32), ("n_det", ctypes.c_int32),
                 ("det_pitch", ctypes.c_double), ("det_width", ctypes.c_double),
-                ("sid", ctypes.c_double), ("sdd", ctypes.c_double), ("kind", ctypes.c_int32)]
+                ("sid", ctypes.c_double), ("sdd", ctypes.c_double), ("kind", ctypes.c_int32),
+                ("model", ctypes.c_int32)]
 
 
 FAN_FLAT, PARALLEL, FAN_ARC = 0, 1, 2  # cbp_geometry_t.kind
+MODEL_CNSF, MODEL_MAG = 0, 1  # cbp_geometry_t.model (the paper's weight; magnified footprint, row f3)
 
 
 @dataclass(frozen=True)
@@ -61,6 +63,7 @@ class Geometry:
     sid: float
     sdd: float
     kind: int = FAN_FLAT
+    model: int = MODEL_CNSF
 
     @classmethod
     def from_dict(cls, d: dict) -> "Geometry":
@@ -69,7 +72,7 @@ class Geometry:
     def c_struct(self) -> cbp_geometry_t:
         return cbp_geometry_t(int(self.n), float(self.pixel), int(self.n_views), int(self.n_det),
                               float(self.det_pitch), float(self.det_width), float(self.sid),
-                              float(self.sdd), int(self.kind))
+                              float(self.sdd), int(self.kind), int(self.model))
 
     def as_dict(self) -> dict:
         return asdict(self)

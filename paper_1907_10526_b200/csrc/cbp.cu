@@ -18,6 +18,7 @@
 #include "cbp_bp.cuh"
 #include "cbp_common.cuh"
 #include "cbp_fp.cuh"
+#include "cbp_mag.cuh"
 #include "cbp_ref.cuh"
 #include "cbp_tables.cuh"
 #include "cbp_vec.cuh"
@@ -319,7 +320,7 @@ int launch_fp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* img,
 bool use_sym4(const cbp_geometry_t& g, int32_t batch, int32_t v0, int32_t nv)
 {
     static const bool off = getenv("CBP_NO_SYMMETRY") != nullptr;
-    return !off && batch == 1 && v0 == 0 && nv == g.n_views && g.n_views % 4 == 0;
+    return !off && g.model == CBP_MODEL_CNSF && batch == 1 && v0 == 0 && nv == g.n_views && g.n_views % 4 == 0;
 }
 
 // sino holds [4][base_count][n_det]: row q base_count + b is view
@@ -396,11 +397,52 @@ int launch_fp_sym8(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     return rc;
 }
 
+// Row f3, the magnified-footprint model (cbp_mag.cuh).  sigma_max bounds
+// every pixel's support half-width (A + tau + C) / 2 <= (sqrt(2) h |grad P| + tau) / 2
+// over the field of view's circumscribed disk (radius R): |grad P| = D_ps |k - p| / depth^2
+// <= D_ps (D_po + R) / (D_po - R)^2 on the flat detector, D_ps / |k - p| <= D_ps / (D_po - R)
+// on the arc, 1 in parallel beam.  fp: img -> sino; else sino -> img (BP).
+int launch_mag(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino, int32_t batch,
+               int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream, bool fp)
+{
+    const double R = 0.5 * (double)g.n * g.pixel * std::sqrt(2.0);
+    double gmax = 1.0;
+    if (g.kind == CBP_FAN_FLAT) gmax = g.sdd * (g.sid + R) / ((g.sid - R) * (g.sid - R));
+    if (g.kind == CBP_FAN_ARC) gmax = g.sdd / (g.sid - R);
+    cbp::MagParams P;
+    P.g = to_dev(g);
+    P.view_cs = t.view_cs;
+    P.view_begin = v0;
+    P.view_count = nv;
+    P.batch = batch;
+    P.accumulate = accumulate ? 1 : 0;
+    P.sigma_max = 0.5 * (std::sqrt(2.0) * g.pixel * gmax + g.det_width) * (1.0 + 1e-9);
+    P.image = nullptr;
+    P.sino = nullptr;
+    P.sino_in = nullptr;
+    P.image_out = nullptr;
+    if (fp) {
+        P.image = img;
+        P.sino = sino;
+        const dim3 grid((g.n_det + cbp::MAG_FP_BLOCK - 1) / cbp::MAG_FP_BLOCK, nv, batch);
+        cbp::cbp_mag_fp_kernel<<<grid, cbp::MAG_FP_BLOCK, 0, stream>>>(P);
+    } else {  // BP: img is the output image, sino the input sinogram
+        P.sino_in = sino;
+        P.image_out = const_cast<float*>(img);
+        const int64_t pix = (int64_t)g.n * g.n;
+        const dim3 grid((unsigned)((pix + cbp::MAG_BP_BLOCK - 1) / cbp::MAG_BP_BLOCK), batch);
+        cbp::cbp_mag_bp_kernel<<<grid, cbp::MAG_BP_BLOCK, 0, stream>>>(P);
+    }
+    ++g_launches;
+    return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+}
+
 // slices per thread: the weight of a (view, bin, pixel) is computed once and
 // applied to S images of the batch
 int launch_fp(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
               int32_t batch, int32_t v0, int32_t nv, cudaStream_t stream)
 {
+    if (g.model == CBP_MODEL_MAG) return launch_mag(g, t, img, sino, batch, v0, nv, 0, stream, true);
     // FP: the 8-fold kernel needs 128 registers (8 slices x 2 lines); on
     // sm_100a the 4-fold one is faster, so the FP uses the mirror only when
     // CBP_FP_MIRROR is set
@@ -597,6 +639,8 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
 int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
               int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream)
 {
+    if (g.model == CBP_MODEL_MAG)
+        return launch_mag(g, t, img, const_cast<float*>(sino), batch, v0, nv, accumulate, stream, false);
     if (use_sym8(g, batch, v0, nv))
         return launch_bp_s<8>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8);
     if (batch > 1 && use_sym8(g, 1, v0, nv))  // a batch: the 8 frames of each image
@@ -618,6 +662,7 @@ int cbp_validate(const cbp_geometry_t* g)
     if (g->n < 1 || g->n_views < 1 || g->n_det < 1) return CBP_EINVAL;
     if (!finite_pos(g->pixel) || !finite_pos(g->det_pitch) || !finite_pos(g->det_width))
         return CBP_EINVAL;
+    if (g->model != CBP_MODEL_CNSF && g->model != CBP_MODEL_MAG) return CBP_EINVAL;
     if (g->kind == CBP_PARALLEL) return std::isfinite(g->sid) && std::isfinite(g->sdd) ? CBP_OK : CBP_EINVAL;
     if (g->kind != CBP_FAN_FLAT && g->kind != CBP_FAN_ARC) return CBP_EINVAL;
     if (!finite_pos(g->sid) || !finite_pos(g->sdd)) return CBP_EINVAL;
@@ -766,6 +811,12 @@ int cbp_forward_orbit(const cbp_geometry_t* g, const float* image, float* sino, 
     cudaStream_t stream = (cudaStream_t)stream_;
     cbp::Tables t;
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    if (g->model == CBP_MODEL_MAG) {  // no shared weights: the 4 view blocks one by one
+        for (int q = 0; q < 4 && rc == CBP_OK; ++q)
+            rc = launch_mag(*g, t, image, sino + (size_t)q * base_count * g->n_det, 1,
+                            base_begin + q * (g->n_views / 4), base_count, 0, stream, true);
+        return rc;
+    }
     return launch_fp_sym4(*g, t, image, sino, base_begin, base_count, stream);
 }
 
@@ -777,10 +828,37 @@ int cbp_back_orbit(const cbp_geometry_t* g, const float* sino, float* image, int
     cudaStream_t stream = (cudaStream_t)stream_;
     cbp::Tables t;
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    if (g->model == CBP_MODEL_MAG) {
+        for (int q = 0; q < 4 && rc == CBP_OK; ++q)
+            rc = launch_mag(*g, t, image, const_cast<float*>(sino) + (size_t)q * base_count * g->n_det, 1,
+                            base_begin + q * (g->n_views / 4), base_count, accumulate || q > 0, stream, false);
+        return rc;
+    }
     return launch_bp_s<4>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 4);
 }
 
 // ---- dihedral shards (views sharded over GPUs keeping the 8-fold symmetry)
+// The magnified-footprint model runs the shard's views as contiguous blocks
+// of the natural layout: the 4 rotations of the base block [b0, b0 + nb) and
+// of its mirror images N/4 - b for b in [max(b0, 1), min(b0 + nb, N/8)).
+static int mag_dihedral(const cbp_geometry_t& g, const cbp::Tables& t, const float* image, float* sino,
+                        int32_t b0, int32_t nb, int32_t accumulate, cudaStream_t stream, bool fp)
+{
+    const int N = g.n_views, q = N / 4, e = N / 8;
+    const int lo = std::max(b0, 1), hi = std::min(b0 + nb, e);
+    const int starts[2] = {b0, q - hi + 1}, counts[2] = {nb, hi - lo};
+    int rc = CBP_OK, done = 0;
+    for (int blk = 0; blk < 2; ++blk) {
+        if (counts[blk] < 1) continue;
+        for (int r = 0; r < 4 && rc == CBP_OK; ++r, ++done) {
+            const int v = starts[blk] + r * q;
+            rc = launch_mag(g, t, image, sino + (size_t)v * g.n_det, 1, v, counts[blk],
+                            accumulate || done > 0, stream, fp);
+        }
+    }
+    return rc;
+}
+
 static int check_dihedral(const cbp_geometry_t* g, const void* a, const void* b, int32_t base_begin,
                           int32_t base_count)
 {
@@ -801,6 +879,7 @@ int cbp_forward_dihedral(const cbp_geometry_t* g, const float* image, float* sin
     cbp::Tables t;
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
     const int N = g->n_views, q = N / 4, e = N / 8;
+    if (g->model == CBP_MODEL_MAG) return mag_dihedral(*g, t, image, sino, base_begin, base_count, 0, stream, true);
     // the 4 rotations of the base block, then those of its mirror images
     // N/4 - v (v = 0 and v = N/8 are their own mirror orbits)
     if ((rc = launch_fp_sym4(*g, t, image, sino, base_begin, base_count, stream, q)) != CBP_OK) return rc;
@@ -817,6 +896,8 @@ int cbp_back_dihedral(const cbp_geometry_t* g, const float* sino, float* image, 
     cudaStream_t stream = (cudaStream_t)stream_;
     cbp::Tables t;
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    if (g->model == CBP_MODEL_MAG)
+        return mag_dihedral(*g, t, image, const_cast<float*>(sino), base_begin, base_count, accumulate, stream, false);
     return launch_bp_s<8>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 8);
 }
 
@@ -1051,7 +1132,7 @@ int cbp_ref_back(const cbp_geometry_t* g, const double* sino, double* image, int
     return launched();
 }
 
-int cbp_version(void) { return 120; }
+int cbp_version(void) { return 130; }
 
 uint64_t cbp_launch_count(void) { return g_launches.load(); }
 

@@ -27,16 +27,17 @@ def test_library_exports_every_declared_symbol():
     L = ctypes.CDLL(cbp.LIB_PATH)
     for name in _declared_functions():
         assert hasattr(L, name), name
-    assert cbp.version() == 120
+    assert cbp.version() == 130
     assert cbp.strerror(0) == "ok"
     assert "invalid" in cbp.strerror(-1)
     assert cbp.strerror(12345) == "unknown error"
 
 
 def test_struct_layout_matches_header():
-    # int32, (pad), double, int32, int32, double x4, int32 (pad) -> 64 bytes on LP64
+    # int32, (pad), double, int32, int32, double x4, int32, int32 -> 64 bytes on LP64
     assert ctypes.sizeof(cbp.cbp_geometry_t) == 64
     assert cbp.cbp_geometry_t.kind.offset == 56
+    assert cbp.cbp_geometry_t.model.offset == 60
     assert cbp.cbp_geometry_t.pixel.offset == 8
     assert cbp.cbp_geometry_t.det_pitch.offset == 24
 
@@ -46,6 +47,7 @@ def test_struct_layout_matches_header():
     ("det_pitch", 0.0), ("det_width", 0.0), ("det_width", -0.5), ("sid", 0.0),
     ("sdd", 400.0), ("pixel", float("nan")), ("sid", float("inf")),
     ("sid", 45.0),  # 64 mm FOV: circumscribed radius 45.25 mm must be < sid
+    ("model", 2), ("model", -1), ("kind", 3),
 ])
 def test_validate_rejects(field, value):
     g = W.geometry("1")
