@@ -14,15 +14,19 @@
 // its centre: (D_ps^2 + P^2) / (D_ps |k - p|) on the flat detector, D_ps / |k - p|
 // on the arc, 1 in parallel beam.  Unlike the paper's CNSF weight (per bin
 // ray, effective blur tau' in the object plane, Eq. 13) every (view, pixel)
-// pair has ONE footprint that all its bins share, so the footprint is
-// computed once per (view, pixel) -- FP64, the precision-critical P(k) and
-// s_j - P(k) included -- and the bins evaluate only the nested FP32 form of
-// Eq. 14 at x = s_j - P(k).
+// pair has ONE footprint that all its bins share: it is computed once per
+// (view, pixel) -- P(k) in FP64, since s_j - P(k) cancels -- and the bins
+// evaluate only the nested FP32 form of Eq. 14 at
+// x = s_j - P(k), rounded to FP32 from FP64.
 //
-// FP: one thread per (slice, view, bin) gathers over the image lines the
-// bin's footprint band crosses (no atomics, fixed order); BP: one thread per
-// (slice, pixel) gathers over views and the bins of its footprint.  Both call
-// mag_footprint / mag_weight for a (view, bin, pixel): the same arithmetic.
+// FP: a CTA per (slice, view, 128-bin tile) walks the image lines (rows or
+// columns, whichever the tile's rays cross more steeply); per line it stages
+// the footprints of the pixels the tile's band covers in shared memory (each
+// computed once), and each thread (bin) sums over the index interval of its
+// own band -- no atomics, a fixed order.  BP: one thread per (slice, pixel)
+// gathers over views and the bins of its footprint.  Both use mag_footprint
+// and mag_weight; x differs only by the FP64 rounding of s_j (direct in the
+// FP, incremental in the BP), far below FP32's.
 #pragma once
 
 #include "cbp_common.cuh"
@@ -33,9 +37,15 @@ constexpr int MAG_FP_BLOCK = 128;
 constexpr int MAG_BP_BLOCK = 128;
 
 struct MagFootprint {
-    double P;      // detector coordinate of the pixel centre, P(k) (FP64: s_j - P(k) cancels)
+    double P;  // detector coordinate of the pixel centre, P(k) (FP64: s_j - P(k) cancels)
+    // FP32 shape, with the per-footprint constants of the nested form hoisted:
+    float A;       // max |zeta|
+    float invC;    // 1 / min |zeta| (+inf when eliminated)
+    float w1;      // 1 - B / C
+    float zoff;    // (A - C) / 2 + B / 2: z11 = x + zoff
+    float minAB;   // min(A, B)
+    float hC;      // C / 2
     float sigma;   // support half-width (A + B + C) / 2
-    float A, C;    // max / min |zeta| (C = 0: eliminated)
     float wscale;  // h^2 m(k) / (A B)
 };
 
@@ -84,39 +94,40 @@ __device__ __forceinline__ MagFootprint mag_footprint(const GeomDev& g, double c
         gx = f * __fmaf_rn(depf, -suf, latf * cuf);
         gy = f * __fmaf_rn(depf, cuf, latf * suf);
     }
-    const float h = (float)g.h, tau = (float)g.tau;
+    const float h = (float)g.h, B = (float)g.tau;
     float a1 = fabsf(h * gx), a2 = fabsf(h * gy);
     const float eps = 1e-6f * h;
     if (a1 < eps) a1 = 0.0f;
     if (a2 < eps) a2 = 0.0f;
+    const float A = fmaxf(a1, a2), C = fminf(a1, a2);
     MagFootprint fp;
     fp.P = P;
-    fp.A = fmaxf(a1, a2);
-    fp.C = fminf(a1, a2);
-    fp.sigma = 0.5f * (fp.A + tau + fp.C);
-    fp.wscale = __fdiv_rn(h * h * m, fp.A * tau);
+    fp.A = A;
+    fp.invC = __frcp_rn(C);  // C = 0 -> +inf: sat() eliminates the direction
+    fp.w1 = __fmaf_rn(-B, fp.invC, 1.0f);
+    fp.zoff = 0.5f * (A - C) + 0.5f * B;
+    fp.minAB = fminf(A, B);
+    fp.hC = 0.5f * C;
+    fp.sigma = 0.5f * (A + B + C);
+    fp.wscale = __fdiv_rn(h * h * m, A * B);
     return fp;
 }
 
-// W at detector coordinate s (exactly 0 outside the open support, ledger #15):
-// the scalar form of cnsf_num2 with B = tau
-__device__ __forceinline__ float mag_weight(const MagFootprint& fp, double s, float B)
+// W at x = s - P(k) (exactly 0 outside the open support, ledger #15): the
+// scalar form of cnsf_num2 with B = tau
+__device__ __forceinline__ float mag_weight_x(const MagFootprint& fp, float x, float B)
 {
-    const float x = (float)(s - fp.P);
     if (!(fabsf(x) < fp.sigma)) return 0.0f;
-    const float A = fp.A, C = fp.C;
-    const float invC = __frcp_rn(C);  // C = 0 -> +inf: sat() eliminates the direction
-    const float w1 = __fmaf_rn(-B, invC, 1.0f);
-    const float z11 = x + 0.5f * (A - C) + 0.5f * B;
-    const float z21 = z11 - A;
-    const float t11 = sat_fma(z11, invC, 1.0f), t12 = sat_fma(z11, invC, w1);
-    const float t21 = sat_fma(z21, invC, 1.0f), t22 = sat_fma(z21, invC, w1);
+    const float z11 = x + fp.zoff;
+    const float z21 = z11 - fp.A;
+    const float t11 = sat_fma(z11, fp.invC, 1.0f), t12 = sat_fma(z11, fp.invC, fp.w1);
+    const float t21 = sat_fma(z21, fp.invC, 1.0f), t22 = sat_fma(z21, fp.invC, fp.w1);
     float T = t11 * t11;
     T = __fmaf_rn(-t12, t12, T);
     T = __fmaf_rn(-t21, t21, T);
     T = __fmaf_rn(t22, t22, T);
-    const float trap = fmaxf(fmin3(z11, fminf(A, B), B - z21), 0.0f);
-    return fp.wscale * __fmaf_rn(0.5f * C, T, trap);
+    const float trap = fmaxf(fmin3(z11, fp.minAB, B - z21), 0.0f);
+    return fp.wscale * __fmaf_rn(fp.hC, T, trap);
 }
 
 __device__ __forceinline__ double mag_bin_s(const GeomDev& g, int j) { return ((double)j - g.cs) * g.pitch; }
@@ -177,76 +188,172 @@ __device__ __forceinline__ MagEdge mag_edge(const GeomDev& g, double cu, double 
     return E;
 }
 
-// restrict [lo, hi] (pixel index units along the line) to G0 + G1 i > 0,
-// widened by 1e-3 pixel against rounding (the exact test decides)
-__device__ __forceinline__ void mag_halfline(double G0, double G1, double& lo, double& hi)
+// The band P in (s_lo, s_hi) on line l as index bounds linear in l:
+// G0(l) + G1 i > 0 with G0(l) = G00 + Gl l is i > -(G00 + Gl l) / G1 for
+// G1 > 0 (a lower bound), i < ... for G1 < 0 (an upper one); G1 = 0 (the
+// edge ray parallel to the lines) leaves the line unrestricted (a superset:
+// the exact test decides).  FP32 coefficients, widened by 0.01 pixel plus
+// their rounding.
+struct MagBand {
+    float loA, loB, hiA, hiB;  // lo(l) = loA + loB l, hi(l) = hiA + hiB l
+};
+
+__device__ __forceinline__ void mag_band_edge(double G00, double Gl, double G1, float& loA, float& loB, float& hiA,
+                                              float& hiB, bool& has_lo, bool& has_hi)
 {
-    if (G1 > 0.0)
-        lo = fmax(lo, -G0 / G1 - 1e-3);
-    else if (G1 < 0.0)
-        hi = fmin(hi, -G0 / G1 + 1e-3);
-    else if (!(G0 > -1e-12))
-        hi = -1e30;
+    if (G1 == 0.0) return;
+    const double A = -G00 / G1, Bl = -Gl / G1;
+    if (G1 > 0.0) {
+        if (!has_lo || A > (double)loA) {  // two bounds on one side: either one is a superset
+            loA = (float)A;
+            loB = (float)Bl;
+        }
+        has_lo = true;
+    } else {
+        if (!has_hi || A < (double)hiA) {
+            hiA = (float)A;
+            hiB = (float)Bl;
+        }
+        has_hi = true;
+    }
 }
+
+__device__ __forceinline__ MagBand mag_band(const MagEdge& lo_e, const MagEdge& hi_e, bool rows, int n)
+{
+    // P > s_lo: G_lo > 0;  P < s_hi: -G_hi > 0
+    float loA = -1e30f, loB = 0.0f, hiA = 1e30f, hiB = 0.0f;
+    bool has_lo = false, has_hi = false;
+    if (rows) {
+        mag_band_edge(lo_e.G00, lo_e.Gr, lo_e.Gc, loA, loB, hiA, hiB, has_lo, has_hi);
+        mag_band_edge(-hi_e.G00, -hi_e.Gr, -hi_e.Gc, loA, loB, hiA, hiB, has_lo, has_hi);
+    } else {
+        mag_band_edge(lo_e.G00, lo_e.Gc, lo_e.Gr, loA, loB, hiA, hiB, has_lo, has_hi);
+        mag_band_edge(-hi_e.G00, -hi_e.Gc, -hi_e.Gr, loA, loB, hiA, hiB, has_lo, has_hi);
+    }
+    MagBand B;
+    if (has_lo) {
+        const float w = 0.01f + 1e-6f * (fabsf(loA) + fabsf(loB) * (float)n);
+        B.loA = loA - w;
+        B.loB = loB;
+    } else {
+        B.loA = -1e30f;
+        B.loB = 0.0f;
+    }
+    if (has_hi) {
+        const float w = 0.01f + 1e-6f * (fabsf(hiA) + fabsf(hiB) * (float)n);
+        B.hiA = hiA + w;
+        B.hiB = hiB;
+    } else {
+        B.hiA = 1e30f;
+        B.hiB = 0.0f;
+    }
+    return B;
+}
+
+// index interval [i0, i1] of the band on line l
+__device__ __forceinline__ void mag_band_range(const MagBand& B, int l, int n, int& i0, int& i1)
+{
+    const float lo = fmaxf(fmaf(B.loB, (float)l, B.loA), -1.0f);
+    const float hi = fminf(fmaf(B.hiB, (float)l, B.hiA), (float)n);
+    i0 = max(0, (int)ceilf(lo));
+    i1 = min(n - 1, (int)floorf(hi));
+}
+
+// the staged footprint of one pixel of a line (48 bytes)
+struct MagStaged {
+    double P;
+    float A, invC, w1, zoff, minAB, hC, sigma, wscale, val, pad;
+};
 
 // FP: y[b][v][j] = sum_k c[b][k] W(v, j, k).  The pixels whose footprint can
 // reach bin j have P(k) in (s_j - sigma_max, s_j + sigma_max): on each image
-// line (rows when the bin's ray is within 45 degrees of the y axis, else
-// columns) that is an index interval, from the two affine edge functions of
-// mag_edge; the exact open-support test of mag_weight decides.
+// line that is an index interval, from the two affine edge functions of
+// mag_edge (per thread for its bin, per CTA for the tile's band); the exact
+// open-support test of mag_weight_x decides.
 __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
 {
+    __shared__ MagStaged st[MAG_FP_BLOCK];
     const GeomDev& g = p.g;
-    const int j = blockIdx.x * MAG_FP_BLOCK + threadIdx.x;
+    const int j0 = blockIdx.x * MAG_FP_BLOCK;
+    const int j = j0 + threadIdx.x, jl = min(j0 + MAG_FP_BLOCK, g.n_det) - 1;
     const int vl = blockIdx.y, b = blockIdx.z;
-    if (j >= g.n_det) return;
     const double2 cs = p.view_cs[p.view_begin + vl];
     const double cu = cs.x, su = cs.y;
-    const double s = mag_bin_s(g, j);
+    const double s = mag_bin_s(g, min(j, g.n_det - 1));
     const float B = (float)g.tau;
-    const MagEdge lo_e = mag_edge(g, cu, su, s - p.sigma_max), hi_e = mag_edge(g, cu, su, s + p.sigma_max);
-    // direction of the bin-centre ray
+    // the tile's band, and this bin's
+    // lines: rows when the tile's middle ray is within 45 degrees of the y axis
+    const double sm = 0.5 * (mag_bin_s(g, j0) + mag_bin_s(g, jl));
     double dx, dy;
     if (g.parallel) {
         dx = -cu;
         dy = -su;
     } else if (g.arc) {
         double sg, cg;
-        sincos(s / g.sdd, &sg, &cg);
+        sincos(sm / g.sdd, &sg, &cg);
         dx = -cg * cu - sg * su;
         dy = -cg * su + sg * cu;
     } else {
-        dx = -g.sdd * cu - s * su;
-        dy = -g.sdd * su + s * cu;
+        dx = -g.sdd * cu - sm * su;
+        dy = -g.sdd * su + sm * cu;
     }
     const bool rows = fabs(dy) >= fabs(dx);
     const int n = g.n;
+    const MagBand tband = mag_band(mag_edge(g, cu, su, mag_bin_s(g, j0) - p.sigma_max),
+                                   mag_edge(g, cu, su, mag_bin_s(g, jl) + p.sigma_max), rows, n);
+    const MagBand band = mag_band(mag_edge(g, cu, su, s - p.sigma_max), mag_edge(g, cu, su, s + p.sigma_max), rows, n);
     const float* img = p.image + (size_t)b * n * n;
     float acc = 0.0f;
     for (int l = 0; l < n; ++l) {
-        double lo = -0.5, hi = (double)n - 0.5;
-        // P > s - sigma_max: G_lo > 0;  P < s + sigma_max: -G_hi > 0
-        if (rows) {
-            mag_halfline(lo_e.G00 + lo_e.Gr * l, lo_e.Gc, lo, hi);
-            mag_halfline(-(hi_e.G00 + hi_e.Gr * l), -hi_e.Gc, lo, hi);
-        } else {
-            mag_halfline(lo_e.G00 + lo_e.Gc * l, lo_e.Gr, lo, hi);
-            mag_halfline(-(hi_e.G00 + hi_e.Gc * l), -hi_e.Gr, lo, hi);
-        }
-        if (!(hi >= lo)) continue;
-        const int i0 = max(0, (int)ceil(lo)), i1 = min(n - 1, (int)floor(hi));
-        for (int i = i0; i <= i1; ++i) {
-            const int row = rows ? l : i, col = rows ? i : l;
-            const double kx = ((double)col - g.c0) * g.h, ky = (g.c0 - (double)row) * g.h;
-            const MagFootprint fp = mag_footprint(g, cu, su, kx, ky);
-            const float wgt = mag_weight(fp, s, B);
-            if (wgt != 0.0f) acc = __fmaf_rn(__ldg(img + (size_t)row * n + col), wgt, acc);
+        int I0, I1, i0, i1;
+        mag_band_range(tband, l, n, I0, I1);  // uniform over the CTA
+        if (I1 < I0) continue;
+        mag_band_range(band, l, n, i0, i1);
+        for (int base = I0; base <= I1; base += MAG_FP_BLOCK) {
+            const int i = base + threadIdx.x;
+            if (i <= I1) {
+                const int row = rows ? l : i, col = rows ? i : l;
+                const double kx = ((double)col - g.c0) * g.h, ky = (g.c0 - (double)row) * g.h;
+                const MagFootprint fp = mag_footprint(g, cu, su, kx, ky);
+                MagStaged m;
+                m.P = fp.P;
+                m.A = fp.A;
+                m.invC = fp.invC;
+                m.w1 = fp.w1;
+                m.zoff = fp.zoff;
+                m.minAB = fp.minAB;
+                m.hC = fp.hC;
+                m.sigma = fp.sigma;
+                m.wscale = fp.wscale;
+                m.val = __ldg(img + (size_t)row * n + col);
+                m.pad = 0.0f;
+                st[threadIdx.x] = m;
+            }
+            __syncthreads();
+            const int a = max(i0, base), e = min(i1, min(I1, base + MAG_FP_BLOCK - 1));
+            for (int q = a; q <= e; ++q) {
+                const MagStaged& m = st[q - base];
+                MagFootprint fp;
+                fp.P = m.P;
+                fp.A = m.A;
+                fp.invC = m.invC;
+                fp.w1 = m.w1;
+                fp.zoff = m.zoff;
+                fp.minAB = m.minAB;
+                fp.hC = m.hC;
+                fp.sigma = m.sigma;
+                fp.wscale = m.wscale;
+                const float wgt = mag_weight_x(fp, (float)(s - fp.P), B);
+                acc = __fmaf_rn(m.val, wgt, acc);
+            }
+            __syncthreads();
         }
     }
-    p.sino[((size_t)b * p.view_count + vl) * g.n_det + j] = acc;
+    if (j < g.n_det) p.sino[((size_t)b * p.view_count + vl) * g.n_det + j] = acc;
 }
 
 // BP: c[b][k] = sum_{v, j} y[b][v][j] W(v, j, k) over the bins of k's footprint
+// (|j - P/Delta_s - c_s| < sigma/Delta_s, widened by 1e-3 bin; the exact test decides)
 __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
 {
     const GeomDev& g = p.g;
@@ -263,13 +370,14 @@ __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
     for (int vl = 0; vl < p.view_count; ++vl) {
         const double2 cs = p.view_cs[p.view_begin + vl];
         const MagFootprint fp = mag_footprint(g, cs.x, cs.y, kx, ky);
-        const double jc = fp.P * inv_pitch + g.cs, jw = (double)fp.sigma * inv_pitch;
-        const double jlo = fmax(jc - jw, -2.0), jhi = fmin(jc + jw, (double)g.n_det + 1.0);
-        const int j0 = max(0, (int)ceil(jlo) - 1), j1 = min(g.n_det - 1, (int)floor(jhi) + 1);
+        const double jc = fp.P * inv_pitch + g.cs, jw = (double)fp.sigma * inv_pitch + 1e-3;
+        const double jlo = fmax(jc - jw, -1.0), jhi = fmin(jc + jw, (double)g.n_det);
+        const int ja = max(0, (int)ceil(jlo)), jb = min(g.n_det - 1, (int)floor(jhi));
         const float* yv = y + (size_t)vl * g.n_det;
-        for (int j = j0; j <= j1; ++j) {
-            const float wgt = mag_weight(fp, mag_bin_s(g, j), B);
-            if (wgt != 0.0f) acc = __fmaf_rn(__ldg(yv + j), wgt, acc);
+        double sj = mag_bin_s(g, ja);
+        for (int j = ja; j <= jb; ++j, sj += g.pitch) {
+            const float wgt = mag_weight_x(fp, (float)(sj - fp.P), B);
+            acc = __fmaf_rn(__ldg(yv + j), wgt, acc);
         }
     }
     float* out = p.image_out + (size_t)b * n * n + k;
