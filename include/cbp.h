@@ -128,6 +128,20 @@ int cbp_back(const cbp_geometry_t* g, const float* sino, float* image, int32_t b
  * as cbp_forward. */
 int cbp_normal(const cbp_geometry_t* g, const float* image, float* out, int32_t batch, void* stream);
 
+/* The normal operator over a sequence of `count` inputs, pipelined: input i
+ * is images + i batch n n, its result out + i batch n n (both [count][batch][n][n]).
+ * With HOST buffers (pinned for overlap; pageable memory works but its
+ * copies serialise) the library runs a three-stage pipeline on the device:
+ * the host->device copy of input i+1 and the device->host copy of result
+ * i-1 (two internal streams, double-buffered device images) overlap the
+ * FP+BP pair of input i on `stream`; the call returns when every result is
+ * in host memory.  With DEVICE buffers the pairs run back to back on
+ * `stream` (asynchronous).  The sinogram never leaves the device.  One call
+ * at a time per device (a mutex serialises callers).  CBP_EINVAL as
+ * cbp_normal, count < 1, or one host and one device pointer. */
+int cbp_normal_stream(const cbp_geometry_t* g, const float* images, float* out, int32_t count, int32_t batch,
+                      void* stream);
+
 /* Rotational symmetry.  Rotating the whole scanner by 90
  * degrees maps view v to view v + n_views/4, keeps every detector coordinate
  * and permutes the square pixel grid, so W(v + n_views/4, j, k) = W(v, j, R^-1 k)

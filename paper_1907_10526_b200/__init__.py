@@ -23,7 +23,7 @@ LIB_PATH = os.environ.get("CBP_LIB_PATH") or os.path.join(_HERE, "libcbp.so")
 CBP_OK, CBP_EINVAL, CBP_ECUDA, CBP_ENOMEM = 0, -1, -2, -3
 
 # names declared in include/cbp.h
-ABI_FUNCTIONS = ("cbp_validate", "cbp_forward", "cbp_back", "cbp_normal", "cbp_symmetry_fold",
+ABI_FUNCTIONS = ("cbp_validate", "cbp_forward", "cbp_back", "cbp_normal", "cbp_normal_stream", "cbp_symmetry_fold",
                  "cbp_forward_orbit", "cbp_back_orbit", "cbp_forward_dihedral", "cbp_back_dihedral",
                  "cbp_sart_residual", "cbp_sart_update",
                  "cbp_fill", "cbp_dot", "cbp_cgls_step", "cbp_cgls_direction", "cbp_ref_forward",
@@ -99,6 +99,8 @@ def lib() -> ctypes.CDLL:
         L.cbp_back.restype = ctypes.c_int
         L.cbp_normal.argtypes = [G, fp, fp, i32, vp]
         L.cbp_normal.restype = ctypes.c_int
+        L.cbp_normal_stream.argtypes = [G, fp, fp, i32, i32, vp]
+        L.cbp_normal_stream.restype = ctypes.c_int
         L.cbp_symmetry_fold.argtypes = [G, i32, i32, i32]
         L.cbp_symmetry_fold.restype = ctypes.c_int
         L.cbp_forward_orbit.argtypes = [G, fp, fp, i32, i32, vp]
@@ -236,6 +238,29 @@ def normal(geom, image, out=None, stream=None):
     rc = lib().cbp_normal(ctypes.byref(g), pi, po, batch, st)
     if rc != CBP_OK:
         raise CbpError(rc, "cbp_normal")
+    return out
+
+
+def normal_stream(geom, images, out=None, stream=None):
+    """out[i] = A^T A images[i] for a sequence of inputs (images [count, n, n]
+    or [count, B, n, n]).  Host buffers (numpy / CPU tensors; pin them for
+    overlap) go through the library's copy / compute / copy pipeline and the
+    call returns with every result on the host; CUDA tensors run back to back
+    on the stream."""
+    g = _checked(geom)
+    if images.ndim not in (3, 4) or tuple(images.shape[-2:]) != (g.n, g.n):
+        raise ValueError(f"images shape {tuple(images.shape)}: expected [count, (B,) {g.n}, {g.n}]")
+    count = int(images.shape[0])
+    batch = 1 if images.ndim == 3 else int(images.shape[1])
+    if out is None:
+        out = _empty_like(images, tuple(images.shape))
+    elif tuple(out.shape) != tuple(images.shape):
+        raise ValueError("out must have the images' shape")
+    pi, st = _ptr_and_stream(images, stream)
+    po, _ = _ptr_and_stream(out, stream)
+    rc = lib().cbp_normal_stream(ctypes.byref(g), pi, po, count, batch, st)
+    if rc != CBP_OK:
+        raise CbpError(rc, "cbp_normal_stream")
     return out
 
 

@@ -784,6 +784,119 @@ int cbp_normal(const cbp_geometry_t* g, const float* image, float* out, int32_t 
     return CBP_OK;
 }
 
+// ---- the streamed normal operator: a copy / compute / copy pipeline ------
+// Per device: an H2D and a D2H stream (non-blocking) beside the caller's
+// compute stream, double-buffered device images, one sinogram, and events
+// that order slot reuse: image i+1 crosses PCIe while image i is projected,
+// and image i-1's result returns meanwhile.
+struct Pipe {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t start, done, in_ready[2], in_free[2], out_ready[2], out_free[2];
+    void* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // in0, in1, out0, out1, sino
+    size_t cap[5] = {0, 0, 0, 0, 0};
+};
+std::mutex g_pipe_mu;
+std::map<int, Pipe> g_pipes;
+
+static int pipe_get(int dev, Pipe** out)
+{
+    auto it = g_pipes.find(dev);
+    if (it == g_pipes.end()) {
+        Pipe p;
+        bool ok = cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&p.done, cudaEventDisableTiming) == cudaSuccess;
+        for (int k = 0; k < 2 && ok; ++k)
+            ok = cudaEventCreateWithFlags(&p.in_ready[k], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&p.in_free[k], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&p.out_ready[k], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&p.out_free[k], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) {
+            cudaGetLastError();
+            return CBP_ECUDA;
+        }
+        it = g_pipes.emplace(dev, p).first;
+    }
+    *out = &it->second;
+    return CBP_OK;
+}
+
+static int pipe_buf(Pipe& p, int k, size_t bytes)
+{
+    if (p.cap[k] >= bytes) return CBP_OK;
+    cudaFree(p.buf[k]);
+    p.buf[k] = nullptr;
+    p.cap[k] = 0;
+    if (cudaMalloc(&p.buf[k], bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return CBP_ECUDA;
+    }
+    p.cap[k] = bytes;
+    return CBP_OK;
+}
+
+int cbp_normal_stream(const cbp_geometry_t* g, const float* images, float* out, int32_t count, int32_t batch,
+                      void* stream_)
+{
+    int rc = check_common(g, images, out, batch, 0, g ? g->n_views : 0);
+    if (rc != CBP_OK) return rc;
+    if (count < 1) return CBP_EINVAL;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const int ki = pointer_kind(images), ko = pointer_kind(out);
+    if (ki < 0 || ko < 0 || ki != ko) return CBP_EINVAL;
+    cbp::Tables t;
+    if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
+    const size_t ni = (size_t)batch * g->n * g->n;
+    const size_t ib = sizeof(float) * ni, sb = sizeof(float) * (size_t)batch * g->n_views * g->n_det;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_pipe_mu);
+    Pipe* P = nullptr;
+    if ((rc = pipe_get(dev, &P)) != CBP_OK) return rc;
+    if ((rc = pipe_buf(*P, 4, sb)) != CBP_OK) return rc;
+    float* sino = (float*)P->buf[4];
+    if (ki == 1) {  // device buffers: the pairs back to back on `stream`
+        for (int32_t i = 0; i < count && rc == CBP_OK; ++i) {
+            rc = launch_fp(*g, t, images + i * ni, sino, batch, 0, g->n_views, stream);
+            if (rc == CBP_OK) rc = launch_bp(*g, t, sino, out + i * ni, batch, 0, g->n_views, 0, stream);
+        }
+        return rc;
+    }
+    for (int k = 0; k < 4 && rc == CBP_OK; ++k) rc = pipe_buf(*P, k, ib);
+    if (rc != CBP_OK) return rc;
+    // everything after the work already queued on `stream`
+    if (cudaEventRecord(P->start, stream) != cudaSuccess || cudaStreamWaitEvent(P->h2d, P->start, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(P->d2h, P->start, 0) != cudaSuccess)
+        return CBP_ECUDA;
+    bool ok = true;
+    for (int32_t i = 0; i < count && ok; ++i) {
+        const int k = i & 1;
+        float* din = (float*)P->buf[k];
+        float* dout = (float*)P->buf[2 + k];
+        // H2D of image i once image i-2's FP has read the slot
+        if (i >= 2) ok = ok && cudaStreamWaitEvent(P->h2d, P->in_free[k], 0) == cudaSuccess;
+        ok = ok && cudaMemcpyAsync(din, images + i * ni, ib, cudaMemcpyHostToDevice, P->h2d) == cudaSuccess;
+        ok = ok && cudaEventRecord(P->in_ready[k], P->h2d) == cudaSuccess;
+        // FP + BP on the caller's stream once the image is in and result slot i-2 has left
+        ok = ok && cudaStreamWaitEvent(stream, P->in_ready[k], 0) == cudaSuccess;
+        if (i >= 2) ok = ok && cudaStreamWaitEvent(stream, P->out_free[k], 0) == cudaSuccess;
+        if (!ok) break;
+        if ((rc = launch_fp(*g, t, din, sino, batch, 0, g->n_views, stream)) != CBP_OK) return rc;
+        ok = ok && cudaEventRecord(P->in_free[k], stream) == cudaSuccess;
+        if ((rc = launch_bp(*g, t, sino, dout, batch, 0, g->n_views, 0, stream)) != CBP_OK) return rc;
+        ok = ok && cudaEventRecord(P->out_ready[k], stream) == cudaSuccess;
+        // D2H of result i
+        ok = ok && cudaStreamWaitEvent(P->d2h, P->out_ready[k], 0) == cudaSuccess;
+        ok = ok && cudaMemcpyAsync(out + i * ni, dout, ib, cudaMemcpyDeviceToHost, P->d2h) == cudaSuccess;
+        ok = ok && cudaEventRecord(P->out_free[k], P->d2h) == cudaSuccess;
+    }
+    ok = ok && cudaEventRecord(P->done, P->d2h) == cudaSuccess;
+    ok = ok && cudaStreamWaitEvent(stream, P->done, 0) == cudaSuccess;
+    ok = ok && cudaEventSynchronize(P->done) == cudaSuccess;
+    return ok ? CBP_OK : CBP_ECUDA;
+}
+
 int cbp_symmetry_fold(const cbp_geometry_t* g, int32_t batch, int32_t view_begin,
                       int32_t view_count)
 {
