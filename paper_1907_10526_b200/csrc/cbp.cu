@@ -397,6 +397,16 @@ int launch_fp_sym8(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     return rc;
 }
 
+// the magnified-footprint model over a full scan of one image with N_v % 4 == 0
+// and an even grid: one footprint serves 4 views (the quadrant of pixels x
+// the 4 rotations)
+bool use_mag_sym4(const cbp_geometry_t& g, int32_t batch, int32_t v0, int32_t nv)
+{
+    static const bool off = getenv("CBP_NO_SYMMETRY") != nullptr;
+    return !off && g.model == CBP_MODEL_MAG && batch == 1 && v0 == 0 && nv == g.n_views && g.n_views % 4 == 0 &&
+           g.n % 2 == 0;
+}
+
 // Row f3, the magnified-footprint model (cbp_mag.cuh).  sigma_max bounds
 // every pixel's support half-width (A + tau + C) / 2 <= (sqrt(2) h |grad P| + tau) / 2
 // over the field of view's circumscribed disk (radius R): |grad P| = D_ps |k - p| / depth^2
@@ -417,6 +427,7 @@ int launch_mag(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, 
     P.batch = batch;
     P.accumulate = accumulate ? 1 : 0;
     P.sigma_max = 0.5 * (std::sqrt(2.0) * g.pixel * gmax + g.det_width) * (1.0 + 1e-9);
+    const bool sym4 = use_mag_sym4(g, batch, v0, nv);
     P.image = nullptr;
     P.sino = nullptr;
     P.sino_in = nullptr;
@@ -424,14 +435,25 @@ int launch_mag(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, 
     if (fp) {
         P.image = img;
         P.sino = sino;
-        const dim3 grid((g.n_det + cbp::MAG_FP_BLOCK - 1) / cbp::MAG_FP_BLOCK, nv, batch);
-        cbp::cbp_mag_fp_kernel<<<grid, cbp::MAG_FP_BLOCK, 0, stream>>>(P);
+        const int bins = (g.n_det + cbp::MAG_FP_BLOCK - 1) / cbp::MAG_FP_BLOCK;
+        if (sym4) {
+            P.view_count = g.n_views / 4;
+            cbp::cbp_mag_fp_kernel<4><<<dim3(bins, g.n_views / 4, 1), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
+        } else {
+            cbp::cbp_mag_fp_kernel<1><<<dim3(bins, nv, batch), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
+        }
     } else {  // BP: img is the output image, sino the input sinogram
         P.sino_in = sino;
         P.image_out = const_cast<float*>(img);
-        const int64_t pix = (int64_t)g.n * g.n;
-        const dim3 grid((unsigned)((pix + cbp::MAG_BP_BLOCK - 1) / cbp::MAG_BP_BLOCK), batch);
-        cbp::cbp_mag_bp_kernel<<<grid, cbp::MAG_BP_BLOCK, 0, stream>>>(P);
+        if (sym4) {  // all views, a quadrant of pixels
+            const int64_t pix = (int64_t)(g.n / 2) * (g.n / 2);
+            const unsigned blocks = (unsigned)((pix + cbp::MAG_BP_BLOCK - 1) / cbp::MAG_BP_BLOCK);
+            cbp::cbp_mag_bp_kernel<4><<<dim3(blocks, 1), cbp::MAG_BP_BLOCK, 0, stream>>>(P);
+        } else {
+            const int64_t pix = (int64_t)g.n * g.n;
+            const unsigned blocks = (unsigned)((pix + cbp::MAG_BP_BLOCK - 1) / cbp::MAG_BP_BLOCK);
+            cbp::cbp_mag_bp_kernel<1><<<dim3(blocks, batch), cbp::MAG_BP_BLOCK, 0, stream>>>(P);
+        }
     }
     ++g_launches;
     return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
@@ -901,6 +923,7 @@ int cbp_symmetry_fold(const cbp_geometry_t* g, int32_t batch, int32_t view_begin
                       int32_t view_count)
 {
     if (cbp_validate(g) != CBP_OK) return CBP_EINVAL;
+    if (use_mag_sym4(*g, batch, view_begin, view_count)) return 4;
     if (use_sym8(*g, 1, view_begin, view_count)) return 8;  // the BP of any batch (per image)
     return use_sym4(*g, batch, view_begin, view_count) ? 4 : 1;
 }

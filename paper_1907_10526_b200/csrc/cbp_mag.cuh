@@ -259,20 +259,38 @@ __device__ __forceinline__ void mag_band_range(const MagBand& B, int l, int n, i
     i1 = min(n - 1, (int)floorf(hi));
 }
 
-// the staged footprint of one pixel of a line (48 bytes)
+// the staged footprint of one pixel of a line, with its F image values
+// (F = 4: the pixel's values in the 4 rotated frames)
+template <int F>
 struct MagStaged {
     double P;
-    float A, invC, w1, zoff, minAB, hC, sigma, wscale, val, pad;
+    float A, invC, w1, zoff, minAB, hC, sigma, wscale;
+    float val[F];
 };
+
+// pixel R^q (row, col) of the n x n grid, R(r, c) = (n-1-c, r) (+90 degrees,
+// DESIGN.md 5.6): W(v + q N_v/4, j, R^q k) = W(v, j, k)
+__device__ __forceinline__ void mag_rot(int n, int q, int& r, int& c)
+{
+    for (int t = 0; t < q; ++t) {
+        const int nr = n - 1 - c;
+        c = r;
+        r = nr;
+    }
+}
 
 // FP: y[b][v][j] = sum_k c[b][k] W(v, j, k).  The pixels whose footprint can
 // reach bin j have P(k) in (s_j - sigma_max, s_j + sigma_max): on each image
 // line that is an index interval, from the two affine edge functions of
 // mag_edge (per thread for its bin, per CTA for the tile's band); the exact
 // open-support test of mag_weight_x decides.
+// F = 4 (one image, a full scan, N_v % 4 == 0): blockIdx.y is a base view
+// v < N_v/4 and each weight serves the 4 views v + q N_v/4, reading the image
+// at R^q k and writing the natural sinogram rows.
+template <int F>
 __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
 {
-    __shared__ MagStaged st[MAG_FP_BLOCK];
+    __shared__ MagStaged<F> st[MAG_FP_BLOCK];
     const GeomDev& g = p.g;
     const int j0 = blockIdx.x * MAG_FP_BLOCK;
     const int j = j0 + threadIdx.x, jl = min(j0 + MAG_FP_BLOCK, g.n_det) - 1;
@@ -281,7 +299,6 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
     const double cu = cs.x, su = cs.y;
     const double s = mag_bin_s(g, min(j, g.n_det - 1));
     const float B = (float)g.tau;
-    // the tile's band, and this bin's
     // lines: rows when the tile's middle ray is within 45 degrees of the y axis
     const double sm = 0.5 * (mag_bin_s(g, j0) + mag_bin_s(g, jl));
     double dx, dy;
@@ -299,14 +316,17 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
     }
     const bool rows = fabs(dy) >= fabs(dx);
     const int n = g.n;
+    // the tile's band (uniform over the CTA), and this bin's
     const MagBand tband = mag_band(mag_edge(g, cu, su, mag_bin_s(g, j0) - p.sigma_max),
                                    mag_edge(g, cu, su, mag_bin_s(g, jl) + p.sigma_max), rows, n);
     const MagBand band = mag_band(mag_edge(g, cu, su, s - p.sigma_max), mag_edge(g, cu, su, s + p.sigma_max), rows, n);
     const float* img = p.image + (size_t)b * n * n;
-    float acc = 0.0f;
+    float acc[F];
+#pragma unroll
+    for (int q = 0; q < F; ++q) acc[q] = 0.0f;
     for (int l = 0; l < n; ++l) {
         int I0, I1, i0, i1;
-        mag_band_range(tband, l, n, I0, I1);  // uniform over the CTA
+        mag_band_range(tband, l, n, I0, I1);
         if (I1 < I0) continue;
         mag_band_range(band, l, n, i0, i1);
         for (int base = I0; base <= I1; base += MAG_FP_BLOCK) {
@@ -315,7 +335,7 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
                 const int row = rows ? l : i, col = rows ? i : l;
                 const double kx = ((double)col - g.c0) * g.h, ky = (g.c0 - (double)row) * g.h;
                 const MagFootprint fp = mag_footprint(g, cu, su, kx, ky);
-                MagStaged m;
+                MagStaged<F> m;
                 m.P = fp.P;
                 m.A = fp.A;
                 m.invC = fp.invC;
@@ -325,14 +345,18 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
                 m.hC = fp.hC;
                 m.sigma = fp.sigma;
                 m.wscale = fp.wscale;
-                m.val = __ldg(img + (size_t)row * n + col);
-                m.pad = 0.0f;
+#pragma unroll
+                for (int q = 0; q < F; ++q) {
+                    int r = row, c = col;
+                    mag_rot(n, q, r, c);
+                    m.val[q] = __ldg(img + (size_t)r * n + c);
+                }
                 st[threadIdx.x] = m;
             }
             __syncthreads();
             const int a = max(i0, base), e = min(i1, min(I1, base + MAG_FP_BLOCK - 1));
             for (int q = a; q <= e; ++q) {
-                const MagStaged& m = st[q - base];
+                const MagStaged<F>& m = st[q - base];
                 MagFootprint fp;
                 fp.P = m.P;
                 fp.A = m.A;
@@ -344,44 +368,74 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
                 fp.sigma = m.sigma;
                 fp.wscale = m.wscale;
                 const float wgt = mag_weight_x(fp, (float)(s - fp.P), B);
-                acc = __fmaf_rn(m.val, wgt, acc);
+#pragma unroll
+                for (int f = 0; f < F; ++f) acc[f] = __fmaf_rn(m.val[f], wgt, acc[f]);
             }
             __syncthreads();
         }
     }
-    if (j < g.n_det) p.sino[((size_t)b * p.view_count + vl) * g.n_det + j] = acc;
+    if (j < g.n_det) {
+        if (F == 1) {
+            p.sino[((size_t)b * p.view_count + vl) * g.n_det + j] = acc[0];
+        } else {
+#pragma unroll
+            for (int q = 0; q < F; ++q)
+                p.sino[((size_t)(p.view_begin + vl) + (size_t)q * (g.n_views / 4)) * g.n_det + j] = acc[q];
+        }
+    }
 }
 
 // BP: c[b][k] = sum_{v, j} y[b][v][j] W(v, j, k) over the bins of k's footprint
-// (|j - P/Delta_s - c_s| < sigma/Delta_s, widened by 1e-3 bin; the exact test decides)
+// (|j - P/Delta_s - c_s| < sigma/Delta_s, widened by 1e-3 bin; the exact test decides).
+// F = 4 (one image, a full scan, N_v % 4 == 0, n even): a thread per pixel k
+// of the quadrant rows < n/2, cols < n/2 (whose 4 rotations tile the grid)
+// accumulates the 4 pixels R^q k over all views v, each weight serving
+// (v + q N_v/4 mod N_v, R^q k): one footprint per 4 (view, pixel) pairs.
+template <int F>
 __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
 {
     const GeomDev& g = p.g;
     const int n = g.n;
+    const int nq = F == 1 ? n : n / 2;  // side of the pixel domain the threads cover
     const int k = blockIdx.x * MAG_BP_BLOCK + threadIdx.x;
     const int b = blockIdx.y;
-    if (k >= n * n) return;
-    const int row = k / n, col = k - row * n;
+    if (k >= nq * nq) return;
+    const int row = k / nq, col = k - row * nq;
     const double kx = ((double)col - g.c0) * g.h, ky = (g.c0 - (double)row) * g.h;
     const float B = (float)g.tau;
     const double inv_pitch = 1.0 / g.pitch;
+    const int vq = g.n_views / 4;  // F = 4: frame q reads sinogram row v + q vq (mod N_v)
     const float* y = p.sino_in + (size_t)b * p.view_count * g.n_det;
-    float acc = 0.0f;
+    float acc[F];
+#pragma unroll
+    for (int q = 0; q < F; ++q) acc[q] = 0.0f;
     for (int vl = 0; vl < p.view_count; ++vl) {
         const double2 cs = p.view_cs[p.view_begin + vl];
         const MagFootprint fp = mag_footprint(g, cs.x, cs.y, kx, ky);
         const double jc = fp.P * inv_pitch + g.cs, jw = (double)fp.sigma * inv_pitch + 1e-3;
         const double jlo = fmax(jc - jw, -1.0), jhi = fmin(jc + jw, (double)g.n_det);
         const int ja = max(0, (int)ceil(jlo)), jb = min(g.n_det - 1, (int)floor(jhi));
-        const float* yv = y + (size_t)vl * g.n_det;
+        const float* yq[F];
+#pragma unroll
+        for (int q = 0; q < F; ++q) {
+            int v = vl + q * vq;
+            if (v >= g.n_views) v -= g.n_views;
+            yq[q] = y + (size_t)(F == 1 ? vl : v) * g.n_det;
+        }
         double sj = mag_bin_s(g, ja);
         for (int j = ja; j <= jb; ++j, sj += g.pitch) {
             const float wgt = mag_weight_x(fp, (float)(sj - fp.P), B);
-            acc = __fmaf_rn(__ldg(yv + j), wgt, acc);
+#pragma unroll
+            for (int q = 0; q < F; ++q) acc[q] = __fmaf_rn(__ldg(yq[q] + j), wgt, acc[q]);
         }
     }
-    float* out = p.image_out + (size_t)b * n * n + k;
-    *out = p.accumulate ? *out + acc : acc;
+#pragma unroll
+    for (int q = 0; q < F; ++q) {
+        int r = row, c = col;
+        mag_rot(n, q, r, c);
+        float* out = p.image_out + (size_t)b * n * n + (size_t)r * n + c;
+        *out = p.accumulate ? *out + acc[q] : acc[q];
+    }
 }
 
 }  // namespace cbp

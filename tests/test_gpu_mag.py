@@ -28,10 +28,11 @@ def _mag(kind=cbp.FAN_FLAT, **kw):
 
 
 @pytest.mark.parametrize("kind", [cbp.FAN_FLAT, cbp.FAN_ARC, cbp.PARALLEL])
-@pytest.mark.parametrize("n_views", [90, 88])  # 88: a full scan the CNSF model would fold
+@pytest.mark.parametrize("n_views", [90, 88])  # 88: the 4-fold rotational path
 def test_mag_forward_back(torch_cuda, kind, n_views):
     g = _mag(kind, n_views=n_views)
-    assert cbp.symmetry_fold(g) == 1
+    # a full scan with n_views % 4 == 0 on an even grid: one footprint per 4 views
+    assert cbp.symmetry_fold(g) == (4 if n_views % 4 == 0 else 1)
     for img in (W.shepp_logan(64), W.random_image(64, 5)):
         _assert_parity(_fp(torch_cuda, g, img), O.forward(g, img), f"FP mag kind {kind} {n_views}")
     y = W.random_sino(n_views, g["n_det"], 6)
@@ -125,3 +126,17 @@ def test_mag_orbit_and_dihedral_shards(torch_cuda):
         assert sorted(seen) == list(range(88))
         torch.cuda.synchronize()
         _assert_parity(total.cpu().numpy(), full_c.cpu().numpy(), f"BP mag shards dihedral={dihedral}")
+
+
+def test_mag_symmetric_equals_plain(torch_cuda):
+    # the 4-fold path against the same projector run view by view (no symmetry)
+    torch = torch_cuda
+    g = _mag(cbp.FAN_ARC, n=48, n_views=40, n_det=120)
+    img = torch.from_numpy(W.random_image(48, 21)).cuda()
+    y_sym = cbp.forward(g, img)
+    y_plain = torch.cat([cbp.forward(g, img, view_begin=v, view_count=1) for v in range(40)])
+    _assert_parity(y_sym.cpu().numpy(), y_plain.cpu().numpy(), "mag FP sym vs plain")
+    s = torch.from_numpy(W.random_sino(40, 120, 22)).cuda()
+    c_sym = cbp.back(g, s)
+    c_plain = sum(cbp.back(g, s[v:v + 1].contiguous(), view_begin=v) for v in range(40))
+    _assert_parity(c_sym.cpu().numpy(), c_plain.cpu().numpy(), "mag BP sym vs plain")
