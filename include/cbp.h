@@ -115,9 +115,26 @@ int cbp_validate(const cbp_geometry_t* g);
 int cbp_forward(const cbp_geometry_t* g, const float* image, float* sino, int32_t batch,
                 int32_t view_begin, int32_t view_count, void* stream);
 
+/* Accumulate modes of the back-projections (the `accumulate` argument) */
+#define CBP_ACC_OVERWRITE 0  /* image = A^T y                                               */
+#define CBP_ACC_ADD       1  /* image += A^T y                                              */
+#define CBP_ACC_MULTIMEM  2  /* row a7 fused into the BP: `image` is a MULTICAST address (an
+                                NVLink/NVSwitch multicast object, e.g. torch symmetric memory's
+                                multicast_ptr, bound to one n x n buffer per rank); the BP's last
+                                kernel adds this rank's partial A_g^T y_g to EVERY rank's copy with
+                                multimem.red.add.f32 (the switch performs the sum), so after all
+                                ranks' calls complete and a barrier, each copy holds sum_g A_g^T y_g
+                                -- the view-sharded all-reduce with no separate collective.  The
+                                caller zeroes the copies and fences (barrier) before the first
+                                rank's call.  Device sinogram only; the image pointer is not
+                                checked (a multicast address is not an ordinary allocation);
+                                the order of the cross-rank sum is the switch's (not bitwise
+                                deterministic).                                            */
+
 /* Back-projection c = A^T y over views [view_begin, view_begin + view_count)
  * (the partial adjoint when the range is a shard of the views).  Overwrites
- * image, or adds to it when accumulate != 0.  Errors as cbp_forward. */
+ * image, adds to it (CBP_ACC_ADD) or adds through a multicast address
+ * (CBP_ACC_MULTIMEM).  Errors as cbp_forward, or accumulate outside 0..2. */
 int cbp_back(const cbp_geometry_t* g, const float* sino, float* image, int32_t batch,
              int32_t view_begin, int32_t view_count, int32_t accumulate, void* stream);
 

@@ -320,6 +320,34 @@ def back(geom, sino, image=None, view_begin: int = 0, accumulate: bool = False, 
     return image
 
 
+ACC_OVERWRITE, ACC_ADD, ACC_MULTIMEM = 0, 1, 2  # the back-projections' accumulate modes
+
+
+def back_multimem(geom, sino, mc_ptr: int, view_begin: int = 0, shard=None, stream=None):
+    """Row a7 fused into the BP (CBP_ACC_MULTIMEM, include/cbp.h): add this
+    rank's partial A_g^T y_g to every rank's copy of the image through the
+    multicast address `mc_ptr` (an int: e.g. torch symmetric memory's
+    multicast_ptr).  `sino` is a CUDA tensor: [V, n_det] for the views
+    view_begin.. (shard None), or the sinogram of a sharded.Shard ("orbit":
+    [4, base_count, n_det]; "dihedral": the natural [n_views, n_det]).  The
+    caller zeroes every copy and fences before, and fences after."""
+    g = _checked(geom)
+    ps, st = _ptr_and_stream(sino, stream)
+    mc = ctypes.c_void_p(int(mc_ptr))
+    if shard is None or shard.mode == "block":
+        v0 = view_begin if shard is None else shard.begin
+        rc = lib().cbp_back(ctypes.byref(g), ps, mc, 1, v0, sino.shape[-2], ACC_MULTIMEM, st)
+        name = "cbp_back"
+    elif shard.mode == "orbit":
+        rc = lib().cbp_back_orbit(ctypes.byref(g), ps, mc, shard.begin, shard.count, ACC_MULTIMEM, st)
+        name = "cbp_back_orbit"
+    else:
+        rc = lib().cbp_back_dihedral(ctypes.byref(g), ps, mc, shard.begin, shard.count, ACC_MULTIMEM, st)
+        name = "cbp_back_dihedral"
+    if rc != CBP_OK:
+        raise CbpError(rc, name)
+
+
 def symmetry_fold(geom, batch: int = 1, view_begin: int = 0, view_count: int | None = None) -> int:
     """views per BP weight evaluation: 8 (dihedral), 4 (rotations) or 1 (include/cbp.h)."""
     g = _checked(geom)

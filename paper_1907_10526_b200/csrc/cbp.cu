@@ -47,6 +47,9 @@ cbp::GeomDev to_dev(const cbp_geometry_t& g)
     return d;
 }
 
+// the accumulate mode of the second and later launches into one output
+int acc_next(int32_t accumulate) { return accumulate == CBP_ACC_MULTIMEM ? CBP_ACC_MULTIMEM : 1; }
+
 // ---- per-(geometry, device) tables --------------------------------------
 struct TableKey {
     int device;
@@ -425,7 +428,7 @@ int launch_mag(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, 
     P.view_begin = v0;
     P.view_count = nv;
     P.batch = batch;
-    P.accumulate = accumulate ? 1 : 0;
+    P.accumulate = accumulate;  // 0, 1 or CBP_ACC_MULTIMEM
     P.sigma_max = 0.5 * (std::sqrt(2.0) * g.pixel * gmax + g.det_width) * (1.0 + 1e-9);
     const bool sym4 = use_mag_sym4(g, batch, v0, nv);
     P.image = nullptr;
@@ -603,7 +606,8 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     const int vpg = (nv + G - 1) / G;
     const size_t plane = (size_t)g.n * g.n;
     float* part = nullptr;
-    if (G > 1 || sym) {
+    const bool mc = accumulate == CBP_ACC_MULTIMEM;  // always through the reduce kernel
+    if (G > 1 || sym || mc) {
         int rc = scratch_alloc((void**)&part, sizeof(float) * plane * batch * G * (sym ? images : 1), stream);
         if (rc != CBP_OK) return rc;
     }
@@ -623,16 +627,16 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     P.g = to_dev(g);
     P.t = t;
     P.sino = sino;
-    P.out = (G > 1 || sym) ? part : img;
+    P.out = (G > 1 || sym || mc) ? part : img;
     P.sym_stride = symmode == 4 ? nv : 0;
     P.sym_mode = symmode;
     P.images = sym ? images : 1;
     P.view_begin = v0;
     P.view_count = nv;
-    P.groups = (G > 1 || sym) ? G : 1;
+    P.groups = (G > 1 || sym || mc) ? G : 1;
     P.views_per_group = vpg;
     P.batch = batch;
-    P.accumulate = (G == 1 && !sym && accumulate) ? 1 : 0;
+    P.accumulate = (G == 1 && !sym && !mc && accumulate) ? 1 : 0;
     dim3 grid(tiles, tiles, G * SG);
 #ifdef CBP_DEBUG_CHECKS
     fprintf(stderr, "launch_bp S=%d G=%d vpg=%d grid=%d,%d,%d smem=%zu\n", S, G, vpg, grid.x, grid.y,
@@ -644,14 +648,14 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     fprintf(stderr, "bp kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
 #endif
     if (hdrs_owned) cudaFreeAsync(hdrs_owned, stream);
-    if (sym || G > 1) {
+    if (sym || G > 1 || mc) {
         // symmetric: the G x S frame planes are already in output orientation
         const size_t count = sym ? plane : plane * batch;
         const int planes = sym ? G * batch : G;
         const int outs = sym ? images : 1;  // symmetric batch: one reduction per image
         const int blocks = (int)std::min<size_t>((count / 4 + 255) / 256, (size_t)sms * 8 / outs + 1);
         cbp::cbp_reduce_kernel<<<dim3(std::max(blocks, 1), outs), 256, 0, stream>>>(part, img, count, planes,
-                                                                                   accumulate ? 1 : 0);
+                                                                                   mc ? 2 : (accumulate ? 1 : 0));
         ++g_launches;
         cudaFreeAsync(part, stream);
     }
@@ -736,10 +740,16 @@ int cbp_back(const cbp_geometry_t* g, const float* sino, float* image, int32_t b
 {
     int rc = check_common(g, sino, image, batch, view_begin, view_count);
     if (rc != CBP_OK) return rc;
+    if (accumulate < 0 || accumulate > CBP_ACC_MULTIMEM) return CBP_EINVAL;
     cudaStream_t stream = (cudaStream_t)stream_;
     cbp::Tables t;
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
-    const int ks = pointer_kind(sino), ki = pointer_kind(image);
+    const int ks = pointer_kind(sino);
+    if (accumulate == CBP_ACC_MULTIMEM) {  // image: a device multicast address (not checked)
+        if (ks != 1) return CBP_EINVAL;
+        return launch_bp(*g, t, sino, image, batch, view_begin, view_count, accumulate, stream);
+    }
+    const int ki = pointer_kind(image);
     if (ki < 0 || ks < 0) return CBP_EINVAL;
     if (ki == 1 && ks == 1)
         return launch_bp(*g, t, sino, image, batch, view_begin, view_count, accumulate, stream);
@@ -929,13 +939,13 @@ int cbp_symmetry_fold(const cbp_geometry_t* g, int32_t batch, int32_t view_begin
 }
 
 static int check_orbit(const cbp_geometry_t* g, const void* a, const void* b, int32_t base_begin,
-                       int32_t base_count)
+                       int32_t base_count, bool mc_image = false)
 {
     if (cbp_validate(g) != CBP_OK || g->n_views % 4 != 0) return CBP_EINVAL;
     if (!a || !b || base_count < 1 || base_begin < 0 || (int64_t)base_begin + base_count > g->n_views / 4)
         return CBP_EINVAL;
     if (((uintptr_t)a & 3) || ((uintptr_t)b & 3)) return CBP_EINVAL;
-    if (pointer_kind(a) != 1 || pointer_kind(b) != 1) return CBP_EINVAL;
+    if ((!mc_image && pointer_kind(a) != 1) || pointer_kind(b) != 1) return CBP_EINVAL;
     return CBP_OK;
 }
 
@@ -959,7 +969,8 @@ int cbp_forward_orbit(const cbp_geometry_t* g, const float* image, float* sino, 
 int cbp_back_orbit(const cbp_geometry_t* g, const float* sino, float* image, int32_t base_begin,
                    int32_t base_count, int32_t accumulate, void* stream_)
 {
-    int rc = check_orbit(g, image, sino, base_begin, base_count);
+    if (accumulate < 0 || accumulate > CBP_ACC_MULTIMEM) return CBP_EINVAL;
+    int rc = check_orbit(g, image, sino, base_begin, base_count, accumulate == CBP_ACC_MULTIMEM);
     if (rc != CBP_OK) return rc;
     cudaStream_t stream = (cudaStream_t)stream_;
     cbp::Tables t;
@@ -967,7 +978,8 @@ int cbp_back_orbit(const cbp_geometry_t* g, const float* sino, float* image, int
     if (g->model == CBP_MODEL_MAG) {
         for (int q = 0; q < 4 && rc == CBP_OK; ++q)
             rc = launch_mag(*g, t, image, const_cast<float*>(sino) + (size_t)q * base_count * g->n_det, 1,
-                            base_begin + q * (g->n_views / 4), base_count, accumulate || q > 0, stream, false);
+                            base_begin + q * (g->n_views / 4), base_count, q > 0 ? acc_next(accumulate) : accumulate,
+                            stream, false);
         return rc;
     }
     return launch_bp_s<4>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 4);
@@ -989,20 +1001,20 @@ static int mag_dihedral(const cbp_geometry_t& g, const cbp::Tables& t, const flo
         for (int r = 0; r < 4 && rc == CBP_OK; ++r, ++done) {
             const int v = starts[blk] + r * q;
             rc = launch_mag(g, t, image, sino + (size_t)v * g.n_det, 1, v, counts[blk],
-                            accumulate || done > 0, stream, fp);
+                            done > 0 ? acc_next(accumulate) : accumulate, stream, fp);
         }
     }
     return rc;
 }
 
 static int check_dihedral(const cbp_geometry_t* g, const void* a, const void* b, int32_t base_begin,
-                          int32_t base_count)
+                          int32_t base_count, bool mc_image = false)
 {
     if (cbp_validate(g) != CBP_OK || g->n_views % 8 != 0) return CBP_EINVAL;
     if (!a || !b || base_count < 1 || base_begin < 0 || (int64_t)base_begin + base_count > g->n_views / 8 + 1)
         return CBP_EINVAL;
     if (((uintptr_t)a & 3) || ((uintptr_t)b & 3)) return CBP_EINVAL;
-    if (pointer_kind(a) != 1 || pointer_kind(b) != 1) return CBP_EINVAL;
+    if ((!mc_image && pointer_kind(a) != 1) || pointer_kind(b) != 1) return CBP_EINVAL;
     return CBP_OK;
 }
 
@@ -1027,7 +1039,8 @@ int cbp_forward_dihedral(const cbp_geometry_t* g, const float* image, float* sin
 int cbp_back_dihedral(const cbp_geometry_t* g, const float* sino, float* image, int32_t base_begin,
                       int32_t base_count, int32_t accumulate, void* stream_)
 {
-    int rc = check_dihedral(g, sino, image, base_begin, base_count);
+    if (accumulate < 0 || accumulate > CBP_ACC_MULTIMEM) return CBP_EINVAL;
+    int rc = check_dihedral(g, sino, image, base_begin, base_count, accumulate == CBP_ACC_MULTIMEM);
     if (rc != CBP_OK) return rc;
     cudaStream_t stream = (cudaStream_t)stream_;
     cbp::Tables t;

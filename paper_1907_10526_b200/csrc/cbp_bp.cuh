@@ -752,10 +752,12 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
     }
 }
 
-// out[p] = (accumulate ? out[p] : 0) + sum_g part[g][p] over `groups` planes
+// out[p] = (mode 1 ? out[p] : 0) + sum_g part[g][p] over `groups` planes
 // of `count` floats, fixed order (deterministic); float4 when aligned
 // (blockIdx.y selects one of gridDim.y independent outputs: part + y groups count,
-// out + y count)
+// out + y count).  mode 2: out is a multicast address and the sum is ADDED
+// to every rank's copy by multimem.red (the view-sharded all-reduce of row a7
+// fused into the BP's last kernel; order across ranks is the switch's).
 __global__ void cbp_reduce_kernel(const float* __restrict__ part, float* __restrict__ out,
                                   size_t count, int groups, int accumulate)
 {
@@ -768,7 +770,7 @@ __global__ void cbp_reduce_kernel(const float* __restrict__ part, float* __restr
         const float4* p4 = reinterpret_cast<const float4*>(part);
         float4* o4 = reinterpret_cast<float4*>(out);
         for (size_t i = t0; i < c4; i += stride) {
-            float4 s = accumulate ? o4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 s = accumulate == 1 ? o4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
             int gi = 0;
             for (; gi + 8 <= groups; gi += 8) {  // 8 loads in flight, summed in plane order
                 float4 v[8];
@@ -789,14 +791,20 @@ __global__ void cbp_reduce_kernel(const float* __restrict__ part, float* __restr
                 s.z += v.z;
                 s.w += v.w;
             }
-            o4[i] = s;
+            if (accumulate == 2)
+                mc_red_add4(o4 + i, s);
+            else
+                o4[i] = s;
         }
         return;
     }
     for (size_t i = t0; i < count; i += stride) {
-        float s = accumulate ? out[i] : 0.0f;
+        float s = accumulate == 1 ? out[i] : 0.0f;
         for (int gi = 0; gi < groups; ++gi) s += part[(size_t)gi * count + i];
-        out[i] = s;
+        if (accumulate == 2)
+            mc_red_add(out + i, s);
+        else
+            out[i] = s;
     }
 }
 

@@ -108,6 +108,20 @@ __device__ __forceinline__ float2 cnsf_num2(float2 z11, float2 z21, float2 B, fl
     return __ffma2_rn(make_float2(hC, hC), T, M2);
 }
 
+// the multimem reduction (accumulate mode CBP_ACC_MULTIMEM): `mc` is a
+// multicast address (an NVLink/NVSwitch multicast object bound to one buffer
+// on every rank); the add is performed in the switch on every rank's copy
+__device__ __forceinline__ void mc_red_add(float* mc, float v)
+{
+    asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(mc), "f"(v) : "memory");
+}
+__device__ __forceinline__ void mc_red_add4(float4* mc, float4 v)
+{
+    asm volatile("multimem.red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc), "f"(v.x),
+                 "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+
 __device__ __forceinline__ float2 rcp2(float2 b) { return make_float2(rcp_approx(b.x), rcp_approx(b.y)); }
 
 }  // namespace cbp

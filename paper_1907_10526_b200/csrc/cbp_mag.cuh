@@ -434,7 +434,10 @@ __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
         int r = row, c = col;
         mag_rot(n, q, r, c);
         float* out = p.image_out + (size_t)b * n * n + (size_t)r * n + c;
-        *out = p.accumulate ? *out + acc[q] : acc[q];
+        if (p.accumulate == 2)
+            mc_red_add(out, acc[q]);  // multicast address (CBP_ACC_MULTIMEM)
+        else
+            *out = p.accumulate ? *out + acc[q] : acc[q];
     }
 }
 
