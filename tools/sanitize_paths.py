@@ -1,0 +1,80 @@
+"""One small call of every kernel path, for compute-sanitizer (memcheck /
+racecheck / synccheck): CNSF FP/BP on the direct, batched (S = 2, 4),
+4-fold and 8-fold symmetric paths, ragged grids, the parallel and arc
+kinds, the magnified-footprint model (plain and 4-fold), orbit and dihedral
+shards, the normal operator and its host pipeline, the FP64 reference pair,
+and the vector / TV kernels of the iterative loops."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1907_10526_b200 as cbp  # noqa: E402
+from paper_1907_10526_b200 import sharded  # noqa: E402
+import workloads as W  # noqa: E402
+
+
+def pair(g, batch=1, v0=0, nv=None):
+    n = g["n"]
+    nv = g["n_views"] - v0 if nv is None else nv
+    img = torch.from_numpy(W.random_image(n, 1, batch=batch) if batch > 1 else W.random_image(n, 1)).cuda()
+    y = cbp.forward(g, img, view_begin=v0, view_count=nv)
+    c = cbp.back(g, y, view_begin=v0)
+    cbp.back(g, y, image=c, view_begin=v0, accumulate=True)
+
+
+g1 = W.geometry("1")
+for nvw in (90, 92, 88):                       # direct, 4-fold, 8-fold
+    pair(dict(g1, n_views=nvw))
+pair(g1, v0=13, nv=21)                         # view range
+for b in (2, 3, 5):                            # batched S = 2 / 4, ragged batch
+    pair(g1, batch=b)
+pair(dict(g1, n_views=88), batch=3)            # batch over a full scan (per-image dihedral BP)
+rag = dict(n=37, pixel=1.3, n_views=30, n_det=77, det_pitch=1.1, det_width=0.6, sid=120.0, sdd=260.0)
+pair(rag)
+pair(rag, batch=5)
+pair(dict(rag, n_views=32))                    # ragged tiles with the symmetry
+for kind in (cbp.PARALLEL, cbp.FAN_ARC):
+    g = dict(g1, kind=kind, n_views=88) if kind == cbp.PARALLEL else \
+        dict(n=64, pixel=1.0, n_views=88, n_det=160, det_pitch=1.2, det_width=1.0, sid=100.0, sdd=200.0, kind=kind)
+    pair(g)
+    pair(dict(g, n_views=90), batch=2)
+for model_g in (dict(g1, model=1), dict(g1, model=1, n_views=88), dict(rag, model=1)):
+    pair(model_g)
+pair(dict(rag, model=1), batch=3)
+# shards
+g = dict(g1, n_views=88)
+img = torch.from_numpy(W.random_image(64, 2)).cuda()
+for dihedral in (False, True):
+    for r in range(3):
+        sh = sharded.make_shard(88, r, 3, dihedral=dihedral)
+        if sh.mode == "orbit":
+            y = cbp.forward_orbit(g, img, sh.begin, sh.count)
+            cbp.back_orbit(g, y, sh.begin)
+        else:
+            y = cbp.forward_dihedral(g, img, sh.begin, sh.count)
+            cbp.back_dihedral(g, y, sh.begin, sh.count)
+# normal operator, device and host pipeline
+cbp.normal(g1, img)
+cbp.normal_stream(g1, np.stack([W.random_image(64, i) for i in range(3)]))
+# reference projector
+gs = dict(g1, n=16, n_views=6, n_det=40)
+yr = cbp.ref_forward(gs, torch.from_numpy(W.random_image(16, 3)).cuda())
+cbp.ref_back(gs, yr)
+# vector / TV kernels
+x = torch.rand(64 * 64, device="cuda")
+z = torch.rand(64 * 64, device="cuda")
+d = torch.zeros(4, dtype=torch.float64, device="cuda")
+cbp.dot(x, z, d[0:1])
+cbp.tv_value(x.view(64, 64), d[1:2])
+cbp.tv_gradient(x.view(64, 64), z.view(64, 64))
+cbp.diff_norm2(x, z, d[2:3])
+# SART / CGLS iterations (their vector kernels)
+from paper_1907_10526_b200 import recon  # noqa: E402
+yf = cbp.forward(g1, img)
+recon.sart(g1, yf, 1)
+recon.cgls(g1, yf, 1)
+torch.cuda.synchronize()
+print("sanitize paths ok, launches", cbp.launch_count())
