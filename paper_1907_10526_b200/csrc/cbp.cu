@@ -914,18 +914,25 @@ int cbp_normal_stream(const cbp_geometry_t* g, const float* images, float* out, 
         ok = ok && cudaStreamWaitEvent(stream, P->in_ready[k], 0) == cudaSuccess;
         if (i >= 2) ok = ok && cudaStreamWaitEvent(stream, P->out_free[k], 0) == cudaSuccess;
         if (!ok) break;
-        if ((rc = launch_fp(*g, t, din, sino, batch, 0, g->n_views, stream)) != CBP_OK) return rc;
+        if ((rc = launch_fp(*g, t, din, sino, batch, 0, g->n_views, stream)) != CBP_OK) break;
         ok = ok && cudaEventRecord(P->in_free[k], stream) == cudaSuccess;
-        if ((rc = launch_bp(*g, t, sino, dout, batch, 0, g->n_views, 0, stream)) != CBP_OK) return rc;
+        if ((rc = launch_bp(*g, t, sino, dout, batch, 0, g->n_views, 0, stream)) != CBP_OK) break;
         ok = ok && cudaEventRecord(P->out_ready[k], stream) == cudaSuccess;
         // D2H of result i
         ok = ok && cudaStreamWaitEvent(P->d2h, P->out_ready[k], 0) == cudaSuccess;
         ok = ok && cudaMemcpyAsync(out + i * ni, dout, ib, cudaMemcpyDeviceToHost, P->d2h) == cudaSuccess;
         ok = ok && cudaEventRecord(P->out_free[k], P->d2h) == cudaSuccess;
     }
-    ok = ok && cudaEventRecord(P->done, P->d2h) == cudaSuccess;
-    ok = ok && cudaStreamWaitEvent(stream, P->done, 0) == cudaSuccess;
-    ok = ok && cudaEventSynchronize(P->done) == cudaSuccess;
+    if (rc != CBP_OK || !ok) {
+        // nothing may still write the caller's host buffers after an error return
+        cudaStreamSynchronize(P->h2d);
+        cudaStreamSynchronize(stream);
+        cudaStreamSynchronize(P->d2h);
+        cudaGetLastError();
+        return rc != CBP_OK ? rc : CBP_ECUDA;
+    }
+    ok = cudaEventRecord(P->done, P->d2h) == cudaSuccess && cudaStreamWaitEvent(stream, P->done, 0) == cudaSuccess &&
+         cudaEventSynchronize(P->done) == cudaSuccess;
     return ok ? CBP_OK : CBP_ECUDA;
 }
 

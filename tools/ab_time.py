@@ -12,7 +12,7 @@ CHILD = r'''
 import os, sys, json, statistics, torch
 sys.path.insert(0, %r)
 import paper_1907_10526_b200 as cbp, workloads as W
-g = W.geometry(%r)
+g = dict(W.geometry(%r), model=int(os.environ.get("AB_MODEL", "0")))
 img = torch.from_numpy(W.shepp_logan(g["n"])).cuda()
 y = cbp.forward(g, img); c = cbp.back(g, y)
 def t(fn, reps=30):
