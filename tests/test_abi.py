@@ -124,3 +124,12 @@ def test_product_package_does_not_import_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", text).replace(
                     "no oracle", ""), f
+
+
+def test_fuzz_draws_are_valid_scanners():
+    """the randomised GPU parity test (test_gpu_fuzz.py) draws only valid
+    scanners: cbp_validate makes no CUDA call"""
+    from tests.test_gpu_fuzz import draw
+    for s in range(160):
+        g = draw(s)[0]
+        assert cbp.validate(g) == cbp.CBP_OK, (s, g)

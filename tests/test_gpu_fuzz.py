@@ -1,0 +1,68 @@
+"""Randomised parity: seeded random scanners (every kind and weight model,
+odd and even grids, ragged tiles, one view / one bin, close and far
+sources, wide and narrow bins, tau != Delta_s), batches and view ranges,
+FP and BP of the CUDA path against the oracle at the parity bar of
+test_gpu_parity.py.  The draws are fixed by the seed, so a failure
+reproduces; they cover the symmetric paths (full scans with n_views % 4,
+% 8 == 0) as well as the direct and batched ones."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1907_10526_b200 as cbp
+import workloads as W
+
+from tests.test_gpu_parity import _assert_parity, _bp, _fp, torch_cuda  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+
+def draw(seed):
+    rng = np.random.default_rng(1000 + seed)
+    kind = int(rng.integers(0, 3))
+    model = int(rng.random() < 0.3)
+    n = int(rng.choice([1, 2, 5, 16, 31, 32, 33, 48, 64, 70, 97, 130]))
+    h = float(rng.uniform(0.3, 2.0))
+    n_views = int(rng.choice([1, 3, 8, 16, 24, 30, 40, 45, 64, 72]))
+    pitch = float(rng.uniform(0.4, 2.5)) * h
+    width = float(np.exp(rng.uniform(np.log(0.05), np.log(3.0)))) * pitch  # tau/Delta_s 0.05 .. 3
+    R = n * h / np.sqrt(2.0)
+    sid = float(R * rng.uniform(1.15, 6.0) + 1.0)
+    sdd = float(sid * rng.uniform(1.0, 2.5))
+    # enough bins to cover the field of view (plus a random margin or shortfall)
+    if kind == 1:
+        span = 2 * R
+    else:
+        span = 2 * sdd * np.tan(np.arcsin(min(R / sid, 0.999)))
+    n_det = max(1, int(span / pitch * rng.uniform(0.6, 1.3)) + int(rng.integers(0, 4)))
+    if kind == 2:  # arc: every bin within +-90 degrees (arc length / sdd)
+        n_det = max(1, min(n_det, int(2.9 * sdd / pitch) - 2))
+    g = dict(n=n, pixel=h, n_views=n_views, n_det=n_det, det_pitch=pitch, det_width=width,
+             sid=sid if kind != 1 else 0.0, sdd=sdd if kind != 1 else 0.0, kind=kind, model=model)
+    batch = int(rng.choice([1, 1, 1, 2, 3, 5]))
+    full = rng.random() < 0.6
+    v0 = 0 if full else int(rng.integers(0, n_views))
+    nv = n_views - v0 if full else int(rng.integers(1, n_views - v0 + 1))
+    return g, batch, v0, nv, rng
+
+
+@pytest.mark.parametrize("seed", range(160))
+def test_random_scanner_parity(torch_cuda, seed):
+    g, batch, v0, nv, rng = draw(seed)
+    assert cbp.validate(g) == cbp.CBP_OK, g
+    n = g["n"]
+    imgs = W.random_image(n, 500 + seed, batch=batch) if batch > 1 else W.random_image(n, 500 + seed)
+    what = f"seed {seed} {g} batch {batch} views {v0}+{nv}"
+    want = O.forward(g, imgs, view_begin=v0, view_count=nv)
+    if np.abs(want).max() == 0.0:  # the bins miss the image entirely: exact zeros
+        assert not _fp(torch_cuda, g, imgs, view_begin=v0, view_count=nv).any(), what
+    else:
+        _assert_parity(_fp(torch_cuda, g, imgs, view_begin=v0, view_count=nv), want, "FP " + what)
+    y = W.random_sino(nv, g["n_det"], 600 + seed, batch=batch) if batch > 1 else \
+        W.random_sino(nv, g["n_det"], 600 + seed)
+    want_b = O.back(g, y, view_begin=v0)
+    if np.abs(want_b).max() == 0.0:
+        assert not _bp(torch_cuda, g, y, view_begin=v0).any(), what
+    else:
+        _assert_parity(_bp(torch_cuda, g, y, view_begin=v0), want_b, "BP " + what)
+
