@@ -342,10 +342,15 @@ def main():
                          "effective_tflops_per_view_weight": units * FLOPS_PER_WEIGHT / (ms * 1e-3) / 1e12
                          if units else None}
     dom = "bp" if bp_avg >= fp_avg else "fp"
-    traffic = traffic_table().get(args.config, {}).get(dom)
+    ttab = traffic_table().get(args.config, {})
+    traffic = ttab.get(dom)
     roof = {"bound": "alu", "kernel": f"cbp_{dom}_kernel", "achieved": kernels[dom]["tflops"],
             "peak": peak_tflops, "unit": "TFLOP/s", "frac": kernels[dom]["frac"],
             "traffic": traffic,
+            # the FP32 (FMA) pipe utilisation ncu measured for this kernel in the
+            # committed capture of this command (profiles/traffic.json), and its issue-slot use
+            "fma_pipe_util_ncu": ttab.get(f"{dom}_fma_pipe"),
+            "issue_active_ncu": ttab.get(f"{dom}_issue"),
             "peak_basis": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 flop x "
                           f"{sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
             "work": f"{units} nonzero view-weights per launch ({nw} x {batch} slices), each weight "
