@@ -387,52 +387,100 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
 
 // BP: c[b][k] = sum_{v, j} y[b][v][j] W(v, j, k) over the bins of k's footprint
 // (|j - P/Delta_s - c_s| < sigma/Delta_s, widened by 1e-3 bin; the exact test decides).
-// F = 4 (one image, a full scan, N_v % 4 == 0, n even): a thread per pixel k
-// of the quadrant rows < n/2, cols < n/2 (whose 4 rotations tile the grid)
-// accumulates the 4 pixels R^q k over all views v, each weight serving
-// (v + q N_v/4 mod N_v, R^q k): one footprint per 4 (view, pixel) pairs.
+// F = 8 (one image, a full scan, N_v % 4 == 0, n even): the dihedral group of
+// the square grid, frames g = R^q M^m (R(r, c) = (n-1-c, r), M(r, c) =
+// (n-1-r, c)) with W(view_g(v), bin_g(j), g k) = W(v, j, k),
+// view_g(v) = (m ? N_v - v : v) + q N_v/4 (mod N_v), bin_g(j) = m ? N_s-1-j : j.
+// A thread per pixel k of the triangle r <= c of the top-left quadrant (a
+// fundamental domain: its 8 images tile the grid; the transpose M R fixes
+// its diagonal, whose pixels take the 4 rotations only) loops over all views
+// and owns the 8 (4) output pixels g k: one footprint per 8 (view, pixel)
+// pairs, no write conflicts.
+// A CTA is 32 pixels x MAG_BP_VG view groups (views interleaved over the
+// groups, for parallelism: the 8-fold domain has only n^2/8 pixels); the
+// groups' partial sums are added in group order in shared memory.
+constexpr int MAG_BP_VG = MAG_BP_BLOCK / 32;
+
 template <int F>
 __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
 {
+    __shared__ float red[MAG_BP_VG][F][32];
     const GeomDev& g = p.g;
     const int n = g.n;
-    const int nq = F == 1 ? n : n / 2;  // side of the pixel domain the threads cover
-    const int k = blockIdx.x * MAG_BP_BLOCK + threadIdx.x;
+    const int lane = threadIdx.x & 31, vg = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + lane;
     const int b = blockIdx.y;
-    if (k >= nq * nq) return;
-    const int row = k / nq, col = k - row * nq;
+    int row = 0, col = 0;
+    bool valid;
+    if (F == 1) {
+        valid = t < n * n;
+        row = t / n;
+        col = t - row * n;
+    } else if (F == 4) {  // the top-left quadrant (its 4 rotations tile the grid)
+        const int half = n / 2;
+        valid = t < half * half;
+        row = min(t / half, half - 1);
+        col = t - (t / half) * half;
+    } else {
+        // triangle index t -> (row, col), row <= col < half; row r starts at r half - r (r - 1) / 2
+        const int half = n / 2;
+        valid = t < half * (half + 1) / 2;
+        const float tw = (float)(2 * half + 1);
+        int r = (int)floorf(0.5f * (tw - sqrtf(fmaxf(tw * tw - 8.0f * (float)t, 0.0f))));
+        r = max(0, min(r, half - 1));
+        while (r > 0 && r * half - r * (r - 1) / 2 > t) --r;
+        while (r + 1 < half && (r + 1) * half - (r + 1) * r / 2 <= t) ++r;
+        row = r;
+        col = min(half - 1, r + (t - (r * half - r * (r - 1) / 2)));
+    }
+    const bool diag = F == 8 && row == col;
     const double kx = ((double)col - g.c0) * g.h, ky = (g.c0 - (double)row) * g.h;
     const float B = (float)g.tau;
     const double inv_pitch = 1.0 / g.pitch;
-    const int vq = g.n_views / 4;  // F = 4: frame q reads sinogram row v + q vq (mod N_v)
+    const int N = g.n_views, vq = N / 4;
     const float* y = p.sino_in + (size_t)b * p.view_count * g.n_det;
     float acc[F];
 #pragma unroll
     for (int q = 0; q < F; ++q) acc[q] = 0.0f;
-    for (int vl = 0; vl < p.view_count; ++vl) {
+    for (int vl = vg; valid && vl < p.view_count; vl += MAG_BP_VG) {
         const double2 cs = p.view_cs[p.view_begin + vl];
         const MagFootprint fp = mag_footprint(g, cs.x, cs.y, kx, ky);
         const double jc = fp.P * inv_pitch + g.cs, jw = (double)fp.sigma * inv_pitch + 1e-3;
         const double jlo = fmax(jc - jw, -1.0), jhi = fmin(jc + jw, (double)g.n_det);
         const int ja = max(0, (int)ceil(jlo)), jb = min(g.n_det - 1, (int)floor(jhi));
+        // sinogram rows of the frames (mirrored frames read their rows backwards)
         const float* yq[F];
 #pragma unroll
         for (int q = 0; q < F; ++q) {
-            int v = vl + q * vq;
-            if (v >= g.n_views) v -= g.n_views;
-            yq[q] = y + (size_t)(F == 1 ? vl : v) * g.n_det;
+            int v = F == 1 ? vl : (((q >= 4) ? N - vl : vl) + (q & 3) * vq) % N;
+            yq[q] = y + (size_t)v * g.n_det + ((q >= 4) ? g.n_det - 1 : 0);
         }
         double sj = mag_bin_s(g, ja);
         for (int j = ja; j <= jb; ++j, sj += g.pitch) {
             const float wgt = mag_weight_x(fp, (float)(sj - fp.P), B);
 #pragma unroll
-            for (int q = 0; q < F; ++q) acc[q] = __fmaf_rn(__ldg(yq[q] + j), wgt, acc[q]);
+            for (int q = 0; q < F; ++q) {
+                if (q < 4 || !diag) acc[q] = __fmaf_rn(__ldg(yq[q] + (q >= 4 ? -j : j)), wgt, acc[q]);
+            }
         }
     }
 #pragma unroll
+    for (int q = 0; q < F; ++q) red[vg][q][lane] = acc[q];
+    __syncthreads();
+    if (vg != 0 || !valid) return;
+#pragma unroll
     for (int q = 0; q < F; ++q) {
+        float sum = red[0][q][lane];
+#pragma unroll
+        for (int gg = 1; gg < MAG_BP_VG; ++gg) sum += red[gg][q][lane];
+        acc[q] = sum;
+    }
+#pragma unroll
+    for (int q = 0; q < F; ++q) {
+        if (q >= 4 && diag) continue;  // the transpose repeats the rotations' pixels
         int r = row, c = col;
-        mag_rot(n, q, r, c);
+        if (q >= 4) r = n - 1 - r;  // M, then R^(q mod 4)
+        mag_rot(n, q & 3, r, c);
         float* out = p.image_out + (size_t)b * n * n + (size_t)r * n + c;
         if (p.accumulate == 2)
             mc_red_add(out, acc[q]);  // multicast address (CBP_ACC_MULTIMEM)

@@ -32,7 +32,7 @@ def _mag(kind=cbp.FAN_FLAT, **kw):
 def test_mag_forward_back(torch_cuda, kind, n_views):
     g = _mag(kind, n_views=n_views)
     # a full scan with n_views % 4 == 0 on an even grid: one footprint per 4 views
-    assert cbp.symmetry_fold(g) == (4 if n_views % 4 == 0 else 1)
+    assert cbp.symmetry_fold(g) == (4 if n_views % 4 == 0 else 1)  # the BP at n = 64: 4 frames
     for img in (W.shepp_logan(64), W.random_image(64, 5)):
         _assert_parity(_fp(torch_cuda, g, img), O.forward(g, img), f"FP mag kind {kind} {n_views}")
     y = W.random_sino(n_views, g["n_det"], 6)
@@ -140,3 +140,20 @@ def test_mag_symmetric_equals_plain(torch_cuda):
     c_sym = cbp.back(g, s)
     c_plain = sum(cbp.back(g, s[v:v + 1].contiguous(), view_begin=v) for v in range(40))
     _assert_parity(c_sym.cpu().numpy(), c_plain.cpu().numpy(), "mag BP sym vs plain")
+
+
+def test_mag_dihedral_bp_large_grid(torch_cuda):
+    # n = 1024: the BP takes the 8-frame dihedral triangle (diagonal pixels 4 frames);
+    # sampled pixels on and off the diagonals against the oracle
+    g = dict(W.geometry("3"), model=cbp.MODEL_MAG, n_views=48)
+    assert cbp.symmetry_fold(g) == 8
+    s = W.random_sino(48, g["n_det"], 77)
+    c = _bp(torch_cuda, g, s)
+    rows = np.array([0, 511, 512, 1023, 100, 923, 300, 5, 700])
+    cols = np.array([0, 511, 512, 1023, 100, 100, 723, 900, 20])
+    _assert_parity(c[rows, cols], O.back_pixels(g, s, rows, cols), "BP mag dihedral n=1024")
+    # every pixel against the same projector view by view (no symmetry)
+    torch = torch_cuda
+    st = torch.from_numpy(s).cuda()
+    plain = sum(cbp.back(g, st[v:v + 1].contiguous(), view_begin=v) for v in range(48))
+    _assert_parity(c, plain.cpu().numpy(), "BP mag dihedral vs plain n=1024")
