@@ -416,8 +416,19 @@ bool use_mag_sym4(const cbp_geometry_t& g, int32_t batch, int32_t v0, int32_t nv
 // config 3 (n = 1024) 4.86 vs 4.30 ms
 int mag_bp_fold(const cbp_geometry_t& g)
 {
+    static const int force = getenv("CBP_MAG_BP_FOLD") ? atoi(getenv("CBP_MAG_BP_FOLD")) : 0;  // tuning knob
+    if (force == 4 || force == 8) return force;
     const int64_t half = g.n / 2;
     return half * (half + 1) / 2 >= 100000 ? 8 : 4;
+}
+
+// view groups per pixel of the magnified-footprint BP: enough threads for
+// ~256 k (about 14 resident warps per SM), at most MAG_BP_VG
+int mag_bp_groups(int64_t pixels)
+{
+    int vg = 1;
+    while (vg < cbp::MAG_BP_VG && pixels * vg < (256 << 10)) vg *= 2;
+    return vg;
 }
 
 // Row f3, the magnified-footprint model (cbp_mag.cuh).  sigma_max bounds
@@ -439,6 +450,7 @@ int launch_mag(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, 
     P.view_count = nv;
     P.batch = batch;
     P.accumulate = accumulate;  // 0, 1 or CBP_ACC_MULTIMEM
+    P.vg = 1;
     P.sigma_max = 0.5 * (std::sqrt(2.0) * g.pixel * gmax + g.det_width) * (1.0 + 1e-9);
     const bool sym4 = use_mag_sym4(g, batch, v0, nv);
     P.image = nullptr;
@@ -458,19 +470,24 @@ int launch_mag(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, 
     } else {  // BP: img is the output image, sino the input sinogram
         P.sino_in = sino;
         P.image_out = const_cast<float*>(img);
-        if (sym4) {  // all views; CTAs of 32 pixels x MAG_BP_VG view groups
+        if (sym4) {  // all views; CTAs of 32 pixels x VG view groups
             const int64_t half = g.n / 2;
-            if (mag_bp_fold(g) == 8) {  // the dihedral fundamental triangle, 8 frames
-                const int64_t pix = half * (half + 1) / 2;
-                cbp::cbp_mag_bp_kernel<8><<<dim3((unsigned)((pix + 31) / 32), 1), cbp::MAG_BP_BLOCK, 0, stream>>>(P);
-            } else {  // the top-left quadrant, 4 rotations
-                const int64_t pix = half * half;
-                cbp::cbp_mag_bp_kernel<4><<<dim3((unsigned)((pix + 31) / 32), 1), cbp::MAG_BP_BLOCK, 0, stream>>>(P);
-            }
+            const int fold = mag_bp_fold(g);
+            const int64_t pix = fold == 8 ? half * (half + 1) / 2 : half * half;
+            P.vg = mag_bp_groups(pix);
+            const int per = cbp::MAG_BP_BLOCK / P.vg;  // pixels per CTA
+            const dim3 grid((unsigned)((pix + per - 1) / per), 1);
+            const size_t sm = P.vg > 1 ? sizeof(float) * fold * cbp::MAG_BP_BLOCK : 0;
+            if (fold == 8)  // the dihedral fundamental triangle, 8 frames
+                cbp::cbp_mag_bp_kernel<8><<<grid, cbp::MAG_BP_BLOCK, sm, stream>>>(P);
+            else  // the top-left quadrant, 4 rotations
+                cbp::cbp_mag_bp_kernel<4><<<grid, cbp::MAG_BP_BLOCK, sm, stream>>>(P);
         } else {
             const int64_t pix = (int64_t)g.n * g.n;
-            const unsigned blocks = (unsigned)((pix + 31) / 32);
-            cbp::cbp_mag_bp_kernel<1><<<dim3(blocks, batch), cbp::MAG_BP_BLOCK, 0, stream>>>(P);
+            P.vg = mag_bp_groups(pix * batch);
+            const int per = cbp::MAG_BP_BLOCK / P.vg;
+            cbp::cbp_mag_bp_kernel<1><<<dim3((unsigned)((pix + per - 1) / per), batch), cbp::MAG_BP_BLOCK,
+                                        P.vg > 1 ? sizeof(float) * cbp::MAG_BP_BLOCK : 0, stream>>>(P);
         }
     }
     ++g_launches;

@@ -140,6 +140,7 @@ struct MagParams {
     const float* sino_in;  // BP: [batch][view_count][n_det]
     float* image_out;      // BP: [batch][n][n]
     int view_begin, view_count, batch, accumulate;
+    int vg;            // BP: view groups per pixel (1, 2, 4)
     double sigma_max;  // upper bound of every pixel's support half-width
 };
 
@@ -396,19 +397,21 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
 // its diagonal, whose pixels take the 4 rotations only) loops over all views
 // and owns the 8 (4) output pixels g k: one footprint per 8 (view, pixel)
 // pairs, no write conflicts.
-// A CTA is 32 pixels x MAG_BP_VG view groups (views interleaved over the
-// groups, for parallelism: the 8-fold domain has only n^2/8 pixels); the
-// groups' partial sums are added in group order in shared memory.
+// A CTA (MAG_BP_BLOCK threads) is 32 (4 / VG) pixels x VG view groups (views
+// interleaved over the groups, for parallelism when the pixel domain is
+// small; p.vg = VG in 1, 2, 4); the groups' partial sums are added in group
+// order in shared memory.
 constexpr int MAG_BP_VG = MAG_BP_BLOCK / 32;
 
 template <int F>
 __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
 {
-    __shared__ float red[MAG_BP_VG][F][32];
+    extern __shared__ float red[];  // VG > 1: [VG][F][MAG_BP_BLOCK / VG] (none for VG = 1: the L1 keeps it)
     const GeomDev& g = p.g;
     const int n = g.n;
-    const int lane = threadIdx.x & 31, vg = threadIdx.x >> 5;
-    const int t = blockIdx.x * 32 + lane;
+    const int VG = p.vg, warp = threadIdx.x >> 5, vg = warp % VG;
+    const int slot = (warp / VG) * 32 + (threadIdx.x & 31);  // pixel of the CTA
+    const int t = blockIdx.x * (MAG_BP_BLOCK / VG) + slot;
     const int b = blockIdx.y;
     int row = 0, col = 0;
     bool valid;
@@ -442,7 +445,7 @@ __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
     float acc[F];
 #pragma unroll
     for (int q = 0; q < F; ++q) acc[q] = 0.0f;
-    for (int vl = vg; valid && vl < p.view_count; vl += MAG_BP_VG) {
+    for (int vl = vg; valid && vl < p.view_count; vl += VG) {
         const double2 cs = p.view_cs[p.view_begin + vl];
         const MagFootprint fp = mag_footprint(g, cs.x, cs.y, kx, ky);
         const double jc = fp.P * inv_pitch + g.cs, jw = (double)fp.sigma * inv_pitch + 1e-3;
@@ -452,7 +455,8 @@ __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
         const float* yq[F];
 #pragma unroll
         for (int q = 0; q < F; ++q) {
-            int v = F == 1 ? vl : (((q >= 4) ? N - vl : vl) + (q & 3) * vq) % N;
+            int v = F == 1 ? vl : ((q >= 4) ? N - vl : vl) + (q & 3) * vq;  // < 2 N
+            if (v >= N) v -= N;
             yq[q] = y + (size_t)v * g.n_det + ((q >= 4) ? g.n_det - 1 : 0);
         }
         double sj = mag_bin_s(g, ja);
@@ -464,17 +468,20 @@ __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
             }
         }
     }
+    if (VG > 1) {
 #pragma unroll
-    for (int q = 0; q < F; ++q) red[vg][q][lane] = acc[q];
-    __syncthreads();
-    if (vg != 0 || !valid) return;
+        const int per = MAG_BP_BLOCK / VG;
+        for (int q = 0; q < F; ++q) red[(vg * F + q) * per + slot] = acc[q];
+        __syncthreads();
+        if (vg != 0) return;
 #pragma unroll
-    for (int q = 0; q < F; ++q) {
-        float sum = red[0][q][lane];
-#pragma unroll
-        for (int gg = 1; gg < MAG_BP_VG; ++gg) sum += red[gg][q][lane];
-        acc[q] = sum;
+        for (int q = 0; q < F; ++q) {
+            float sum = red[q * per + slot];
+            for (int gg = 1; gg < VG; ++gg) sum += red[(gg * F + q) * per + slot];
+            acc[q] = sum;
+        }
     }
+    if (!valid) return;
 #pragma unroll
     for (int q = 0; q < F; ++q) {
         if (q >= 4 && diag) continue;  // the transpose repeats the rotations' pixels
