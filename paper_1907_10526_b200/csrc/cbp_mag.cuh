@@ -469,8 +469,8 @@ __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
         }
     }
     if (VG > 1) {
-#pragma unroll
         const int per = MAG_BP_BLOCK / VG;
+#pragma unroll
         for (int q = 0; q < F; ++q) red[(vg * F + q) * per + slot] = acc[q];
         __syncthreads();
         if (vg != 0) return;
