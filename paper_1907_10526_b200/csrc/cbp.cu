@@ -268,13 +268,19 @@ int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stre
     static const int force = getenv("CBP_FP_PARTS") ? atoi(getenv("CBP_FP_PARTS")) : 0;  // tuning knob
     const int64_t slots = (int64_t)sms * per_sm[dev & 63];
     auto ctas = [&](int parts) {
-        return (int64_t)((Pm.g.n_det + cbp::FP_BLOCK / parts - 1) / (cbp::FP_BLOCK / parts)) * views * groups;
+        const int bins = cbp::fp_threads(parts) / parts;  // bins per CTA
+        return (int64_t)((Pm.g.n_det + bins - 1) / bins) * views * groups;
     };
     int parts = 1;
     while (parts < 4 && ctas(parts) < 16 * slots) parts *= 2;  // config 3 (6.5 waves): parts 4 -4 %
-    if (force == 1 || force == 2 || force == 4) parts = force;
+    // under one wave of 4-part CTAs (a view shard, a small image): 8 warps per
+    // ray group in 256-thread CTAs, each walking an eighth of the lines
+    if (parts == 4 && ctas(4) < slots) parts = 8;
+    if (force == 1 || force == 2 || force == 4 || force == 8) parts = force;
     const dim3 grid((unsigned)(ctas(parts) / ((int64_t)views * groups)), views, groups);
-    if (parts == 4)
+    if (parts == 8)
+        cbp::cbp_fp_kernel<S, 8><<<grid, cbp::fp_threads(8), 0, stream>>>(Pm);
+    else if (parts == 4)
         cbp::cbp_fp_kernel<S, 4><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
     else if (parts == 2)
         cbp::cbp_fp_kernel<S, 2><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
@@ -301,6 +307,9 @@ int launch_fp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* img,
                                                                          batch);
     ++g_launches;
     cbp::FPParams Pm;
+    Pm.split = 0x7fffffff;
+    Pm.view_begin2 = 0;
+    Pm.sino2 = nullptr;
     Pm.g = to_dev(g);
     Pm.t = t;
     Pm.pad = pad;
@@ -331,7 +340,8 @@ bool use_sym4(const cbp_geometry_t& g, int32_t batch, int32_t v0, int32_t nv)
 // stride 0: sino is the orbit layout [4][base_count][n_det]; stride n_views/4:
 // sino is the natural [n_views][n_det] layout (rows base_begin + i + q n_views/4)
 int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
-                   int32_t base_begin, int32_t base_count, cudaStream_t stream, int32_t stride = 0)
+                   int32_t base_begin, int32_t base_count, cudaStream_t stream, int32_t stride = 0,
+                   int32_t begin2 = 0, int32_t count2 = 0)
 {
     const int P = fp_pad_width(g);
     const int np = g.n + 2 * P;
@@ -344,6 +354,9 @@ int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     cbp::cbp_pad_sym4_kernel<<<pgrid, dim3(cbp::PAD_TILE, 8), 0, stream>>>(img, pad, padT, g.n, P, np);
     ++g_launches;
     cbp::FPParams Pm;
+    Pm.split = 0x7fffffff;
+    Pm.view_begin2 = 0;
+    Pm.sino2 = nullptr;
     Pm.g = to_dev(g);
     Pm.t = t;
     Pm.pad = pad;
@@ -356,7 +369,12 @@ int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     Pm.batch = 4;
     Pm.sym_stride = stride ? stride : base_count;
     Pm.sym_mode = 4;
-    rc = launch_fp_kernel<4>(Pm, base_count, 1, stream);
+    if (count2 > 0) {  // a second block of base views (natural layout only), same pad, same launch
+        Pm.split = base_count;
+        Pm.view_begin2 = begin2;
+        Pm.sino2 = sino + (size_t)begin2 * g.n_det;
+    }
+    rc = launch_fp_kernel<4>(Pm, base_count + (count2 > 0 ? count2 : 0), 1, stream);
     cudaFreeAsync(pad, stream);
     return rc;
 }
@@ -383,6 +401,9 @@ int launch_fp_sym8(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     cbp::cbp_pad_sym8_kernel<<<pgrid, dim3(cbp::PAD_TILE, 8), 0, stream>>>(img, pad, padT, g.n, P, np);
     ++g_launches;
     cbp::FPParams Pm;
+    Pm.split = 0x7fffffff;
+    Pm.view_begin2 = 0;
+    Pm.sino2 = nullptr;
     Pm.g = to_dev(g);
     Pm.t = t;
     Pm.pad = pad;
@@ -519,7 +540,10 @@ int launch_fp(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, f
 // balances the tail); small problems take as many groups as allowed.
 // Measured on the B200 at config 2 (256 tiles, 91 base views, 296 slots):
 // G = 3/4/5/6/8/12 -> BP 0.220/0.206/0.213/0.219/0.224/0.257 ms; the earlier
-// whole-wave score picked 8.  Each group has >= 8 views and the partial
+// whole-wave score picked 8.  Each group has >= 8 views (8 base views of a
+// symmetric launch: a small dihedral shard of 12 base views measured 0.093 /
+// 0.102 / 0.107 / 0.113 ms per pair with G = 1 / 2 / 3 / 4 -- the per-CTA
+// setup and the partial planes outweigh the fuller wave) and the partial
 // images are capped at 32 / slice_groups per slice.
 int bp_groups(const cbp_geometry_t& g, int32_t slice_groups, int32_t nv, int slots)
 {
@@ -1069,10 +1093,9 @@ int cbp_forward_dihedral(const cbp_geometry_t* g, const float* image, float* sin
     if (g->model == CBP_MODEL_MAG) return mag_dihedral(*g, t, image, sino, base_begin, base_count, 0, stream, true);
     // the 4 rotations of the base block, then those of its mirror images
     // N/4 - v (v = 0 and v = N/8 are their own mirror orbits)
-    if ((rc = launch_fp_sym4(*g, t, image, sino, base_begin, base_count, stream, q)) != CBP_OK) return rc;
+    // one pad and one launch for both blocks (the grid of a small shard is far short of a wave)
     const int lo = std::max(base_begin, 1), hi = std::min(base_begin + base_count, e);  // [lo, hi)
-    if (hi > lo) rc = launch_fp_sym4(*g, t, image, sino, q - hi + 1, hi - lo, stream, q);
-    return rc;
+    return launch_fp_sym4(*g, t, image, sino, base_begin, base_count, stream, q, q - hi + 1, hi > lo ? hi - lo : 0);
 }
 
 int cbp_back_dihedral(const cbp_geometry_t* g, const float* sino, float* image, int32_t base_begin,

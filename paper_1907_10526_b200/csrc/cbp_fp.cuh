@@ -39,6 +39,11 @@ struct FPParams {
     int np, P;          // padded side, pad width (>= max K)
     float* sino;        // [batch][view_count][n_det]
     int view_begin, view_count, batch;
+    // a second block of (base) views in the same launch: blockIdx.y >= split
+    // is view view_begin2 + (blockIdx.y - split), written through sino2
+    // (the dihedral shard's mirrored block; split = INT_MAX: none)
+    int split, view_begin2;
+    float* sino2;
     // > 0: 4-fold rotational symmetry (see cbp_pad_sym4_kernel): the S = 4
     // slices are the image rotated by 0, 90, 180, 270 degrees and slice q of
     // base view vl is view vl + q sym_stride of the single output sinogram
@@ -50,6 +55,9 @@ struct FPParams {
 };
 
 constexpr int FP_BLOCK = 128;
+// threads of an FP CTA: 128, or 32 PARTS when a ray group's lines are split
+// over more than 4 warps (small grids: view shards, small images)
+__host__ __device__ constexpr int fp_threads(int parts) { return parts <= 4 ? FP_BLOCK : 32 * parts; }
 constexpr int FP_KMAX_UNROLLED = 6;
 
 // ---- zero-padded (and transposed) image copies, S slices interleaved ------
@@ -223,8 +231,8 @@ struct FPRay {
 // four sat() arguments t.. = sat(z/C + ...) are formed directly from k
 // (u11 = z11/C + 1, u12 = u11 - tau'/C, u21 = u11 - A/C, u22 = u12 - A/C),
 // and the trapezoid bound r = A + tau' - z11 is affine in k too.
-// `out` holds the thread's S FP64 totals at stride FP_BLOCK (shared memory)
-template <int K, int MAB, int S, bool PRE>
+// `out` holds the thread's S FP64 totals at stride NT (shared memory)
+template <int K, int MAB, int S, bool PRE, int NT>
 __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, int np, int P,
                                         double* out)
 {
@@ -329,24 +337,24 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
         } else {
 #pragma unroll
             for (int q = 0; q < S; q += 2) {
-                out[q * FP_BLOCK] += (double)acc[q / 2].x + (double)acc[S / 2 + q / 2].x;
-                out[(q + 1) * FP_BLOCK] += (double)acc[q / 2].y + (double)acc[S / 2 + q / 2].y;
+                out[q * NT] += (double)acc[q / 2].x + (double)acc[S / 2 + q / 2].x;
+                out[(q + 1) * NT] += (double)acc[q / 2].y + (double)acc[S / 2 + q / 2].y;
             }
         }
     }
 }
 
-template <int K, int S, bool PRE>
+template <int K, int S, bool PRE, int NT>
 __device__ __forceinline__ void fp_walk_k(const FPRay& R, int mab, int i0, int i1, int n, int np,
                                           int P, double* out)
 {
-    if (mab == 1) fp_walk<K, 1, S, PRE>(R, i0, i1, n, np, P, out);
-    else if (mab == 2) fp_walk<K, 2, S, PRE>(R, i0, i1, n, np, P, out);
-    else fp_walk<K, 0, S, PRE>(R, i0, i1, n, np, P, out);
+    if (mab == 1) fp_walk<K, 1, S, PRE, NT>(R, i0, i1, n, np, P, out);
+    else if (mab == 2) fp_walk<K, 2, S, PRE, NT>(R, i0, i1, n, np, P, out);
+    else fp_walk<K, 0, S, PRE, NT>(R, i0, i1, n, np, P, out);
 }
 
 // generic K (wide bins relative to pixels): same arithmetic, runtime trip count
-template <int S>
+template <int S, int NT>
 __device__ void fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, int np, int P,
                                 double* out)
 {
@@ -380,7 +388,7 @@ __device__ void fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, in
             for (int q = 0; q < S; ++q) part[q] = fmaf(c[q], w, part[q]);
         }
 #pragma unroll
-        for (int q = 0; q < S; ++q) out[q * FP_BLOCK] += (double)part[q];
+        for (int q = 0; q < S; ++q) out[q * NT] += (double)part[q];
     }
 }
 
@@ -390,17 +398,21 @@ __device__ void fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, in
 // when the grid would otherwise be short of ~16 waves: the ragged last wave
 // of a 1.6-wave grid cost ~25 %.
 template <int S, int PARTS>
-__global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_fp_kernel(const FPParams P)
+__global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? 2 : (S == 1 ? 7 : (S == 4 ? 6 : 4)))
+    cbp_fp_kernel(const FPParams P)
 {
     const GeomDev& g = P.g;
-    constexpr int BINS = FP_BLOCK / PARTS;  // bins per CTA
+    constexpr int NT = fp_threads(PARTS);
+    constexpr int BINS = NT / PARTS;  // bins per CTA
     const int warp = threadIdx.x >> 5, part = warp % PARTS;
     const int jr = blockIdx.x * BINS + (warp / PARTS) * 32 + (threadIdx.x & 31);
     const bool valid = jr < g.n_det;
     const int j = valid ? jr : g.n_det - 1;
-    const int vl = blockIdx.y;
+    const bool second = (int)blockIdx.y >= P.split;
+    const int vl = second ? (int)blockIdx.y - P.split : (int)blockIdx.y;
     const int grp = blockIdx.z;  // slices grp S .. grp S + S - 1
-    const int v = P.view_begin + vl;
+    const int v = (second ? P.view_begin2 : P.view_begin) + vl;
+    float* const sino_out = second ? P.sino2 : P.sino;
     const int n = g.n;
 
     // ---- per-ray constants (FP64): Eq. 11 frame, Eq. 12 directions, Eq. 13 gain
@@ -464,11 +476,11 @@ __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_f
     const int whi = __reduce_max_sync(0xffffffffu, ihi);
     const int Kw = __reduce_max_sync(0xffffffffu, K);
 
-    __shared__ double sacc[S * FP_BLOCK];  // FP64 totals, [q][thread]
+    __shared__ double sacc[S * NT];  // FP64 totals, [q][thread]
     double* acc = sacc + threadIdx.x;
 #pragma unroll
     for (int q = 0; q < S; ++q)
-        acc[q * FP_BLOCK] = Kw > P.P ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;  // pad too thin: NaN
+        acc[q * NT] = Kw > P.P ? __longlong_as_double(0x7ff8000000000000ll) : 0.0;  // pad too thin: NaN
     int i0 = wlo, i1 = whi;
     if (PARTS > 1) {  // this warp's part of the lines: even lengths, because the walk takes
                       // lines in pairs (an odd range reads one line past its end -- harmless
@@ -510,26 +522,26 @@ __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_f
         const int mab_t = gj * dmax * (1.0 + 1e-6) < A ? 1 : (gj * dmin * (1.0 - 1e-6) > A ? 2 : 0);
         const int mab = __all_sync(0xffffffffu, mab_t == 1) ? 1 : (__all_sync(0xffffffffu, mab_t == 2) ? 2 : 0);
         switch (Kw) {
-            case 1: fp_walk_k<1, S, (S <= 2 || (S == 4 && PARTS > 1))>(R, mab, i0, i1, n, P.np, P.P, acc); break;
-            case 2: fp_walk_k<2, S, (S <= 2 || (S == 4 && PARTS > 1))>(R, mab, i0, i1, n, P.np, P.P, acc); break;
-            case 3: fp_walk_k<3, S, (S <= 2 || (S == 4 && PARTS > 1))>(R, mab, i0, i1, n, P.np, P.P, acc); break;
-            case 4: fp_walk_k<4, S, (S <= 2 || (S == 4 && PARTS > 1))>(R, mab, i0, i1, n, P.np, P.P, acc); break;
-            case 5: fp_walk_k<5, S, (S <= 2 || (S == 4 && PARTS > 1))>(R, mab, i0, i1, n, P.np, P.P, acc); break;
-            case 6: fp_walk_k<6, S, (S <= 2 || (S == 4 && PARTS > 1))>(R, mab, i0, i1, n, P.np, P.P, acc); break;
-            default: fp_walk_generic<S>(R, Kw, i0, i1, n, P.np, P.P, acc); break;
+            case 1: fp_walk_k<1, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 2: fp_walk_k<2, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 3: fp_walk_k<3, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 4: fp_walk_k<4, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 5: fp_walk_k<5, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 6: fp_walk_k<6, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            default: fp_walk_generic<S, NT>(R, Kw, i0, i1, n, P.np, P.P, acc); break;
         }
 #pragma unroll
-        for (int q = 0; q < S; ++q) acc[q * FP_BLOCK] *= h * h * inv_A;  // W = (h^2 / A) num / B
+        for (int q = 0; q < S; ++q) acc[q * NT] *= h * h * inv_A;  // W = (h^2 / A) num / B
     }
     if (PARTS > 1) {  // sum the parts in part order; the first part's warp writes
         __syncthreads();
         if (part != 0) return;
 #pragma unroll
         for (int q = 0; q < S; ++q) {
-            double t = acc[q * FP_BLOCK];
+            double t = acc[q * NT];
 #pragma unroll
-            for (int pp = 1; pp < PARTS; ++pp) t += acc[q * FP_BLOCK + pp * 32];
-            acc[q * FP_BLOCK] = t;
+            for (int pp = 1; pp < PARTS; ++pp) t += acc[q * NT + pp * 32];
+            acc[q * NT] = t;
         }
     }
     if (valid)
@@ -542,13 +554,13 @@ __global__ void __launch_bounds__(FP_BLOCK, S == 1 ? 7 : (S == 4 ? 6 : 4)) cbp_f
                 if (m && (v == 0 || 8 * v == N)) continue;  // mirrored frame repeats a rotation
                 const int view = ((m ? N - v : v) + qq * (N / 4)) % N;
                 const int bin = m ? g.n_det - 1 - j : j;
-                dst = P.sino + (size_t)view * g.n_det + bin;
+                dst = sino_out + (size_t)view * g.n_det + bin;
             } else if (P.sym_stride > 0) {
-                dst = P.sino + ((size_t)vl + (size_t)q * P.sym_stride) * g.n_det + j;
+                dst = sino_out + ((size_t)vl + (size_t)q * P.sym_stride) * g.n_det + j;
             } else if (b < P.batch) {
-                dst = P.sino + ((size_t)b * P.view_count + vl) * g.n_det + j;
+                dst = sino_out + ((size_t)b * P.view_count + vl) * g.n_det + j;
             }
-            if (dst) *dst = (float)acc[q * FP_BLOCK];
+            if (dst) *dst = (float)acc[q * NT];
         }
 }
 
