@@ -213,10 +213,19 @@ def main():
     from paper_1907_10526_b200.sharded import make_shard, view_shard
 
     assert args.warmup >= 3, "at least 3 warm-up steps"
+    # CBP_BENCH_BACKEND=gloo (a logic check, not a measurement): the ranks may
+    # share GPUs (device = local rank mod the device count) and the BP partials
+    # are summed through gloo, so the N > 1 code path runs on a one-GPU box
+    backend = os.environ.get("CBP_BENCH_BACKEND", "nccl")
+    if backend == "gloo":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     g = W.geometry(args.config)
     n, ns = g["n"], g["n_det"]
     batch = W.BATCH[args.config]
@@ -479,6 +488,8 @@ def main():
             "gpu_launches": launches,
             "clocks": clk,
         }
+        if backend == "gloo" and world > 1:
+            line["note"] = "CBP_BENCH_BACKEND=gloo: a logic check of the N > 1 path (ranks may share a GPU), not a measurement"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
