@@ -13,6 +13,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "cbp_bp.cuh"
@@ -26,6 +27,26 @@
 namespace {
 
 std::atomic<uint64_t> g_launches{0};
+
+// launch with programmatic dependent launch allowed (cbp_common.cuh): the
+// kernel may start during its stream predecessor's tail; CBP_NO_PDL turns it off
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args)
+{
+    static const bool off = getenv("CBP_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
 
@@ -279,13 +300,13 @@ int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stre
     if (force == 1 || force == 2 || force == 4 || force == 8) parts = force;
     const dim3 grid((unsigned)(ctas(parts) / ((int64_t)views * groups)), views, groups);
     if (parts == 8)
-        cbp::cbp_fp_kernel<S, 8><<<grid, cbp::fp_threads(8), 0, stream>>>(Pm);
+        launch_pdl(cbp::cbp_fp_kernel<S, 8>, grid, dim3(cbp::fp_threads(8)), 0, stream, Pm);
     else if (parts == 4)
-        cbp::cbp_fp_kernel<S, 4><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
+        launch_pdl(cbp::cbp_fp_kernel<S, 4>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
     else if (parts == 2)
-        cbp::cbp_fp_kernel<S, 2><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
+        launch_pdl(cbp::cbp_fp_kernel<S, 2>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
     else
-        cbp::cbp_fp_kernel<S, 1><<<grid, cbp::FP_BLOCK, 0, stream>>>(Pm);
+        launch_pdl(cbp::cbp_fp_kernel<S, 1>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
     ++g_launches;
     return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
 }
@@ -698,7 +719,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     fprintf(stderr, "launch_bp S=%d G=%d vpg=%d grid=%d,%d,%d smem=%zu\n", S, G, vpg, grid.x, grid.y,
             grid.z, smem);
 #endif
-    cbp::cbp_bp_kernel<S><<<grid, cbp::BP_THREADS, smem, stream>>>(P);
+    launch_pdl(cbp::cbp_bp_kernel<S>, grid, dim3(cbp::BP_THREADS), smem, stream, P);
     ++g_launches;
 #ifdef CBP_DEBUG_CHECKS
     fprintf(stderr, "bp kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
@@ -710,8 +731,8 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
         const int planes = sym ? G * batch : G;
         const int outs = sym ? images : 1;  // symmetric batch: one reduction per image
         const int blocks = (int)std::min<size_t>((count / 4 + 255) / 256, (size_t)sms * 8 / outs + 1);
-        cbp::cbp_reduce_kernel<<<dim3(std::max(blocks, 1), outs), 256, 0, stream>>>(part, img, count, planes,
-                                                                                   mc ? 2 : (accumulate ? 1 : 0));
+        launch_pdl(cbp::cbp_reduce_kernel, dim3(std::max(blocks, 1), outs), dim3(256), 0, stream,
+                   (const float*)part, img, count, planes, mc ? 2 : (accumulate ? 1 : 0));
         ++g_launches;
         cudaFreeAsync(part, stream);
     }

@@ -550,6 +550,8 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
     };
 
     for (int i = tid; i < S * BP_TILE * (BP_TILE + 1); i += BP_THREADS) acc_s[i] = 0;
+    griddep_launch_dependents();  // the reduce may launch into this grid's tail
+    griddep_wait();               // the sinogram, headers and pool memory are ready
 
     if constexpr (STAGE) {
         if (nchunks > 0) {
@@ -761,6 +763,7 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
 __global__ void cbp_reduce_kernel(const float* __restrict__ part, float* __restrict__ out,
                                   size_t count, int groups, int accumulate)
 {
+    griddep_wait();  // the BP's partial planes
     part += (size_t)blockIdx.y * groups * count;
     out += (size_t)blockIdx.y * count;
     const size_t stride = (size_t)gridDim.x * blockDim.x;

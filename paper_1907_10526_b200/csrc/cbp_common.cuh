@@ -122,6 +122,15 @@ __device__ __forceinline__ void mc_red_add4(float4* mc, float4 v)
                  : "memory");
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-stream-serialization attribute may start while its stream
+// predecessor finishes; it runs griddep_wait() before touching anything the
+// predecessor produced (or memory the predecessor's stream-ordered frees may
+// hand out).  griddep_launch_dependents() lets the NEXT kernel launch once
+// every CTA of this grid has called it.  Both are no-ops without the attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 __device__ __forceinline__ float2 rcp2(float2 b) { return make_float2(rcp_approx(b.x), rcp_approx(b.y)); }
 
 }  // namespace cbp

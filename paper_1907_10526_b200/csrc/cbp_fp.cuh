@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_kernel(const float* __re
                                                                float* __restrict__ padT, int n,
                                                                int P, int np, int batch)
 {
+    griddep_launch_dependents();  // the FP may launch and set up its rays meanwhile
     __shared__ float tile[PAD_TILE][PAD_TILE + 1][S];
     const int grp = blockIdx.z;
     const int r0 = blockIdx.y * PAD_TILE, c0 = blockIdx.x * PAD_TILE;
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym4_kernel(const float*
                                                                     float* __restrict__ padT, int n,
                                                                     int P, int np)
 {
+    griddep_launch_dependents();  // the FP may launch and set up its rays meanwhile
     __shared__ float tile[PAD_TILE][PAD_TILE + 1][4];
     const int r0 = blockIdx.y * PAD_TILE, c0 = blockIdx.x * PAD_TILE;
     for (int rr = threadIdx.y; rr < PAD_TILE; rr += 8) {
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym8_kernel(const float*
                                                                     float* __restrict__ padT, int n,
                                                                     int P, int np)
 {
+    griddep_launch_dependents();  // the FP may launch and set up its rays meanwhile
     __shared__ float tile[PAD_TILE][PAD_TILE + 1][8];
     const int r0 = blockIdx.y * PAD_TILE, c0 = blockIdx.x * PAD_TILE;
     for (int rr = threadIdx.y; rr < PAD_TILE; rr += 8) {
@@ -489,6 +492,8 @@ __global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? 2 : (S == 1 ? 7
         i0 = wlo + part * L;
         i1 = part == PARTS - 1 ? whi : min(whi, i0 + L - 1);
     }
+    griddep_launch_dependents();  // the BP may launch into this grid's tail
+    griddep_wait();               // the padded image (and its pool memory) is ready
     if (i0 <= i1 && Kw <= P.P) {
         FPRay R;
         // lower support edge on line i: q*(i) - sig_q, as 32.32 fixed point from line i0
