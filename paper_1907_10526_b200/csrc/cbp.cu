@@ -294,9 +294,11 @@ int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stre
     };
     int parts = 1;
     while (parts < 4 && ctas(parts) < 16 * slots) parts *= 2;  // config 3 (6.5 waves): parts 4 -4 %
-    // under one wave of 4-part CTAs (a view shard, a small image): 8 warps per
+    // under two waves of 4-part CTAs (a view shard, a small image): 8 warps per
     // ray group in 256-thread CTAs, each walking an eighth of the lines
-    if (parts == 4 && ctas(4) < slots) parts = 8;
+    // (measured at a W = 8 dihedral shard: config 2 0.092 -> 0.085 ms, config 3
+    // 0.403 -> 0.384 ms; 16 parts in 512-thread CTAs: no further gain)
+    if (parts == 4 && ctas(4) < 2 * slots) parts = 8;
     if (force == 1 || force == 2 || force == 4 || force == 8) parts = force;
     const dim3 grid((unsigned)(ctas(parts) / ((int64_t)views * groups)), views, groups);
     if (parts == 8)
