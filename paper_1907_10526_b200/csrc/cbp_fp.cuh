@@ -406,6 +406,14 @@ __global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? 2 : (S == 1 ? 7
 {
     const GeomDev& g = P.g;
     constexpr int NT = fp_threads(PARTS);
+    // PDL: with one part per ray (long walks, large grids) the wait comes first
+    // -- placed after the set-up it cost the walk 2.4 % at config 5 (code
+    // generation); with line parts (short walks) the set-up overlaps the pad's
+    // tail (config 2: 1.5 % faster)
+    if constexpr (PARTS == 1) {
+        griddep_wait();
+        griddep_launch_dependents();
+    }
     constexpr int BINS = NT / PARTS;  // bins per CTA
     const int warp = threadIdx.x >> 5, part = warp % PARTS;
     const int jr = blockIdx.x * BINS + (warp / PARTS) * 32 + (threadIdx.x & 31);
@@ -492,8 +500,10 @@ __global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? 2 : (S == 1 ? 7
         i0 = wlo + part * L;
         i1 = part == PARTS - 1 ? whi : min(whi, i0 + L - 1);
     }
-    griddep_launch_dependents();  // the BP may launch into this grid's tail
-    griddep_wait();               // the padded image (and its pool memory) is ready
+    if constexpr (PARTS > 1) {
+        griddep_launch_dependents();  // the BP may launch into this grid's tail
+        griddep_wait();               // the padded image (and its pool memory) is ready
+    }
     if (i0 <= i1 && Kw <= P.P) {
         FPRay R;
         // lower support edge on line i: q*(i) - sig_q, as 32.32 fixed point from line i0
