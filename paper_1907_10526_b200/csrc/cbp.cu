@@ -505,11 +505,18 @@ int launch_mag(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, 
         P.image = img;
         P.sino = sino;
         const int bins = (g.n_det + cbp::MAG_FP_BLOCK - 1) / cbp::MAG_FP_BLOCK;
+        static const bool warp_walk = getenv("CBP_MAG_FP_BLOCKWALK") == nullptr;  // A/B knob
         if (sym4) {
             P.view_count = g.n_views / 4;
-            cbp::cbp_mag_fp_kernel<4><<<dim3(bins, g.n_views / 4, 1), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
+            if (warp_walk)
+                cbp::cbp_mag_fpw_kernel<4><<<dim3(bins, g.n_views / 4, 1), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
+            else
+                cbp::cbp_mag_fp_kernel<4><<<dim3(bins, g.n_views / 4, 1), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
         } else {
-            cbp::cbp_mag_fp_kernel<1><<<dim3(bins, nv, batch), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
+            if (warp_walk)
+                cbp::cbp_mag_fpw_kernel<1><<<dim3(bins, nv, batch), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
+            else
+                cbp::cbp_mag_fp_kernel<1><<<dim3(bins, nv, batch), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
         }
     } else {  // BP: img is the output image, sino the input sinogram
         P.sino_in = sino;

@@ -386,6 +386,131 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
     }
 }
 
+// FP, warp-per-line form (no CTA barriers in the walk): the CTA's 4 warps
+// take the image lines round-robin; a warp stages the footprints of its
+// line's band in its own shared memory (each footprint once per CTA, as in
+// cbp_mag_fp_kernel) and each lane sums the candidates of its 4 bins
+// j0 + lane + 32 r; the warps' partial sums are added in warp order at the end.
+constexpr int MAG_FPW_STAGE = 160;  // staged pixels per warp and pass
+
+template <int F>
+__global__ void __launch_bounds__(MAG_FP_BLOCK, 5) cbp_mag_fpw_kernel(MagParams p)
+{
+    constexpr int NW = MAG_FP_BLOCK / 32, R = MAG_FP_BLOCK / 32;  // warps; bins per lane
+    __shared__ MagStaged<F> st_all[NW][MAG_FPW_STAGE];
+    __shared__ float comb[NW][F][MAG_FP_BLOCK];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    MagStaged<F>* st = st_all[warp];
+    const GeomDev& g = p.g;
+    const int j0 = blockIdx.x * MAG_FP_BLOCK;
+    const int jl = min(j0 + MAG_FP_BLOCK, g.n_det) - 1;
+    const int vl = blockIdx.y, b = blockIdx.z;
+    const double2 cs = p.view_cs[p.view_begin + vl];
+    const double cu = cs.x, su = cs.y;
+    const float B = (float)g.tau;
+    const double sm = 0.5 * (mag_bin_s(g, j0) + mag_bin_s(g, jl));
+    double dx, dy;
+    if (g.parallel) {
+        dx = -cu;
+        dy = -su;
+    } else if (g.arc) {
+        double sg, cg;
+        sincos(sm / g.sdd, &sg, &cg);
+        dx = -cg * cu - sg * su;
+        dy = -cg * su + sg * cu;
+    } else {
+        dx = -g.sdd * cu - sm * su;
+        dy = -g.sdd * su + sm * cu;
+    }
+    const bool rows = fabs(dy) >= fabs(dx);
+    const int n = g.n;
+    const MagBand tband = mag_band(mag_edge(g, cu, su, mag_bin_s(g, j0) - p.sigma_max),
+                                   mag_edge(g, cu, su, mag_bin_s(g, jl) + p.sigma_max), rows, n);
+    double s[R];
+    MagBand band[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        s[r] = mag_bin_s(g, min(j0 + lane + 32 * r, g.n_det - 1));
+        band[r] = mag_band(mag_edge(g, cu, su, s[r] - p.sigma_max), mag_edge(g, cu, su, s[r] + p.sigma_max), rows, n);
+    }
+    const float* img = p.image + (size_t)b * n * n;
+    float acc[R][F];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int q = 0; q < F; ++q) acc[r][q] = 0.0f;
+    for (int l = warp; l < n; l += NW) {
+        int I0, I1;
+        mag_band_range(tband, l, n, I0, I1);
+        for (int base = I0; base <= I1; base += MAG_FPW_STAGE) {
+            const int cnt = min(MAG_FPW_STAGE, I1 - base + 1);
+            for (int t = lane; t < cnt; t += 32) {
+                const int i = base + t;
+                const int row = rows ? l : i, col = rows ? i : l;
+                const double kx = ((double)col - g.c0) * g.h, ky = (g.c0 - (double)row) * g.h;
+                const MagFootprint fp = mag_footprint(g, cu, su, kx, ky);
+                MagStaged<F> m;
+                m.P = fp.P;
+                m.A = fp.A;
+                m.invC = fp.invC;
+                m.w1 = fp.w1;
+                m.zoff = fp.zoff;
+                m.minAB = fp.minAB;
+                m.hC = fp.hC;
+                m.sigma = fp.sigma;
+                m.wscale = fp.wscale;
+#pragma unroll
+                for (int q = 0; q < F; ++q) {
+                    int rr = row, cc = col;
+                    mag_rot(n, q, rr, cc);
+                    m.val[q] = __ldg(img + (size_t)rr * n + cc);
+                }
+                st[t] = m;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                int i0, i1;
+                mag_band_range(band[r], l, n, i0, i1);
+                const int a = max(i0, base), e = min(i1, base + cnt - 1);
+                for (int q = a; q <= e; ++q) {
+                    const MagStaged<F>& m = st[q - base];
+                    MagFootprint fp;
+                    fp.P = m.P;
+                    fp.A = m.A;
+                    fp.invC = m.invC;
+                    fp.w1 = m.w1;
+                    fp.zoff = m.zoff;
+                    fp.minAB = m.minAB;
+                    fp.hC = m.hC;
+                    fp.sigma = m.sigma;
+                    fp.wscale = m.wscale;
+                    const float wgt = mag_weight_x(fp, (float)(s[r] - fp.P), B);
+#pragma unroll
+                    for (int f = 0; f < F; ++f) acc[r][f] = __fmaf_rn(m.val[f], wgt, acc[r][f]);
+                }
+            }
+            __syncwarp();
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int f = 0; f < F; ++f) comb[warp][f][lane + 32 * r] = acc[r][f];
+    __syncthreads();
+    const int jj = threadIdx.x, j = j0 + jj;  // one output bin per thread, warps summed in order
+    if (j >= g.n_det) return;
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+        float t = comb[0][f][jj];
+        for (int w = 1; w < NW; ++w) t += comb[w][f][jj];
+        if (F == 1)
+            p.sino[((size_t)b * p.view_count + vl) * g.n_det + j] = t;
+        else
+            p.sino[((size_t)(p.view_begin + vl) + (size_t)f * (g.n_views / 4)) * g.n_det + j] = t;
+    }
+}
+
 // BP: c[b][k] = sum_{v, j} y[b][v][j] W(v, j, k) over the bins of k's footprint
 // (|j - P/Delta_s - c_s| < sigma/Delta_s, widened by 1e-3 bin; the exact test decides).
 // F = 8 (one image, a full scan, N_v % 4 == 0, n even): the dihedral group of
