@@ -272,7 +272,10 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
             const float2 f = make_float2((float)fla, (float)flb);
             float2 B0 = __ffma2_rn(f, make_float2(R.btq, R.btq),
                                    __ffma2_rn(fi, make_float2(R.dB, R.dB), make_float2(R.Be0, R.Be0)));
-            B0 = make_float2(fmaxf(B0.x, 1e-30f), fmaxf(B0.y, 1e-30f));  // rays that miss: keep finite
+            // (no clamp here: tau' is affine along the line, and the first candidate
+            // may lie in the zero border behind a close source with tau' < 0 --
+            // clamping it shifted every later candidate's tau'; only the
+            // reciprocal below is kept finite)
             fi = __fadd2_rn(fi, make_float2(2.0f, 2.0f));
             float2 z0 = __ffma2_rn(f, make_float2(R.bqs, R.bqs), make_float2(R.z0c, R.z0c));
             z0 = __ffma2_rn(make_float2(0.5f, 0.5f), B0, z0);                       // z11
@@ -321,11 +324,15 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
                 const float2 M2 = make_float2(fmaxf(fmin3(z11.x, ma, r.x), 0.0f),
                                               fmaxf(fmin3(z11.y, mb, r.y), 0.0f));
                 const float2 num = __ffma2_rn(make_float2(R.hC, R.hC), T, M2);
+                // tau' > 0 at every pixel a ray's support reaches; candidates in the zero
+                // border behind a close source can have tau' <= 0: keep 1/tau' finite
+                // (their image values are 0)
+                const float2 iB = rcp2(make_float2(fmaxf(B.x, 1e-30f), fmaxf(B.y, 1e-30f)));
                 if constexpr (S == 1) {
-                    const float2 cw = __fmul2_rn(make_float2(ca[0], cb[0]), rcp2(B));
+                    const float2 cw = __fmul2_rn(make_float2(ca[0], cb[0]), iB);
                     acc[0] = __ffma2_rn(cw, num, acc[0]);
                 } else {  // one weight, S slices
-                    const float2 w = __fmul2_rn(num, rcp2(B));
+                    const float2 w = __fmul2_rn(num, iB);
 #pragma unroll
                     for (int q = 0; q < S; q += 2) {
                         acc[q / 2] = __ffma2_rn(make_float2(ca[q], ca[q + 1]), make_float2(w.x, w.x), acc[q / 2]);
@@ -371,7 +378,7 @@ __device__ void fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, in
             : "+r"(flo), "+r"(fhi) : "r"(R.mlo), "r"(R.mhi));
         const float* p = R.base + ((size_t)(i + P) * np + (qc + P)) * S;
         const float ff = (float)fl;
-        const float B0 = fmaxf(fmaf(ff, R.btq, fmaf((float)i, R.dB, R.Be0)), 1e-30f);
+        const float B0 = fmaf(ff, R.btq, fmaf((float)i, R.dB, R.Be0));  // affine: no clamp (see fp_walk)
         const float z0 = fmaf(0.5f, B0, fmaf(ff, R.bqs, R.z0c));
         float part[S];
 #pragma unroll
@@ -384,7 +391,7 @@ __device__ void fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, in
             const float w1 = fmaf(-B, R.invC, 1.0f);
             const float2 num = cnsf_num2(make_float2(z11, z11), make_float2(z21, z21),
                                          make_float2(B, B), make_float2(w1, w1), R.A, R.invC, R.hC);
-            const float w = num.x * rcp_approx(B);
+            const float w = num.x * rcp_approx(fmaxf(B, 1e-30f));
             float c[S];
             ld_pix<S>(p + k * S, c);
 #pragma unroll

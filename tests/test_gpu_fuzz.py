@@ -46,7 +46,11 @@ def draw(seed):
     return g, batch, v0, nv, rng
 
 
-@pytest.mark.parametrize("seed", range(160))
+# 248 and 665 found a bug (fixed): with a source ~2 field radii away and bins
+# wider than 2 pixels, the first FP candidate of a line can sit in the zero
+# border behind the source with tau' < 0, and clamping it shifted tau' of
+# every later candidate on the line (1 % errors in a few views)
+@pytest.mark.parametrize("seed", list(range(160)) + [248, 665])
 def test_random_scanner_parity(torch_cuda, seed):
     g, batch, v0, nv, rng = draw(seed)
     assert cbp.validate(g) == cbp.CBP_OK, g
