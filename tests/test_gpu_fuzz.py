@@ -39,6 +39,10 @@ def draw(seed):
         n_det = max(1, min(n_det, int(2.9 * sdd / pitch) - 2))
     g = dict(n=n, pixel=h, n_views=n_views, n_det=n_det, det_pitch=pitch, det_width=width,
              sid=sid if kind != 1 else 0.0, sdd=sdd if kind != 1 else 0.0, kind=kind, model=model)
+    if cbp.validate(g) != cbp.CBP_OK:  # rare draws: a bin wider than 2 D_ps, or arc bins past 90 degrees
+        g["det_width"] = min(width, 1.9 * sdd) if kind != 1 else width
+        while kind == 2 and g["n_det"] > 1 and cbp.validate(g) != cbp.CBP_OK:
+            g["n_det"] -= 1
     batch = int(rng.choice([1, 1, 1, 2, 3, 5]))
     full = rng.random() < 0.6
     v0 = 0 if full else int(rng.integers(0, n_views))
@@ -58,10 +62,15 @@ def test_random_scanner_parity(torch_cuda, seed):
     imgs = W.random_image(n, 500 + seed, batch=batch) if batch > 1 else W.random_image(n, 500 + seed)
     what = f"seed {seed} {g} batch {batch} views {v0}+{nv}"
     want = O.forward(g, imgs, view_begin=v0, view_count=nv)
+    got = _fp(torch_cuda, g, imgs, view_begin=v0, view_count=nv)
     if np.abs(want).max() == 0.0:  # the bins miss the image entirely: exact zeros
-        assert not _fp(torch_cuda, g, imgs, view_begin=v0, view_count=nv).any(), what
+        assert not got.any(), what
+    elif np.abs(want).max() < 1e-3 * g["pixel"]:
+        # only support-edge tails reach the bins (max|y| far below a pixel's chord):
+        # the max-normalised metric is meaningless; FP32's absolute accuracy is the bar
+        assert np.abs(got - want).max() <= 1e-6 * g["pixel"], what
     else:
-        _assert_parity(_fp(torch_cuda, g, imgs, view_begin=v0, view_count=nv), want, "FP " + what)
+        _assert_parity(got, want, "FP " + what)
     y = W.random_sino(nv, g["n_det"], 600 + seed, batch=batch) if batch > 1 else \
         W.random_sino(nv, g["n_det"], 600 + seed)
     want_b = O.back(g, y, view_begin=v0)

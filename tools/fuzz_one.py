@@ -1,7 +1,7 @@
-"""Debug probe for fuzz seeds: the GPU FP of a single view against the oracle,
-with the bin width varied across the K = 6 / 7 boundary of the FP's
-candidates per line (K > 6 takes the generic walk)."""
+"""Debug probe for a fuzz seed: FP and BP of the CUDA path against the oracle,
+per view (FP) and overall (BP), for batch 1 and the seed's batch."""
 import sys
+
 import numpy as np
 import torch
 
@@ -11,13 +11,16 @@ import paper_1907_10526_b200 as cbp  # noqa: E402
 import workloads as W  # noqa: E402
 from tests.test_gpu_fuzz import draw  # noqa: E402
 
-g, batch, v0, nv, rng = draw(int(sys.argv[1]) if len(sys.argv) > 1 else 665)
+seed = int(sys.argv[1]) if len(sys.argv) > 1 else 1670
+g, batch, v0, nv, rng = draw(seed)
+print(g, batch, v0, nv)
 n = g["n"]
-img = W.random_image(n, 1) + 0.5
-for tw in (2.0, 3.0, 3.5, g["det_width"] / g["det_pitch"] * g["det_pitch"] / g["det_pitch"], 2.4, 2.2):
-    gg = dict(g, det_width=tw * g["det_pitch"])
-    for v in (4, 5, 10):
-        want = O.forward(gg, img, view_begin=v, view_count=1)[0]
-        got = cbp.forward(gg, torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).cuda(),
-                          view_begin=v, view_count=1).cpu().numpy()[0]
-        print(f"tau/pitch {tw:.3f} view {v} rel {np.abs(got - want).max() / np.abs(want).max():.2e}", got, want)
+imgs = W.random_image(n, 500 + seed, batch=batch) if batch > 1 else W.random_image(n, 500 + seed)[None]
+for bb in sorted({1, batch}):
+    x = np.ascontiguousarray(imgs[:bb], dtype=np.float32)
+    want = O.forward(g, x, view_begin=v0, view_count=nv)
+    got = cbp.forward(g, torch.from_numpy(x).cuda(), view_begin=v0, view_count=nv).cpu().numpy()
+    d = np.abs(got - want).max(axis=(0, 2)) / np.abs(want).max()
+    print("FP batch", bb, "bad views", [(int(v), float(d[v])) for v in np.where(d > 1e-4)[0]][:12])
+    for v in np.where(d > 1e-4)[0][:3]:
+        print("   view", int(v), "got", got[0, v], "want", want[0, v])
