@@ -269,8 +269,8 @@ int fp_pad_width(const cbp_geometry_t& g)
 }
 
 // FP launch: PARTS warps per ray (cbp_fp_kernel) while the grid is short of
-// ~16 waves of resident CTAs (config 2: 1.6 waves -> parts 4, FP -17 %;
-// config 3: 6.5 waves -> parts 4, -4 %; config 4 / 5: enough waves)
+// ~8 waves of resident CTAs (config 2: 1.6 waves -> parts 4, FP -17 %;
+// config 3: 6.5 waves -> parts 2; config 4 / 5: enough waves)
 template <int S>
 int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stream)
 {
@@ -293,7 +293,9 @@ int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stre
         return (int64_t)((Pm.g.n_det + bins - 1) / bins) * views * groups;
     };
     int parts = 1;
-    while (parts < 4 && ctas(parts) < 16 * slots) parts *= 2;  // config 3 (6.5 waves): parts 4 -4 %
+    // fewer than 8 waves: split the lines (config 2: 4 parts, 0.181 vs 0.194 ms with 2;
+    // config 3: 2 parts, 1.228 vs 1.245 ms with 4; 16 waves picked 4 there)
+    while (parts < 4 && ctas(parts) < 8 * slots) parts *= 2;
     // under two waves of 4-part CTAs (a view shard, a small image): 8 warps per
     // ray group in 256-thread CTAs, each walking an eighth of the lines
     // (measured at a W = 8 dihedral shard: config 2 0.092 -> 0.085 ms, config 3
