@@ -20,13 +20,16 @@
 // x = s_j - P(k), rounded to FP32 from FP64.
 //
 // FP: a CTA per (slice, view, 128-bin tile) walks the image lines (rows or
-// columns, whichever the tile's rays cross more steeply); per line it stages
-// the footprints of the pixels the tile's band covers in shared memory (each
-// computed once), and each thread (bin) sums over the index interval of its
-// own band -- no atomics, a fixed order.  BP: one thread per (slice, pixel)
-// gathers over views and the bins of its footprint.  Both use mag_footprint
-// and mag_weight; x differs only by the FP64 rounding of s_j (direct in the
-// FP, incremental in the BP), far below FP32's.
+// columns, whichever the tile's rays cross more steeply); per line the
+// footprints of the pixels the tile's band covers are staged in shared
+// memory (each computed once) and each bin sums over the index interval of
+// its own band -- no atomics, a fixed order.  cbp_mag_fpw_kernel (default)
+// gives the lines to the CTA's warps round-robin with warp-private staging;
+// cbp_mag_fp_kernel stages each line for the whole CTA.  BP: threads per
+// (slice, pixel) -- or per pixel of a symmetry domain and its 4 / 8 frames
+// -- gather over views and the bins of the footprint.  All use mag_footprint
+// and mag_weight_x; x differs only by the FP64 rounding of s_j (direct in
+// the FP, incremental in the BP), far below FP32's.
 #pragma once
 
 #include "cbp_common.cuh"
