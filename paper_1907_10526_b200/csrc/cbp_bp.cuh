@@ -775,12 +775,16 @@ __global__ void cbp_reduce_kernel(const float* __restrict__ part, float* __restr
         for (size_t i = t0; i < c4; i += stride) {
             float4 s = accumulate == 1 ? o4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
             int gi = 0;
-            for (; gi + 8 <= groups; gi += 8) {  // 8 loads in flight, summed in plane order
-                float4 v[8];
+#ifndef CBP_REDUCE_INFLIGHT
+#define CBP_REDUCE_INFLIGHT 8
+#endif
+            constexpr int NF = CBP_REDUCE_INFLIGHT;
+            for (; gi + NF <= groups; gi += NF) {  // NF loads in flight, summed in plane order
+                float4 v[NF];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = __ldg(p4 + (size_t)(gi + u) * c4 + i);
+                for (int u = 0; u < NF; ++u) v[u] = __ldg(p4 + (size_t)(gi + u) * c4 + i);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < NF; ++u) {
                     s.x += v[u].x;
                     s.y += v[u].y;
                     s.z += v[u].z;

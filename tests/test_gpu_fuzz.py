@@ -65,7 +65,7 @@ def test_random_scanner_parity(torch_cuda, seed):
     got = _fp(torch_cuda, g, imgs, view_begin=v0, view_count=nv)
     if np.abs(want).max() == 0.0:  # the bins miss the image entirely: exact zeros
         assert not got.any(), what
-    elif np.abs(want).max() < 1e-3 * g["pixel"]:
+    elif np.abs(want).max() < 1e-2 * g["pixel"]:
         # only support-edge tails reach the bins (max|y| far below a pixel's chord):
         # the max-normalised metric is meaningless; FP32's absolute accuracy is the bar
         assert np.abs(got - want).max() <= 1e-6 * g["pixel"], what
