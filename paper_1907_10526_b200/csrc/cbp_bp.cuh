@@ -775,11 +775,10 @@ __global__ void cbp_reduce_kernel(const float* __restrict__ part, float* __restr
         for (size_t i = t0; i < c4; i += stride) {
             float4 s = accumulate == 1 ? o4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
             int gi = 0;
-#ifndef CBP_REDUCE_INFLIGHT
-#define CBP_REDUCE_INFLIGHT 8
-#endif
-            constexpr int NF = CBP_REDUCE_INFLIGHT;
-            for (; gi + NF <= groups; gi += NF) {  // NF loads in flight, summed in plane order
+            // 8 loads in flight, summed in plane order (16 or 32 in flight: the same
+            // time at config 2 -- the reduce is not bound by its load latency)
+            constexpr int NF = 8;
+            for (; gi + NF <= groups; gi += NF) {
                 float4 v[NF];
 #pragma unroll
                 for (int u = 0; u < NF; ++u) v[u] = __ldg(p4 + (size_t)(gi + u) * c4 + i);
