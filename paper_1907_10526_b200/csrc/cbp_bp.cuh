@@ -154,8 +154,13 @@ __device__ void bp_view_header(const GeomDev& g, const Tables& t, int v, double 
         const float dmin = fd - fabsf(dx) * (hcx + 0.5f) - fabsf(dy) * (hcy + 0.5f);
         const double dist_a = sqrt(delta * delta + kae * kae);
         const float sigma = 0.5f * (h * 1.41421356f + (float)(2.0 * tan(0.5 * g.tau / g.sdd)) * ((float)dist_a + Rt));
-        // |gamma - gamma(k)| < asin(sigma / |k - p|) <= 1.01 sigma / delta(k); den = delta(k) <= fd + Rt
-        const float cW = 1.01f * sigma / (float)dgam + E * (fd + Rt);
+        // |gamma - gamma(k)| < asin(sigma / |k - p|) <= asin(x), x = sigma / delta(k)
+        // <= x / sqrt(1 - x^2) (x < 1; x >= 1: any angle) -- the small-angle 1.01 x
+        // undercounts for a source within a few pixels (found by tools/fuzz_wide.py);
+        // den = delta(k) <= fd + Rt
+        const float xs = sigma / fmaxf(dmin, 1e-30f);
+        const float fac = xs < 0.999f ? fmaxf(1.01f, rsqrtf(1.0f - xs * xs)) * 1.0001f : 1e7f;
+        const float cW = fac * sigma / (float)dgam + E * (fd + Rt);
         const float urel = (float)(uaa - jaa);
         const float jsh = (float)jaa;
         const float jl = fmaxf(0.0f, floorf(jsh + urel + umin * sc - cW / dmin - 0.01f));
