@@ -277,10 +277,11 @@ double orc_footprint(const orc_geometry* g, double theta, double s, const double
  * pixel's detector-integrated chord length: integral chord ds = integral over
  * the pixel of (ds / d(angle)) / |x - p| dA (ds / d(angle) = L^2 / D_ps on the
  * flat detector, D_ps on the arc; 1 in parallel beam), taken at the centre. */
-static double weight_mag_f(const orc_geometry* g, const double u[2], const double e[2],
-                           const double p[2], double s, const double k[2])
+/* the linearised projection of pixel k (model 1): centre sk = P(k), gradient
+ * of P at k, and the chord-mass factor */
+static void mag_linear_f(const orc_geometry* g, const double u[2], const double e[2], const double p[2],
+                         const double k[2], double* sk_out, double grad_out[2], double* scale_out)
 {
-    const double h = g->pixel;
     double sk, grad[2], scale;
     if (g->kind == 1) {
         sk = dot2(k, e);
@@ -305,6 +306,18 @@ static double weight_mag_f(const orc_geometry* g, const double u[2], const doubl
             scale = (g->sdd * g->sdd + sk * sk) / (g->sdd * rk);
         }
     }
+    *sk_out = sk;
+    grad_out[0] = grad[0];
+    grad_out[1] = grad[1];
+    *scale_out = scale;
+}
+
+static double weight_mag_f(const orc_geometry* g, const double u[2], const double e[2],
+                           const double p[2], double s, const double k[2])
+{
+    const double h = g->pixel;
+    double sk, grad[2], scale;
+    mag_linear_f(g, u, e, p, k, &sk, grad, &scale);
     const double raw[3] = {h * grad[0], h * grad[1], g->det_width};
     double a[3];
     const int m = orc_canonicalize(3, raw, ORC_EPS_REL * h, a);
@@ -375,7 +388,10 @@ static void view_build(const orc_geometry* g, int32_t vglob, view_t* V)
  * pixel corners (Eq. 4) bound the unblurred support; the blurred support is
  * wider by about tau/2 on each side.  A margin of tau + Delta_s covers it; the
  * exact support test inside orc_box_spline decides, so any
- * superset gives the same result (pinned by a test that widens the margin). */
+ * superset gives the same result (pinned by a test that widens the margin).
+ * Model 1 (ledger #22): the linearised footprint P(k) +- h(|dP/dx| + |dP/dy|)/2
+ * can reach past the corners' images when the source is close, so its span
+ * joins the window. */
 static double g_candidate_margin_scale = 1.0;
 
 static void candidate_bins(const orc_geometry* g, const view_t* V, const double k[2],
@@ -388,6 +404,13 @@ static void candidate_bins(const orc_geometry* g, const view_t* V, const double 
         const double s = perspective_f(g, V->u, V->e, V->p, corner);
         if (s < smin) smin = s;
         if (s > smax) smax = s;
+    }
+    if (g->model == 1) {
+        double sk, grad[2], scale;
+        mag_linear_f(g, V->u, V->e, V->p, k, &sk, grad, &scale);
+        const double half = 0.5 * g->pixel * (fabs(grad[0]) + fabs(grad[1]));
+        if (sk - half < smin) smin = sk - half;
+        if (sk + half > smax) smax = sk + half;
     }
     const double margin = g_candidate_margin_scale * (g->det_width + g->det_pitch);
     const double c0 = 0.5 * (double)(g->n_det - 1);

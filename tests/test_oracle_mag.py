@@ -136,3 +136,25 @@ def test_cnsf_is_more_accurate_than_mag():
             for model in (0, 1):
                 err[model] = max(err[model], abs(oracle.weight(dict(g, model=model), th, s, k) - ref))
     assert err[0] < 1e-3 and err[0] < err[1] < 5e-2
+
+
+def test_candidate_window_is_a_superset_close_source():
+    """The model's support is |s - P(k)| < (h(|dP/dx| + |dP/dy|) + tau)/2, which
+    for a source close to the field of view reaches past the perspective
+    images of the pixel corners; widening the candidate window must not
+    change the projection (any superset is exact).  This
+    geometry (source 1.23 field radii away, narrow bins) found the gap."""
+    g = dict(n=10, pixel=1.069340183528383, n_views=120, n_det=54, det_pitch=0.39025943122344087,
+             det_width=0.0819854190161896, sid=9.339360648764503, sdd=13.032752470587264, kind=0, model=1)
+    img = W.random_image(10, 1348).astype(np.float64)
+    base = oracle.forward(g, img)
+    y = W.random_sino(120, 54, 1349).astype(np.float64)
+    base_b = oracle.back(g, y)
+    try:
+        oracle.set_candidate_margin_scale(25.0)
+        wide = oracle.forward(g, img)
+        wide_b = oracle.back(g, y)
+    finally:
+        oracle.set_candidate_margin_scale(1.0)
+    np.testing.assert_array_equal(base, wide)
+    np.testing.assert_array_equal(base_b, wide_b)
