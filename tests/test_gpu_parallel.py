@@ -135,3 +135,18 @@ def test_variant_batch_full_scan(torch_cuda, kind):
     _assert_parity(_fp(torch_cuda, g, imgs), O.forward(g, imgs), f"FP batch kind {kind}")
     y = W.random_sino(88, g["n_det"], 42, batch=3)
     _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), f"BP batch kind {kind}")
+
+
+def test_arc_bp_close_source_bin_range(torch_cuda):
+    # regression (tools/fuzz_wide.py seed 2009): a source within a few pixels
+    # of the field of view; the arc BP's per-tile bin range used the small-angle
+    # bound 1.01 sigma/delta for asin(sigma/|k - p|) and dropped bins (2.4e-2)
+    g = dict(n=1, pixel=1.4937332023018055, n_views=4, n_det=19, det_pitch=0.6050390134164245,
+             det_width=0.13130810019606656, sid=1.2585, sdd=4.0084, kind=cbp.FAN_ARC)
+    for view_begin in (0, 2):
+        y = W.random_sino(2, 19, 2016)
+        _assert_parity(_bp(torch_cuda, g, y, view_begin=view_begin), O.back(g, y, view_begin=view_begin),
+                       f"arc BP close source from view {view_begin}")
+    g5 = dict(g, n=5, pixel=0.5, sid=4.0, sdd=9.0, n_views=16, n_det=60, det_pitch=0.4)
+    y = W.random_sino(16, 60, 2017)
+    _assert_parity(_bp(torch_cuda, g5, y), O.back(g5, y), "arc BP close source, 5x5")
