@@ -302,7 +302,10 @@ int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stre
     // 0.403 -> 0.384 ms; 16 parts in 512-thread CTAs: no further gain)
     if (parts == 4 && ctas(4) < 2 * slots) parts = 8;
     if (force == 1 || force == 2 || force == 4 || force == 8) parts = force;
-    const dim3 grid((unsigned)(ctas(parts) / ((int64_t)views * groups)), views, groups);
+    // views along x (the view-major CTA order of cbp_fp_kernel), detector tiles along y
+    const int64_t tiles = ctas(parts) / ((int64_t)views * groups);
+    if (tiles > 65535) return CBP_EINVAL;
+    const dim3 grid(views, (unsigned)tiles, groups);
     if (parts == 8)
         launch_pdl(cbp::cbp_fp_kernel<S, 8>, grid, dim3(cbp::fp_threads(8)), 0, stream, Pm);
     else if (parts == 4)
