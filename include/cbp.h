@@ -107,6 +107,28 @@ typedef struct cbp_geometry {
  * tau/sdd at the source, tau'(k) = 2 d tan(tau / (2 sdd)).  The reference
  * projector (cbp_ref_*) takes every kind. */
 int cbp_validate(const cbp_geometry_t* g);
+/* (cbp_validate also rejects bins so narrow that no FP32 projector meets the
+ * parity bar: tau'_min / h < 1e-4, with tau'_min / h the lower bound of
+ * cbp_narrow_ratio below.) */
+
+/* Narrow bins and the precise mode.  Eq. 14's weight has
+ * ramps of width tau' + min|zeta|, and on views where a pixel edge
+ * is parallel to the ray min|zeta| -> 0, so an absolute error e in the FP32
+ * position s' becomes a relative weight error ~e / tau'.  When
+ * cbp_narrow_ratio(g) -- a lower bound on tau' / h over the field of view
+ * (tau / h in parallel beam; (sid - n h / sqrt 2) tau sdd / (sdd^2 + s_max^2) / h
+ * flat, with the arc's tau / sdd gain) -- is below 0.02, every call runs the
+ * precise mode: s', A = max|zeta| and the four knot arguments of the nested
+ * form in FP64, rounded once to FP32, with the smallest width nested
+ * innermost (cbp_common.cuh cnsf_prec); FP32 elsewhere.  It is slower (no
+ * view symmetry or batch sharing, FP64 arithmetic per weight: 3-10x) and
+ * holds the parity bar down to tau'/h = 1e-4.  The environment variable CBP_PRECISE=1
+ * (or 0) forces the mode on (off) for every geometry.
+ * cbp_precise_mode returns 1 if calls with g run the precise mode, 0 if not,
+ * CBP_EINVAL for an invalid geometry; cbp_narrow_ratio returns the bound
+ * (negative for an invalid geometry). */
+int cbp_precise_mode(const cbp_geometry_t* g);
+double cbp_narrow_ratio(const cbp_geometry_t* g);
 
 /* Forward projection y = A c (Eq. 6) for views [view_begin,
  * view_begin + view_count) of `batch` images.  Overwrites sino.
@@ -152,9 +174,11 @@ int cbp_normal(const cbp_geometry_t* g, const float* image, float* out, int32_t 
  * the host->device copy of input i+1 and the device->host copy of result
  * i-1 (two internal streams, double-buffered device images) overlap the
  * FP+BP pair of input i on `stream`; the call returns when every result is
- * in host memory.  With DEVICE buffers the pairs run back to back on
- * `stream` (asynchronous).  The sinogram never leaves the device.  One call
- * at a time per device (a mutex serialises callers).  CBP_EINVAL as
+ * in host memory (one host-buffer call at a time per device: a mutex
+ * serialises them).  With DEVICE buffers the pairs run back to back on
+ * `stream` (asynchronous; the sinogram is stream-ordered scratch of the
+ * call, so calls on different streams do not share it).  The sinogram never
+ * leaves the device.  CBP_EINVAL as
  * cbp_normal, count < 1, or one host and one device pointer. */
 int cbp_normal_stream(const cbp_geometry_t* g, const float* images, float* out, int32_t count, int32_t batch,
                       void* stream);

@@ -29,7 +29,7 @@ ABI_FUNCTIONS = ("cbp_validate", "cbp_forward", "cbp_back", "cbp_normal", "cbp_n
                  "cbp_fill", "cbp_dot", "cbp_cgls_step", "cbp_cgls_direction", "cbp_ref_forward",
                  "cbp_ref_back", "cbp_tv_value", "cbp_tv_gradient", "cbp_diff_norm2", "cbp_tv_step",
                  "cbp_asd_adapt", "cbp_adjoint_check", "cbp_strerror", "cbp_version",
-                 "cbp_launch_count")
+                 "cbp_launch_count", "cbp_precise_mode", "cbp_narrow_ratio")
 
 
 class CbpError(RuntimeError):
@@ -141,6 +141,10 @@ def lib() -> ctypes.CDLL:
         L.cbp_version.restype = ctypes.c_int
         L.cbp_launch_count.argtypes = []
         L.cbp_launch_count.restype = ctypes.c_uint64
+        L.cbp_precise_mode.argtypes = [G]
+        L.cbp_precise_mode.restype = ctypes.c_int
+        L.cbp_narrow_ratio.argtypes = [G]
+        L.cbp_narrow_ratio.restype = ctypes.c_double
         _lib = L
     return _lib
 
@@ -175,6 +179,30 @@ def launch_count() -> int:
 
 def validate(geom) -> int:
     return lib().cbp_validate(ctypes.byref(_geom(geom)))
+
+
+def precise_mode(geom) -> int:
+    """1 if calls with this geometry run the narrow-bin precise mode (include/cbp.h)."""
+    return lib().cbp_precise_mode(ctypes.byref(_geom(geom)))
+
+
+def narrow_ratio(geom) -> float:
+    """the library's lower bound on tau'/h over the field of view (include/cbp.h)."""
+    return float(lib().cbp_narrow_ratio(ctypes.byref(_geom(geom))))
+
+
+def _check_dev(t, shape, what, device=None):
+    """a contiguous float32 CUDA tensor of exactly `shape` (the orbit / dihedral
+    calls take device buffers only, and their kernels trust the extents)"""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{what}: expected a CUDA tensor")
+    if t.dtype != torch.float32 or not t.is_contiguous():
+        raise ValueError(f"{what}: expected a contiguous float32 tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{what}: shape {tuple(t.shape)} != {tuple(shape)}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{what}: on {t.device}, expected {device}")
 
 
 def _ptr_and_stream(t, stream):
@@ -332,6 +360,12 @@ def back_multimem(geom, sino, mc_ptr: int, view_begin: int = 0, shard=None, stre
     [4, base_count, n_det]; "dihedral": the natural [n_views, n_det]).  The
     caller zeroes every copy and fences before, and fences after."""
     g = _checked(geom)
+    if shard is None or shard.mode == "block":
+        _check_dev(sino, (sino.shape[0] if sino.ndim == 2 else -1, g.n_det), "back_multimem sino")
+    elif shard.mode == "orbit":
+        _check_dev(sino, (4, shard.count, g.n_det), "back_multimem sino")
+    else:
+        _check_dev(sino, (g.n_views, g.n_det), "back_multimem sino")
     ps, st = _ptr_and_stream(sino, stream)
     mc = ctypes.c_void_p(int(mc_ptr))
     if shard is None or shard.mode == "block":
@@ -359,9 +393,11 @@ def forward_orbit(geom, image, base_begin: int, base_count: int, sino=None, stre
     """Views {b + q n_views/4 : b in [base_begin, base_begin + base_count), q < 4}
     of one image (CUDA tensor [n, n]); returns sino [4, base_count, n_det]."""
     g = _checked(geom)
+    _check_dev(image, (g.n, g.n), "forward_orbit image")
     shape = (4, base_count, g.n_det)
     if sino is None:
         sino = _empty_like(image, shape)
+    _check_dev(sino, shape, "forward_orbit sino", image.device)
     pi, st = _ptr_and_stream(image, stream)
     ps, _ = _ptr_and_stream(sino, stream)
     rc = lib().cbp_forward_orbit(ctypes.byref(g), pi, ps, base_begin, base_count, st)
@@ -373,10 +409,14 @@ def forward_orbit(geom, image, base_begin: int, base_count: int, sino=None, stre
 def back_orbit(geom, sino, base_begin: int, image=None, accumulate: bool = False, stream=None):
     """Adjoint of forward_orbit: sino [4, base_count, n_det] -> image [n, n]."""
     g = _checked(geom)
+    if sino.ndim != 3:
+        raise ValueError(f"back_orbit sino: expected [4, base_count, n_det], got {tuple(sino.shape)}")
+    _check_dev(sino, (4, sino.shape[1], g.n_det), "back_orbit sino")
     if image is None:
         if accumulate:
             raise ValueError("accumulate=True needs an image to add into")
         image = _empty_like(sino, (g.n, g.n))
+    _check_dev(image, (g.n, g.n), "back_orbit image", sino.device)
     ps, st = _ptr_and_stream(sino, stream)
     pi, _ = _ptr_and_stream(image, stream)
     rc = lib().cbp_back_orbit(ctypes.byref(g), ps, pi, base_begin, sino.shape[1],
@@ -452,8 +492,10 @@ def forward_dihedral(geom, image, base_begin: int, base_count: int, sino=None, s
     sinogram (zero-filled when allocated here; other rows untouched)."""
     import torch
     g = _checked(geom)
+    _check_dev(image, (g.n, g.n), "forward_dihedral image")
     if sino is None:
         sino = torch.zeros((g.n_views, g.n_det), dtype=torch.float32, device=image.device)
+    _check_dev(sino, (g.n_views, g.n_det), "forward_dihedral sino", image.device)
     pi, st = _ptr_and_stream(image, stream)
     ps, _ = _ptr_and_stream(sino, stream)
     rc = lib().cbp_forward_dihedral(ctypes.byref(g), pi, ps, base_begin, base_count, st)
@@ -466,8 +508,12 @@ def back_dihedral(geom, sino, base_begin: int, base_count: int, image=None, accu
                   stream=None):
     """The partial adjoint over a dihedral shard's views (natural sinogram)."""
     g = _checked(geom)
+    _check_dev(sino, (g.n_views, g.n_det), "back_dihedral sino")
     if image is None:
+        if accumulate:
+            raise ValueError("accumulate=True needs an image to add into")
         image = _empty_like(sino, (g.n, g.n))
+    _check_dev(image, (g.n, g.n), "back_dihedral image", sino.device)
     ps, st = _ptr_and_stream(sino, stream)
     pi, _ = _ptr_and_stream(image, stream)
     rc = lib().cbp_back_dihedral(ctypes.byref(g), ps, pi, base_begin, base_count, 1 if accumulate else 0, st)

@@ -235,20 +235,34 @@ int check_common(const cbp_geometry_t* g, const void* a, const void* b, int32_t 
     return CBP_OK;
 }
 
-// stream-ordered scratch from the device's default pool (kept, not released)
+// stream-ordered scratch from the library's own memory pool per device
+// (freed blocks are kept for reuse: release threshold UINT64_MAX on this
+// private pool only, so other cudaMallocAsync users of the process keep the
+// default pool's behaviour); the device's default pool if creation fails
 int scratch_alloc(void** p, size_t bytes, cudaStream_t stream)
 {
     static std::once_flag once[64];
+    static cudaMemPool_t pools[64];
     int dev = 0;
     cudaGetDevice(&dev);
     std::call_once(once[dev & 63], [dev] {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
             uint64_t keep = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            pools[dev & 63] = pool;
+        } else {
+            cudaGetLastError();
+            pools[dev & 63] = nullptr;
         }
     });
-    if (cudaMallocAsync(p, bytes, stream) != cudaSuccess) {
+    const cudaError_t e = pools[dev & 63] ? cudaMallocFromPoolAsync(p, bytes, pools[dev & 63], stream)
+                                          : cudaMallocAsync(p, bytes, stream);
+    if (e != cudaSuccess) {
         cudaGetLastError();
         return CBP_ECUDA;
     }
@@ -268,10 +282,41 @@ int fp_pad_width(const cbp_geometry_t& g)
     return (int)std::floor(2.0 * sigq) + 2;
 }
 
+// The precise mode (cbp_common.cuh cnsf_prec) for narrow
+// bins: the FP32 weight carries s' and its knots with an absolute rounding of
+// ~1e-7 h (several ulp after the kernels' affine steps), which a ramp of
+// width tau' + C turns into a relative error ~1e-7 h / tau' on views with
+// C -> 0.  narrow_ratio() is a lower bound on tau' / h over the field of view:
+// tau' = g_j d with d >= D_po - R (R the circumscribed radius) and g_j >=
+// tau D_ps / (D_ps^2 + s_max^2) (flat), tau / D_ps (arc), 1 (parallel, tau' = tau).
+double narrow_ratio(const cbp_geometry_t& g)
+{
+    if (g.kind == CBP_PARALLEL) return g.det_width / g.pixel;
+    const double R = 0.5 * (double)g.n * g.pixel * std::sqrt(2.0);
+    const double smax = 0.5 * (double)(g.n_det - 1) * g.det_pitch + 0.5 * g.det_width;
+    const double gmin = g.kind == CBP_FAN_ARC ? g.det_width / g.sdd
+                                              : g.det_width * g.sdd / (g.sdd * g.sdd + smax * smax);
+    return gmin * (g.sid - R) / g.pixel;
+}
+
+// below this tau'_min / h the FP32 path's weight error approaches the parity
+// bar: measured (tools/narrow_sweep.py, profiles/r02_narrow_sweep.jsonl) the
+// FP32 path stays <= 7e-6 relL2 / 2e-5 max down to a ratio of 0.0016 at n = 40,
+// ~1e-6 at 0.02; the precise mode costs 3-10x.
+// CBP_PRECISE=0/1 forces either mode
+constexpr double CBP_NARROW_RATIO = 0.02;
+
+bool precise(const cbp_geometry_t& g)
+{
+    const char* e = getenv("CBP_PRECISE");  // read per call: tests switch it at run time
+    if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
+    return narrow_ratio(g) < CBP_NARROW_RATIO;
+}
+
 // FP launch: PARTS warps per ray (cbp_fp_kernel) while the grid is short of
 // ~8 waves of resident CTAs (config 2: 1.6 waves -> parts 4, FP -17 %;
 // config 3: 6.5 waves -> parts 2; config 4 / 5: enough waves)
-template <int S>
+template <int S, bool PREC = false>
 int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stream)
 {
     int dev = 0, sms = 148;
@@ -281,7 +326,7 @@ int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stre
     static int per_sm[64];
     std::call_once(once[dev & 63], [dev] {
         int k = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_fp_kernel<S, 1>, cbp::FP_BLOCK, 0) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_fp_kernel<S, 1, PREC>, cbp::FP_BLOCK, 0) !=
                 cudaSuccess || k < 1)
             k = 1;
         per_sm[dev & 63] = k;
@@ -307,18 +352,18 @@ int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stre
     if (tiles > 65535) return CBP_EINVAL;
     const dim3 grid(views, (unsigned)tiles, groups);
     if (parts == 8)
-        launch_pdl(cbp::cbp_fp_kernel<S, 8>, grid, dim3(cbp::fp_threads(8)), 0, stream, Pm);
+        launch_pdl(cbp::cbp_fp_kernel<S, 8, PREC>, grid, dim3(cbp::fp_threads(8)), 0, stream, Pm);
     else if (parts == 4)
-        launch_pdl(cbp::cbp_fp_kernel<S, 4>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
+        launch_pdl(cbp::cbp_fp_kernel<S, 4, PREC>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
     else if (parts == 2)
-        launch_pdl(cbp::cbp_fp_kernel<S, 2>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
+        launch_pdl(cbp::cbp_fp_kernel<S, 2, PREC>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
     else
-        launch_pdl(cbp::cbp_fp_kernel<S, 1>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
+        launch_pdl(cbp::cbp_fp_kernel<S, 1, PREC>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
     ++g_launches;
     return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
 }
 
-template <int S>
+template <int S, bool PREC = false>
 int launch_fp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
                 int32_t batch, int32_t v0, int32_t nv, cudaStream_t stream)
 {
@@ -350,7 +395,7 @@ int launch_fp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* img,
     Pm.batch = batch;
     Pm.sym_stride = 0;
     Pm.sym_mode = 0;
-    rc = launch_fp_kernel<S>(Pm, nv, G, stream);
+    rc = launch_fp_kernel<S, PREC>(Pm, nv, G, stream);
     cudaFreeAsync(pad, stream);
     return rc;
 }
@@ -360,7 +405,8 @@ int launch_fp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* img,
 bool use_sym4(const cbp_geometry_t& g, int32_t batch, int32_t v0, int32_t nv)
 {
     static const bool off = getenv("CBP_NO_SYMMETRY") != nullptr;
-    return !off && g.model == CBP_MODEL_CNSF && batch == 1 && v0 == 0 && nv == g.n_views && g.n_views % 4 == 0;
+    return !off && g.model == CBP_MODEL_CNSF && batch == 1 && v0 == 0 && nv == g.n_views && g.n_views % 4 == 0 &&
+           !precise(g);
 }
 
 // sino holds [4][base_count][n_det]: row q base_count + b is view
@@ -456,7 +502,7 @@ bool use_mag_sym4(const cbp_geometry_t& g, int32_t batch, int32_t v0, int32_t nv
 {
     static const bool off = getenv("CBP_NO_SYMMETRY") != nullptr;
     return !off && g.model == CBP_MODEL_MAG && batch == 1 && v0 == 0 && nv == g.n_views && g.n_views % 4 == 0 &&
-           g.n % 2 == 0;
+           g.n % 2 == 0 && !precise(g);
 }
 
 // frames per footprint of the symmetric magnified-footprint BP: 8 (the
@@ -511,7 +557,9 @@ int launch_mag(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, 
         P.sino = sino;
         const int bins = (g.n_det + cbp::MAG_FP_BLOCK - 1) / cbp::MAG_FP_BLOCK;
         static const bool warp_walk = getenv("CBP_MAG_FP_BLOCKWALK") == nullptr;  // A/B knob
-        if (sym4) {
+        if (precise(g)) {
+            cbp::cbp_mag_fp_kernel<1, true><<<dim3(bins, nv, batch), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
+        } else if (sym4) {
             P.view_count = g.n_views / 4;
             if (warp_walk)
                 cbp::cbp_mag_fpw_kernel<4><<<dim3(bins, g.n_views / 4, 1), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
@@ -542,8 +590,12 @@ int launch_mag(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, 
             const int64_t pix = (int64_t)g.n * g.n;
             P.vg = mag_bp_groups(pix * batch);
             const int per = cbp::MAG_BP_BLOCK / P.vg;
-            cbp::cbp_mag_bp_kernel<1><<<dim3((unsigned)((pix + per - 1) / per), batch), cbp::MAG_BP_BLOCK,
-                                        P.vg > 1 ? sizeof(float) * cbp::MAG_BP_BLOCK : 0, stream>>>(P);
+            const dim3 grid((unsigned)((pix + per - 1) / per), batch);
+            const size_t sm = P.vg > 1 ? sizeof(float) * cbp::MAG_BP_BLOCK : 0;
+            if (precise(g))
+                cbp::cbp_mag_bp_kernel<1, true><<<grid, cbp::MAG_BP_BLOCK, sm, stream>>>(P);
+            else
+                cbp::cbp_mag_bp_kernel<1><<<grid, cbp::MAG_BP_BLOCK, sm, stream>>>(P);
         }
     }
     ++g_launches;
@@ -556,6 +608,7 @@ int launch_fp(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, f
               int32_t batch, int32_t v0, int32_t nv, cudaStream_t stream)
 {
     if (g.model == CBP_MODEL_MAG) return launch_mag(g, t, img, sino, batch, v0, nv, 0, stream, true);
+    if (precise(g)) return launch_fp_s<1, true>(g, t, img, sino, batch, v0, nv, stream);
     // FP: the 8-fold kernel needs 128 registers (8 slices x 2 lines); on
     // sm_100a the 4-fold one is faster, so the FP uses the mirror only when
     // CBP_FP_MIRROR is set
@@ -667,7 +720,7 @@ int get_headers(const cbp_geometry_t& g, const cbp::Tables& t, int32_t v0, int32
     return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
 }
 
-template <int S>
+template <int S, bool PREC = false>
 int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
                 int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream,
                 int symmode = 0, int images = 1)
@@ -681,14 +734,14 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int SG = sym ? images : (batch + S - 1) / S;
-    const size_t smem = cbp::bp_smem_bytes(S);
+    const size_t smem = cbp::bp_smem_bytes(S, PREC);
     static std::once_flag attr[64];
     static int per_sm[64];
     std::call_once(attr[dev & 63], [smem, dev] {
-        cudaFuncSetAttribute(cbp::cbp_bp_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(cbp::cbp_bp_kernel<S, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         int k = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_bp_kernel<S>, cbp::BP_THREADS,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_bp_kernel<S, PREC>, cbp::BP_THREADS,
                                                           smem) != cudaSuccess || k < 1)
             k = 1;
         per_sm[dev & 63] = k;
@@ -733,7 +786,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     fprintf(stderr, "launch_bp S=%d G=%d vpg=%d grid=%d,%d,%d smem=%zu\n", S, G, vpg, grid.x, grid.y,
             grid.z, smem);
 #endif
-    launch_pdl(cbp::cbp_bp_kernel<S>, grid, dim3(cbp::BP_THREADS), smem, stream, P);
+    launch_pdl(cbp::cbp_bp_kernel<S, PREC>, grid, dim3(cbp::BP_THREADS), smem, stream, P);
     ++g_launches;
 #ifdef CBP_DEBUG_CHECKS
     fprintf(stderr, "bp kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
@@ -758,6 +811,7 @@ int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, 
 {
     if (g.model == CBP_MODEL_MAG)
         return launch_mag(g, t, img, const_cast<float*>(sino), batch, v0, nv, accumulate, stream, false);
+    if (precise(g)) return launch_bp_s<1, true>(g, t, sino, img, batch, v0, nv, accumulate, stream);
     if (use_sym8(g, batch, v0, nv))
         return launch_bp_s<8>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8);
     if (batch > 1 && use_sym8(g, 1, v0, nv))  // a batch: the 8 frames of each image
@@ -780,7 +834,8 @@ int cbp_validate(const cbp_geometry_t* g)
     if (!finite_pos(g->pixel) || !finite_pos(g->det_pitch) || !finite_pos(g->det_width))
         return CBP_EINVAL;
     if (g->model != CBP_MODEL_CNSF && g->model != CBP_MODEL_MAG) return CBP_EINVAL;
-    if (g->kind == CBP_PARALLEL) return std::isfinite(g->sid) && std::isfinite(g->sdd) ? CBP_OK : CBP_EINVAL;
+    if (g->kind == CBP_PARALLEL)
+        return std::isfinite(g->sid) && std::isfinite(g->sdd) && narrow_ratio(*g) >= 1e-4 ? CBP_OK : CBP_EINVAL;
     if (g->kind != CBP_FAN_FLAT && g->kind != CBP_FAN_ARC) return CBP_EINVAL;
     if (!finite_pos(g->sid) || !finite_pos(g->sdd)) return CBP_EINVAL;
     // arc: every bin (and its blur) strictly inside +-90 degrees of the central ray
@@ -791,7 +846,21 @@ int cbp_validate(const cbp_geometry_t* g)
     if (g->det_width >= 2.0 * g->sdd) return CBP_EINVAL;
     const double radius = 0.5 * (double)g->n * g->pixel * std::sqrt(2.0);
     if (!(radius < g->sid)) return CBP_EINVAL;
+    if (!(narrow_ratio(*g) >= 1e-4)) return CBP_EINVAL;  // below the precise mode's range
     return CBP_OK;
+}
+
+int cbp_precise_mode(const cbp_geometry_t* g)
+{
+    if (cbp_validate(g) != CBP_OK) return CBP_EINVAL;
+    return precise(*g) ? 1 : 0;
+}
+
+double cbp_narrow_ratio(const cbp_geometry_t* g)
+{
+    if (cbp_validate(g) != CBP_OK && !(g && g->n >= 1 && finite_pos(g->pixel) && finite_pos(g->det_width)))
+        return -1.0;
+    return narrow_ratio(*g);
 }
 
 int cbp_forward(const cbp_geometry_t* g, const float* image, float* sino, int32_t batch,
@@ -972,6 +1041,21 @@ int cbp_normal_stream(const cbp_geometry_t* g, const float* images, float* out, 
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
     const size_t ni = (size_t)batch * g->n * g->n;
     const size_t ib = sizeof(float) * ni, sb = sizeof(float) * (size_t)batch * g->n_views * g->n_det;
+    if (ki == 1) {
+        // device buffers: the pairs back to back on `stream`, asynchronous -- the
+        // sinogram is stream-ordered scratch of this call (a buffer shared between
+        // calls would race with a later call on another stream)
+        float* sino = nullptr;
+        if ((rc = scratch_alloc((void**)&sino, sb, stream)) != CBP_OK) return rc;
+        for (int32_t i = 0; i < count && rc == CBP_OK; ++i) {
+            rc = launch_fp(*g, t, images + i * ni, sino, batch, 0, g->n_views, stream);
+            if (rc == CBP_OK) rc = launch_bp(*g, t, sino, out + i * ni, batch, 0, g->n_views, 0, stream);
+        }
+        cudaFreeAsync(sino, stream);
+        return rc;
+    }
+    // host buffers: the call is synchronous, so the per-device pipe buffers
+    // are free again when it returns (the mutex serialises callers)
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(g_pipe_mu);
@@ -979,13 +1063,6 @@ int cbp_normal_stream(const cbp_geometry_t* g, const float* images, float* out, 
     if ((rc = pipe_get(dev, &P)) != CBP_OK) return rc;
     if ((rc = pipe_buf(*P, 4, sb)) != CBP_OK) return rc;
     float* sino = (float*)P->buf[4];
-    if (ki == 1) {  // device buffers: the pairs back to back on `stream`
-        for (int32_t i = 0; i < count && rc == CBP_OK; ++i) {
-            rc = launch_fp(*g, t, images + i * ni, sino, batch, 0, g->n_views, stream);
-            if (rc == CBP_OK) rc = launch_bp(*g, t, sino, out + i * ni, batch, 0, g->n_views, 0, stream);
-        }
-        return rc;
-    }
     for (int k = 0; k < 4 && rc == CBP_OK; ++k) rc = pipe_buf(*P, k, ib);
     if (rc != CBP_OK) return rc;
     // everything after the work already queued on `stream`
@@ -1031,6 +1108,7 @@ int cbp_symmetry_fold(const cbp_geometry_t* g, int32_t batch, int32_t view_begin
                       int32_t view_count)
 {
     if (cbp_validate(g) != CBP_OK) return CBP_EINVAL;
+    if (precise(*g)) return 1;
     if (use_mag_sym4(*g, batch, view_begin, view_count)) return mag_bp_fold(*g);  // the BP's (the FP uses 4)
     if (use_sym8(*g, 1, view_begin, view_count)) return 8;  // the BP of any batch (per image)
     return use_sym4(*g, batch, view_begin, view_count) ? 4 : 1;
@@ -1055,10 +1133,10 @@ int cbp_forward_orbit(const cbp_geometry_t* g, const float* image, float* sino, 
     cudaStream_t stream = (cudaStream_t)stream_;
     cbp::Tables t;
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
-    if (g->model == CBP_MODEL_MAG) {  // no shared weights: the 4 view blocks one by one
+    if (g->model == CBP_MODEL_MAG || precise(*g)) {  // no shared weights: the 4 view blocks one by one
         for (int q = 0; q < 4 && rc == CBP_OK; ++q)
-            rc = launch_mag(*g, t, image, sino + (size_t)q * base_count * g->n_det, 1,
-                            base_begin + q * (g->n_views / 4), base_count, 0, stream, true);
+            rc = launch_fp(*g, t, image, sino + (size_t)q * base_count * g->n_det, 1,
+                           base_begin + q * (g->n_views / 4), base_count, stream);
         return rc;
     }
     return launch_fp_sym4(*g, t, image, sino, base_begin, base_count, stream);
@@ -1073,22 +1151,22 @@ int cbp_back_orbit(const cbp_geometry_t* g, const float* sino, float* image, int
     cudaStream_t stream = (cudaStream_t)stream_;
     cbp::Tables t;
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
-    if (g->model == CBP_MODEL_MAG) {
+    if (g->model == CBP_MODEL_MAG || precise(*g)) {
         for (int q = 0; q < 4 && rc == CBP_OK; ++q)
-            rc = launch_mag(*g, t, image, const_cast<float*>(sino) + (size_t)q * base_count * g->n_det, 1,
-                            base_begin + q * (g->n_views / 4), base_count, q > 0 ? acc_next(accumulate) : accumulate,
-                            stream, false);
+            rc = launch_bp(*g, t, sino + (size_t)q * base_count * g->n_det, image, 1,
+                           base_begin + q * (g->n_views / 4), base_count, q > 0 ? acc_next(accumulate) : accumulate,
+                           stream);
         return rc;
     }
     return launch_bp_s<4>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 4);
 }
 
 // ---- dihedral shards (views sharded over GPUs keeping the 8-fold symmetry)
-// The magnified-footprint model runs the shard's views as contiguous blocks
-// of the natural layout: the 4 rotations of the base block [b0, b0 + nb) and
-// of its mirror images N/4 - b for b in [max(b0, 1), min(b0 + nb, N/8)).
-static int mag_dihedral(const cbp_geometry_t& g, const cbp::Tables& t, const float* image, float* sino,
-                        int32_t b0, int32_t nb, int32_t accumulate, cudaStream_t stream, bool fp)
+// The magnified-footprint model and the precise mode run the shard's views as
+// contiguous blocks of the natural layout: the 4 rotations of the base block
+// [b0, b0 + nb) and of its mirror images N/4 - b for b in [max(b0, 1), min(b0 + nb, N/8)).
+static int block_dihedral(const cbp_geometry_t& g, const cbp::Tables& t, const float* image, float* sino,
+                          int32_t b0, int32_t nb, int32_t accumulate, cudaStream_t stream, bool fp)
 {
     const int N = g.n_views, q = N / 4, e = N / 8;
     const int lo = std::max(b0, 1), hi = std::min(b0 + nb, e);
@@ -1098,8 +1176,9 @@ static int mag_dihedral(const cbp_geometry_t& g, const cbp::Tables& t, const flo
         if (counts[blk] < 1) continue;
         for (int r = 0; r < 4 && rc == CBP_OK; ++r, ++done) {
             const int v = starts[blk] + r * q;
-            rc = launch_mag(g, t, image, sino + (size_t)v * g.n_det, 1, v, counts[blk],
-                            done > 0 ? acc_next(accumulate) : accumulate, stream, fp);
+            rc = fp ? launch_fp(g, t, image, sino + (size_t)v * g.n_det, 1, v, counts[blk], stream)
+                    : launch_bp(g, t, sino + (size_t)v * g.n_det, const_cast<float*>(image), 1, v, counts[blk],
+                                done > 0 ? acc_next(accumulate) : accumulate, stream);
         }
     }
     return rc;
@@ -1125,7 +1204,8 @@ int cbp_forward_dihedral(const cbp_geometry_t* g, const float* image, float* sin
     cbp::Tables t;
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
     const int N = g->n_views, q = N / 4, e = N / 8;
-    if (g->model == CBP_MODEL_MAG) return mag_dihedral(*g, t, image, sino, base_begin, base_count, 0, stream, true);
+    if (g->model == CBP_MODEL_MAG || precise(*g))
+        return block_dihedral(*g, t, image, sino, base_begin, base_count, 0, stream, true);
     // the 4 rotations of the base block, then those of its mirror images
     // N/4 - v (v = 0 and v = N/8 are their own mirror orbits)
     // one pad and one launch for both blocks (the grid of a small shard is far short of a wave)
@@ -1142,8 +1222,9 @@ int cbp_back_dihedral(const cbp_geometry_t* g, const float* sino, float* image, 
     cudaStream_t stream = (cudaStream_t)stream_;
     cbp::Tables t;
     if ((rc = get_tables(*g, stream, t)) != CBP_OK) return rc;
-    if (g->model == CBP_MODEL_MAG)
-        return mag_dihedral(*g, t, image, const_cast<float*>(sino), base_begin, base_count, accumulate, stream, false);
+    if (g->model == CBP_MODEL_MAG || precise(*g))
+        return block_dihedral(*g, t, image, const_cast<float*>(sino), base_begin, base_count, accumulate, stream,
+                              false);
     return launch_bp_s<8>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 8);
 }
 
@@ -1378,7 +1459,7 @@ int cbp_ref_back(const cbp_geometry_t* g, const double* sino, double* image, int
     return launched();
 }
 
-int cbp_version(void) { return 130; }
+int cbp_version(void) { return 140; }
 
 uint64_t cbp_launch_count(void) { return g_launches.load(); }
 

@@ -298,6 +298,59 @@ __device__ void bp_build_entry(const GeomDev& g, const Tables& t, const BPHeader
     E.c = make_float4(A, 1.0f / C, 0.5f * C, y * (h * h / A));
 }
 
+// The precise mode (narrow bins, cbp_common.cuh cnsf_prec): s' at the anchor,
+// its slopes and A in FP64, so s'(k) and the knots are exact to ~ulp of
+// their own size (S = 1 only; the symmetric and batched paths stay FP32).
+struct __align__(16) BPEntryP {
+    double xa, sc, sr;  // s'(k_a), ds'/dc, ds'/dr
+    double A;           // max |zeta|
+    float Ba, tx, ty;   // tau'(k_a), dtau'/dc, dtau'/dr
+    float Cz;           // min |zeta|
+    float yw;           // y[v][j] h^2 / A
+};
+
+__device__ void bp_build_entry_prec(const GeomDev& g, const Tables& t, const BPHeader& H, int j, float y,
+                                    BPEntryP& E)
+{
+    const double2 bd = t.bin_d[j];
+    const float4 bf = t.bin_f[j];
+    const double invL = bd.y;
+    const double sphi = g.parallel ? 0.0 : bd.x * invL, cphi = g.parallel ? 1.0 : g.sdd * invL;
+    const double rxd = sphi * H.cth - cphi * H.sth, ryd = cphi * H.cth + sphi * H.sth;
+    E.xa = g.arc ? sqrt(H.delta_a * H.delta_a + H.kae * H.kae) * sin((double)(j - H.ja) * (g.pitch / g.sdd) - H.f_a)
+                 : H.delta_a * ((double)(j - H.ja) * g.pitch - H.f_a) * invL;
+    E.sc = -rxd * g.h;  // dk = (dc h, -dr h), s' = r_j . (p - k)
+    E.sr = ryd * g.h;
+    const double Ad = fmax(fabs(rxd), fabs(ryd)) * g.h;
+    E.A = Ad;
+    const float rx = (float)rxd, ry = (float)ryd, h = (float)g.h, gj = g.parallel ? 0.0f : bf.z;
+    const float da = bf.y * (float)H.delta_a + bf.x * (float)H.kae;  // (k_a - p) . v_j
+    E.Ba = g.parallel ? (float)g.tau : gj * da;
+    E.tx = -gj * ry * h;
+    E.ty = -gj * rx * h;
+    E.Cz = (float)(fmin(fabs(rxd), fabs(ryd)) * g.h);
+    E.yw = y * (float)(g.h * g.h / Ad);
+}
+
+// entries row[jl - base .. jh - base] for one pixel pair (dc, dr).{x, y}
+__device__ __forceinline__ void bp_pair_prec(const BPEntryP* row, int jl, int jh, int base, float2 dc, float2 dr,
+                                             float2& acc)
+{
+    if (jh < jl) return;
+    CBP_CHECK(jl >= base && jh - base < BP_NB, "bp_pair_prec jl=%d jh=%d base=%d\n", jl, jh, base);
+    const BPEntryP* e = row + (jl - base);
+    for (int k = jl; k <= jh; ++k, ++e) {
+        const double xa = e->xa, sc = e->sc, sr = e->sr, A = e->A;
+        const float Ba = e->Ba, tx = e->tx, ty = e->ty, Cz = e->Cz, yw = e->yw;
+        const float wa = cnsf_prec(fma((double)dr.x, sr, fma((double)dc.x, sc, xa)), A,
+                                   fmaf(dr.x, ty, fmaf(dc.x, tx, Ba)), Cz);
+        const float wb = cnsf_prec(fma((double)dr.y, sr, fma((double)dc.y, sc, xa)), A,
+                                   fmaf(dr.y, ty, fmaf(dc.y, tx, Ba)), Cz);
+        acc.x = fmaf(yw, wa, acc.x);
+        acc.y = fmaf(yw, wb, acc.y);
+    }
+}
+
 // one entry, one pixel pair (lane b = lane a + one pixel along the pair axis):
 // returns num / tau' for both pixels (the weight without the h^2/A factor)
 __device__ __forceinline__ float2 bp_weight(const BPEntry* e, float dc, float dr)
@@ -452,9 +505,9 @@ __device__ __forceinline__ void frame_inv(int n, int q, int m, int& r, int& c)
 
 // dynamic shared memory of the BP kernel for S slices: entries, headers,
 // (S > 1) two y buffers [2][VC][NB][S], tile accumulators [S][32][33]
-__host__ __device__ constexpr size_t bp_smem_bytes(int S)
+__host__ __device__ constexpr size_t bp_smem_bytes(int S, bool prec = false)
 {
-    return sizeof(BPEntry) * BP_VC * BP_NB + sizeof(BPHeader) * BP_VC * bp_hdr_bufs(S) +
+    return (prec ? sizeof(BPEntryP) : sizeof(BPEntry)) * BP_VC * BP_NB + sizeof(BPHeader) * BP_VC * bp_hdr_bufs(S) +
            (S > 1 ? 2 * sizeof(float) * BP_VC * BP_NB * S : 0) +
            (S >= 4 ? sizeof(float) : sizeof(double)) * S * BP_TILE * (BP_TILE + 1);
 }
@@ -521,17 +574,19 @@ __device__ __forceinline__ void bp_y_load(const BPParams& P, int vl0, int nvc, i
     }
 }
 
-template <int S>
+template <int S, bool PREC = false>
 __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp_bp_kernel(const BPParams P)
 {
+    static_assert(!PREC || S == 1, "the precise mode runs one slice per weight");
+    using Ent = typename std::conditional<PREC, BPEntryP, BPEntry>::type;
     constexpr bool STAGE = S > 1;  // y staged asynchronously one chunk ahead
     constexpr int HB = bp_hdr_bufs(S);
     extern __shared__ __align__(16) unsigned char smem[];
-    BPEntry(*tab)[BP_NB] = reinterpret_cast<BPEntry(*)[BP_NB]>(smem);
-    BPHeader* hdr_all = reinterpret_cast<BPHeader*>(smem + sizeof(BPEntry) * BP_VC * BP_NB);  // [HB][VC]
+    Ent(*tab)[BP_NB] = reinterpret_cast<Ent(*)[BP_NB]>(smem);
+    BPHeader* hdr_all = reinterpret_cast<BPHeader*>(smem + sizeof(Ent) * BP_VC * BP_NB);  // [HB][VC]
     float* ytab_all = reinterpret_cast<float*>(hdr_all + HB * BP_VC);  // [2][VC][NB][S] (S > 1)
     bp_acc_t<S>* acc_s = reinterpret_cast<bp_acc_t<S>*>(
-        smem + bp_smem_bytes(S) - sizeof(bp_acc_t<S>) * S * BP_TILE * (BP_TILE + 1));
+        smem + bp_smem_bytes(S, PREC) - sizeof(bp_acc_t<S>) * S * BP_TILE * (BP_TILE + 1));
 
     const GeomDev& g = P.g;
     const int tid = threadIdx.x;
@@ -609,7 +664,11 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                     const int j = H.jlo + pass * BP_NB + jj;
                     CBP_CHECK(j > H.jhi || (j >= 0 && j < g.n_det), "entry j=%d jlo=%d jhi=%d\n", j, H.jlo, H.jhi);
                     if (j <= H.jhi) {
-                        if constexpr (S == 1) {
+                        if constexpr (PREC) {
+                            const size_t yo = (size_t)(vg0 + vc + vi) * g.n_det + j;
+                            bp_build_entry_prec(g, P.t, H, j, __ldg(P.sino + (size_t)sg * sino_plane + yo),
+                                                tab[vi][jj]);
+                        } else if constexpr (S == 1) {
                             const size_t yo = (size_t)(vg0 + vc + vi) * g.n_det + j;
                             bp_build_entry(g, P.t, H, j, __ldg(P.sino + (size_t)sg * sino_plane + yo),
                                            tab[vi][jj]);
@@ -652,7 +711,7 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                 }
                 const int base = hi.y + pass * BP_NB;
                 if (base > hi.z) continue;
-                const BPEntry* row = tab[vi];
+                const Ent* row = tab[vi];
                 const float* yrow = ytab + vi * BP_NB * S;
                 const float4 hf = *reinterpret_cast<const float4*>(&H.urel);  // urel, nx, ny, cW
                 const float4 hd = *reinterpret_cast<const float4*>(&H.dena);  // dena, dx, dy, -
@@ -676,7 +735,9 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                     const float hi2 = fmaxf(fminf(fmaxf(u.x + w.x, u.y + w.y), 1e6f), -1e6f);
                     const int jl = max(hi.x + __float2int_rd(lo) + 1, base);
                     const int jh = min(hi.x + __float2int_ru(hi2) - 1, jmax);
-                    if constexpr (BP_UNION<S>) {
+                    if constexpr (PREC) {
+                        bp_pair_prec(row, jl, jh, base, dcp, drp, p ? a1[0] : a0[0]);
+                    } else if constexpr (BP_UNION<S>) {
                         jl2 = min(jl2, jl);
                         jh2 = max(jh2, jh);
                     } else if (p == 0) {

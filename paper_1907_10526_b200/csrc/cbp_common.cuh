@@ -108,6 +108,41 @@ __device__ __forceinline__ float2 cnsf_num2(float2 z11, float2 z21, float2 B, fl
     return __ffma2_rn(make_float2(hC, hC), T, M2);
 }
 
+// ---------------------------------------------------------------------------
+// Eq. 14 for narrow bins (the precise mode).  The FP32 form
+// above carries s' and the knot z11 = s' + (A - C)/2 + tau'/2 as FP32 values
+// of size ~A, so their absolute rounding (~ulp(h), several ulp after the
+// kernels' affine steps) shifts a ramp of width tau' + C by a relative
+// ~1e-7 h / (tau' + C): past the parity bar once tau' ~ 0.01 h on views where
+// C -> 0.  Here s' and A come in FP64 and the four knot arguments
+//   k1 = z11, k2 = z11 - b, k3 = z11 - A, k4 = z11 - A - b
+// are formed in FP64 before the single rounding to FP32, so each is exact to
+// ~ulp of its own (small, near its knot) value.  The two widths besides A are
+// nested smallest-innermost, b = max(tau', C), c = min(tau', C) (the spline
+// box_A * box_tau' * box_C is symmetric in its widths): with c
+// innermost the (c/2) T correction's FP32 rounding is ~1e-7 c / b <= 1e-7 of
+// the plateau b (tau' innermost with C ~ h would give ~1e-7 h / tau').
+// Returns num / b = A M (W = h^2 / A times it), pinned on CPU by
+// tests/test_weight_form.py (<= 2e-7 of the peak for tau' / A down to 1e-4).
+// tau' <= 0 only occurs in the FP's zero border: b, c are kept finite there.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float cnsf_prec(double s, double A, float tau, float Cz)
+{
+    const float b = fmaxf(fmaxf(tau, Cz), 1e-30f), c = fmaxf(fminf(tau, Cz), 0.0f);
+    const double D = fma(0.5, A + (double)(b - c), s);  // z11 = s' + (A + b - c) / 2
+    const double D3 = D - A;
+    const float k1 = (float)D, k2 = (float)(D - (double)b), k3 = (float)D3, k4 = (float)(D3 - (double)b);
+    const float ic = rcp_approx(c);  // c = 0: +inf, sat() eliminates the direction
+    const float t11 = sat_fma(k1, ic, 1.0f), t12 = sat_fma(k2, ic, 1.0f);
+    const float t21 = sat_fma(k3, ic, 1.0f), t22 = sat_fma(k4, ic, 1.0f);
+    float T = t11 * t11;
+    T = fmaf(-t12, t12, T);
+    T = fmaf(-t21, t21, T);
+    T = fmaf(t22, t22, T);
+    const float trap = fmaxf(fmin3(k1, fminf((float)A, b), -k4), 0.0f);
+    return fmaf(0.5f * c, T, trap) * rcp_approx(b);
+}
+
 // the multimem reduction (accumulate mode CBP_ACC_MULTIMEM): `mc` is a
 // multicast address (an NVLink/NVSwitch multicast object bound to one buffer
 // on every rank); the add is performed in the switch on every rank's copy

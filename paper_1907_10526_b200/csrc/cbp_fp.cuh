@@ -402,15 +402,49 @@ __device__ void fp_walk_generic(const FPRay& R, int K, int i0, int i1, int n, in
     }
 }
 
+// The precise mode (narrow bins, cbp_common.cuh cnsf_prec): s' and tau' of a
+// candidate come straight from their FP64 affine forms in (line, candidate)
+// instead of FP32 increments; the 32.32 crossing still picks the candidates.
+struct FPRayD {
+    double X00, a_i, b_q;  // s'(line i, candidate q) = X00 + i a_i + q b_q
+    double T00, t_i, t_q;  // tau'(i, q) = T00 + i t_i + q t_q
+    double A;              // max |zeta|
+    float Cz;              // min |zeta|
+};
+
+template <int NT>
+__device__ void fp_walk_prec(const FPRay& R, const FPRayD& D, int K, int i0, int i1, int n, int np, int P,
+                             double* out)
+{
+    uint32_t flo = R.flo;
+    int32_t fhi = R.fhi;
+    const int qmax = n + P - K;
+    for (int i = i0; i <= i1; ++i) {
+        const int qc = min(max(fhi + 1, -P), qmax);
+        asm("add.cc.u32 %0, %0, %2;\n\taddc.s32 %1, %1, %3;"
+            : "+r"(flo), "+r"(fhi) : "r"(R.mlo), "r"(R.mhi));
+        const float* p = R.base + ((size_t)(i + P) * np + (qc + P));
+        const double Xi = fma((double)i, D.a_i, D.X00), Ti = fma((double)i, D.t_i, D.T00);
+        float part = 0.0f;
+        for (int k = 0; k < K; ++k) {
+            const double q = (double)(qc + k);
+            const float w = cnsf_prec(fma(q, D.b_q, Xi), D.A, (float)fma(q, D.t_q, Ti), D.Cz);
+            part = fmaf(__ldg(p + k), w, part);
+        }
+        out[0] += (double)part;
+    }
+}
+
 // PARTS (1, 2, 4) warps of a CTA share the same 32 rays and walk disjoint
 // parts of their lines; the parts' FP64 totals are summed in part order in
 // shared memory (deterministic).  A CTA covers 128 / PARTS bins.  PARTS > 1
 // when the grid would otherwise be short of ~16 waves: the ragged last wave
 // of a 1.6-wave grid cost ~25 %.
-template <int S, int PARTS>
+template <int S, int PARTS, bool PREC = false>
 __global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? 2 : (S == 1 ? 7 : (S == 4 ? 6 : 4)))
     cbp_fp_kernel(const FPParams P)
 {
+    static_assert(!PREC || S == 1, "the precise mode runs one slice per weight");
     const GeomDev& g = P.g;
     constexpr int NT = fp_threads(PARTS);
     // PDL: with one part per ray (long walks, large grids) the wait comes first
@@ -547,7 +581,19 @@ __global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? 2 : (S == 1 ? 7
         dmin = fmin(dmin, D00 + (n - 1) * (dcol + drow));
         const int mab_t = gj * dmax * (1.0 + 1e-6) < A ? 1 : (gj * dmin * (1.0 - 1e-6) > A ? 2 : 0);
         const int mab = __all_sync(0xffffffffu, mab_t == 1) ? 1 : (__all_sync(0xffffffffu, mab_t == 2) ? 2 : 0);
-        switch (Kw) {
+        if constexpr (PREC) {
+            FPRayD Dr;
+            Dr.X00 = X00;
+            Dr.a_i = a_i;
+            Dr.b_q = b_q;
+            Dr.T00 = gj * D00;
+            Dr.t_i = t_i;
+            Dr.t_q = t_q;
+            Dr.A = A;
+            Dr.Cz = (float)C;
+            fp_walk_prec<NT>(R, Dr, Kw, i0, i1, n, P.np, P.P, acc);
+        } else {
+          switch (Kw) {
             case 1: fp_walk_k<1, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
             case 2: fp_walk_k<2, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
             case 3: fp_walk_k<3, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
@@ -555,8 +601,10 @@ __global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? 2 : (S == 1 ? 7
             case 5: fp_walk_k<5, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
             case 6: fp_walk_k<6, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
             default: fp_walk_generic<S, NT>(R, Kw, i0, i1, n, P.np, P.P, acc); break;
+          }
         }
-#pragma unroll
+        // (an `else switch` followed by a `#pragma unroll` loop lost that loop in the
+        // PREC instantiation -- nvcc 12.9; keep the braces)
         for (int q = 0; q < S; ++q) acc[q * NT] *= h * h * inv_A;  // W = (h^2 / A) num / B
     }
     if (PARTS > 1) {  // sum the parts in part order; the first part's warp writes

@@ -49,7 +49,9 @@ struct MagFootprint {
     float minAB;   // min(A, B)
     float hC;      // C / 2
     float sigma;   // support half-width (A + B + C) / 2
-    float wscale;  // h^2 m(k) / (A B)
+    float wscale;  // h^2 m(k) / (A B)  (precise mode: h^2 m(k) / A)
+    double Ad;     // precise mode only: max |zeta| in FP64
+    float Cz;      // precise mode only: min |zeta|
 };
 
 // lateral offset k.e and depth D_po - k.u of the pixel centre k in view (cu, su)
@@ -114,6 +116,57 @@ __device__ __forceinline__ MagFootprint mag_footprint(const GeomDev& g, double c
     fp.sigma = 0.5f * (A + B + C);
     fp.wscale = __fdiv_rn(h * h * m, A * B);
     return fp;
+}
+
+// The precise mode (narrow bins, cbp_common.cuh cnsf_prec): the footprint's
+// shape in FP64 too, since A enters the knot z11 - A (an FP32 A would shift it
+// by ~1e-7 A against a ramp of width tau + C).
+__device__ __forceinline__ MagFootprint mag_footprint_prec(const GeomDev& g, double cu, double su, double kx,
+                                                           double ky)
+{
+    double lat, dep;
+    mag_frame(g, cu, su, kx, ky, lat, dep);
+    double P, gx, gy;
+    float m;
+    if (g.parallel) {
+        P = lat;
+        gx = -su;
+        gy = cu;
+        m = 1.0f;
+    } else {
+        const double r2 = fma(dep, dep, lat * lat);
+        double f;
+        if (g.arc) {
+            P = g.sdd * atan2(lat, dep);
+            f = g.sdd / r2;
+            m = (float)(g.sdd / sqrt(r2));
+        } else {
+            const double r = 1.0 / dep;
+            P = g.sdd * lat * r;
+            f = g.sdd * r * r;
+            m = (float)((P * P + g.sdd * g.sdd) / (g.sdd * sqrt(r2)));
+        }
+        gx = f * fma(dep, -su, lat * cu);  // grad P = f (dep e + lat u)
+        gy = f * fma(dep, cu, lat * su);
+    }
+    double a1 = fabs(g.h * gx), a2 = fabs(g.h * gy);
+    if (a1 < 1e-6 * g.h) a1 = 0.0;  // ledger #7
+    if (a2 < 1e-6 * g.h) a2 = 0.0;
+    const double A = fmax(a1, a2), C = fmin(a1, a2);
+    MagFootprint fp;
+    fp.P = P;
+    fp.Ad = A;
+    fp.Cz = (float)C;
+    fp.A = (float)A;
+    fp.sigma = (float)(0.5 * (A + g.tau + C));
+    fp.wscale = (float)(g.h * g.h / A) * m;
+    return fp;
+}
+
+__device__ __forceinline__ float mag_weight_prec(const MagFootprint& fp, double x, float B)
+{
+    if (!(fabs(x) < (double)fp.sigma)) return 0.0f;  // sigma rounded up or down: exact 0 there
+    return fp.wscale * cnsf_prec(x, fp.Ad, B, fp.Cz);
 }
 
 // W at x = s - P(k) (exactly 0 outside the open support, ledger #15): the
@@ -265,10 +318,16 @@ __device__ __forceinline__ void mag_band_range(const MagBand& B, int l, int n, i
 
 // the staged footprint of one pixel of a line, with its F image values
 // (F = 4: the pixel's values in the 4 rotated frames)
-template <int F>
+template <int F, bool PREC = false>
 struct MagStaged {
     double P;
     float A, invC, w1, zoff, minAB, hC, sigma, wscale;
+    float val[F];
+};
+template <int F>
+struct MagStaged<F, true> {
+    double P, Ad;
+    float Cz, sigma, wscale;
     float val[F];
 };
 
@@ -291,10 +350,10 @@ __device__ __forceinline__ void mag_rot(int n, int q, int& r, int& c)
 // F = 4 (one image, a full scan, N_v % 4 == 0): blockIdx.y is a base view
 // v < N_v/4 and each weight serves the 4 views v + q N_v/4, reading the image
 // at R^q k and writing the natural sinogram rows.
-template <int F>
+template <int F, bool PREC = false>
 __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
 {
-    __shared__ MagStaged<F> st[MAG_FP_BLOCK];
+    __shared__ MagStaged<F, PREC> st[MAG_FP_BLOCK];
     const GeomDev& g = p.g;
     const int j0 = blockIdx.x * MAG_FP_BLOCK;
     const int j = j0 + threadIdx.x, jl = min(j0 + MAG_FP_BLOCK, g.n_det) - 1;
@@ -338,17 +397,26 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
             if (i <= I1) {
                 const int row = rows ? l : i, col = rows ? i : l;
                 const double kx = ((double)col - g.c0) * g.h, ky = (g.c0 - (double)row) * g.h;
-                const MagFootprint fp = mag_footprint(g, cu, su, kx, ky);
-                MagStaged<F> m;
-                m.P = fp.P;
-                m.A = fp.A;
-                m.invC = fp.invC;
-                m.w1 = fp.w1;
-                m.zoff = fp.zoff;
-                m.minAB = fp.minAB;
-                m.hC = fp.hC;
-                m.sigma = fp.sigma;
-                m.wscale = fp.wscale;
+                MagStaged<F, PREC> m;
+                if constexpr (PREC) {
+                    const MagFootprint fp = mag_footprint_prec(g, cu, su, kx, ky);
+                    m.P = fp.P;
+                    m.Ad = fp.Ad;
+                    m.Cz = fp.Cz;
+                    m.sigma = fp.sigma;
+                    m.wscale = fp.wscale;
+                } else {
+                    const MagFootprint fp = mag_footprint(g, cu, su, kx, ky);
+                    m.P = fp.P;
+                    m.A = fp.A;
+                    m.invC = fp.invC;
+                    m.w1 = fp.w1;
+                    m.zoff = fp.zoff;
+                    m.minAB = fp.minAB;
+                    m.hC = fp.hC;
+                    m.sigma = fp.sigma;
+                    m.wscale = fp.wscale;
+                }
 #pragma unroll
                 for (int q = 0; q < F; ++q) {
                     int r = row, c = col;
@@ -360,20 +428,31 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK) cbp_mag_fp_kernel(MagParams p)
             __syncthreads();
             const int a = max(i0, base), e = min(i1, min(I1, base + MAG_FP_BLOCK - 1));
             for (int q = a; q <= e; ++q) {
-                const MagStaged<F>& m = st[q - base];
-                MagFootprint fp;
-                fp.P = m.P;
-                fp.A = m.A;
-                fp.invC = m.invC;
-                fp.w1 = m.w1;
-                fp.zoff = m.zoff;
-                fp.minAB = m.minAB;
-                fp.hC = m.hC;
-                fp.sigma = m.sigma;
-                fp.wscale = m.wscale;
-                const float wgt = mag_weight_x(fp, (float)(s - fp.P), B);
+                const MagStaged<F, PREC>& m = st[q - base];
+                if constexpr (PREC) {
+                    MagFootprint fp;
+                    fp.Ad = m.Ad;
+                    fp.Cz = m.Cz;
+                    fp.sigma = m.sigma;
+                    fp.wscale = m.wscale;
+                    const float wgt = mag_weight_prec(fp, s - m.P, B);
 #pragma unroll
-                for (int f = 0; f < F; ++f) acc[f] = __fmaf_rn(m.val[f], wgt, acc[f]);
+                    for (int f = 0; f < F; ++f) acc[f] = __fmaf_rn(m.val[f], wgt, acc[f]);
+                } else {
+                    MagFootprint fp;
+                    fp.P = m.P;
+                    fp.A = m.A;
+                    fp.invC = m.invC;
+                    fp.w1 = m.w1;
+                    fp.zoff = m.zoff;
+                    fp.minAB = m.minAB;
+                    fp.hC = m.hC;
+                    fp.sigma = m.sigma;
+                    fp.wscale = m.wscale;
+                    const float wgt = mag_weight_x(fp, (float)(s - fp.P), B);
+#pragma unroll
+                    for (int f = 0; f < F; ++f) acc[f] = __fmaf_rn(m.val[f], wgt, acc[f]);
+                }
             }
             __syncthreads();
         }
@@ -531,7 +610,7 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK, 5) cbp_mag_fpw_kernel(MagParams 
 // order in shared memory.
 constexpr int MAG_BP_VG = MAG_BP_BLOCK / 32;
 
-template <int F>
+template <int F, bool PREC = false>
 __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
 {
     extern __shared__ float red[];  // VG > 1: [VG][F][MAG_BP_BLOCK / VG] (none for VG = 1: the L1 keeps it)
@@ -575,7 +654,7 @@ __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
     for (int q = 0; q < F; ++q) acc[q] = 0.0f;
     for (int vl = vg; valid && vl < p.view_count; vl += VG) {
         const double2 cs = p.view_cs[p.view_begin + vl];
-        const MagFootprint fp = mag_footprint(g, cs.x, cs.y, kx, ky);
+        const MagFootprint fp = PREC ? mag_footprint_prec(g, cs.x, cs.y, kx, ky) : mag_footprint(g, cs.x, cs.y, kx, ky);
         const double jc = fp.P * inv_pitch + g.cs, jw = (double)fp.sigma * inv_pitch + 1e-3;
         const double jlo = fmax(jc - jw, -1.0), jhi = fmin(jc + jw, (double)g.n_det);
         const int ja = max(0, (int)ceil(jlo)), jb = min(g.n_det - 1, (int)floor(jhi));
@@ -589,7 +668,7 @@ __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
         }
         double sj = mag_bin_s(g, ja);
         for (int j = ja; j <= jb; ++j, sj += g.pitch) {
-            const float wgt = mag_weight_x(fp, (float)(sj - fp.P), B);
+            const float wgt = PREC ? mag_weight_prec(fp, sj - fp.P, B) : mag_weight_x(fp, (float)(sj - fp.P), B);
 #pragma unroll
             for (int q = 0; q < F; ++q) {
                 if (q < 4 || !diag) acc[q] = __fmaf_rn(__ldg(yq[q] + (q >= 4 ? -j : j)), wgt, acc[q]);

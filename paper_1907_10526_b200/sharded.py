@@ -114,9 +114,19 @@ def back_sharded(geom, sino_local, shard: Shard, image=None, group=None, dst: Op
                  back_dihedral: Callable = _cbp.back_dihedral, stream=None):
     """c = sum_g A_g^T y_g: back-projects this rank's views, then sums the
     partial images over the group (all_reduce, or reduce to `dst`)."""
+    import contextlib
+
     import torch
     import torch.distributed as dist
     rank, world = _rank_world(group)
+    # the zero fill and the collective run on the BP's stream (NCCL enqueues on
+    # torch's current stream: a different `stream` would let it read the
+    # partial image before the BP has written it)
+    on_bp_stream = contextlib.nullcontext()
+    if stream is not None and isinstance(image if image is not None else sino_local, torch.Tensor) and \
+            (image if image is not None else sino_local).is_cuda:
+        s = stream if isinstance(stream, torch.cuda.Stream) else torch.cuda.ExternalStream(int(stream))
+        on_bp_stream = torch.cuda.stream(s)
     if shard.count > 0:
         if shard.mode == "orbit":
             image = back_orbit(geom, sino_local, shard.begin, image=image, stream=stream)
@@ -124,16 +134,17 @@ def back_sharded(geom, sino_local, shard: Shard, image=None, group=None, dst: Op
             image = back_dihedral(geom, sino_local, shard.begin, shard.count, image=image, stream=stream)
         else:
             image = back(geom, sino_local, image, view_begin=shard.begin, stream=stream)
-    elif image is not None:
-        image[...] = 0
-    else:
+    elif image is None:
         raise ValueError("a rank without views needs an image buffer to receive the sum")
-    if world > 1:
-        t = image if isinstance(image, torch.Tensor) else torch.from_numpy(image)
-        if dst is None:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-        else:
-            dist.reduce(t, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    with on_bp_stream:
+        if shard.count == 0:
+            image[...] = 0
+        if world > 1:
+            t = image if isinstance(image, torch.Tensor) else torch.from_numpy(image)
+            if dst is None:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            else:
+                dist.reduce(t, dst=dst, op=dist.ReduceOp.SUM, group=group)
     return image
 
 

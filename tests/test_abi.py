@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     L = ctypes.CDLL(cbp.LIB_PATH)
     for name in _declared_functions():
         assert hasattr(L, name), name
-    assert cbp.version() == 130
+    assert cbp.version() == 140
     assert cbp.strerror(0) == "ok"
     assert "invalid" in cbp.strerror(-1)
     assert cbp.strerror(12345) == "unknown error"
@@ -133,3 +133,59 @@ def test_fuzz_draws_are_valid_scanners():
     for s in range(160):
         g = draw(s)[0]
         assert cbp.validate(g) == cbp.CBP_OK, (s, g)
+
+
+def test_narrow_ratio_bounds_tau_prime():
+    """cbp_narrow_ratio is a lower bound on tau'/h over the (view, bin, pixel)
+    triples with a nonzero weight, checked against the
+    oracle's explicit Eq. 13 construction (oracle.effective_blur) at the
+    pixels whose support the bin ray crosses."""
+    import oracle as O
+    rng = np.random.default_rng(5)
+    for _ in range(12):
+        kind = int(rng.integers(0, 3))
+        n = int(rng.integers(4, 24))
+        h = float(rng.uniform(0.3, 2.0))
+        R = n * h / np.sqrt(2.0)
+        sid = float(R * rng.uniform(1.1, 5.0))
+        sdd = float(sid * rng.uniform(1.0, 2.5))
+        pitch = float(rng.uniform(0.5, 2.0) * h)
+        g = dict(n=n, pixel=h, n_views=6, n_det=int(2 * sdd * np.tan(np.arcsin(R / sid)) / pitch) + 3,
+                 det_pitch=pitch, det_width=float(pitch * rng.uniform(0.01, 2.0)),
+                 sid=sid if kind != 1 else 0.0, sdd=sdd if kind != 1 else 0.0, kind=kind, model=0)
+        if kind == 2:
+            while cbp.validate(g) != cbp.CBP_OK and g["n_det"] > 1:
+                g["n_det"] -= 1
+        assert cbp.validate(g) == cbp.CBP_OK, g
+        bound = cbp.narrow_ratio(g)
+        assert bound > 0
+        worst = np.inf
+        for v in range(g["n_views"]):
+            th = O.view_angle(g, v)
+            for j in range(g["n_det"]):
+                s = O.bin_center(g, j)
+                for r in range(n):
+                    for c in range(n):
+                        k = O.pixel_center(g, r, c)
+                        if O.weight(g, th, s, k) != 0.0:
+                            worst = min(worst, O.effective_blur(g, th, s, k) / h)
+        assert worst >= 0.99 * bound, (g, worst, bound)
+
+
+def test_validate_rejects_bins_below_the_precise_range():
+    g = W.geometry("1")
+    assert cbp.precise_mode(g) == 0 and cbp.narrow_ratio(g) > 0.25
+    g["det_width"] = 1e-5 * g["pixel"]
+    assert cbp.narrow_ratio(g) < 1e-4
+    assert cbp.validate(g) == cbp.CBP_EINVAL
+    g["det_width"] = 1e-3 * g["pixel"]
+    assert cbp.validate(g) == cbp.CBP_OK and cbp.precise_mode(g) == 1
+
+
+def test_precise_mode_env_override(monkeypatch):
+    g = W.geometry("1")
+    monkeypatch.setenv("CBP_PRECISE", "1")
+    assert cbp.precise_mode(g) == 1
+    g["det_width"] = 1e-3 * g["pixel"]
+    monkeypatch.setenv("CBP_PRECISE", "0")
+    assert cbp.precise_mode(g) == 0

@@ -65,17 +65,43 @@ def test_random_scanner_parity(torch_cuda, seed):
     got = _fp(torch_cuda, g, imgs, view_begin=v0, view_count=nv)
     if np.abs(want).max() == 0.0:  # the bins miss the image entirely: exact zeros
         assert not got.any(), what
-    elif np.abs(want).max() < 1e-2 * g["pixel"]:
-        # only support-edge tails reach the bins (max|y| far below a pixel's chord):
-        # the max-normalised metric is meaningless; FP32's absolute accuracy is the bar
-        assert np.abs(got - want).max() <= 1e-6 * g["pixel"], what
     else:
-        _assert_parity(got, want, "FP " + what)
+        _assert_parity_or_tail(got, want, _mass(imgs, batch), g["pixel"], "FP " + what)
     y = W.random_sino(nv, g["n_det"], 600 + seed, batch=batch) if batch > 1 else \
         W.random_sino(nv, g["n_det"], 600 + seed)
     want_b = O.back(g, y, view_begin=v0)
     if np.abs(want_b).max() == 0.0:
         assert not _bp(torch_cuda, g, y, view_begin=v0).any(), what
     else:
-        _assert_parity(_bp(torch_cuda, g, y, view_begin=v0), want_b, "BP " + what)
+        _assert_parity_or_tail(_bp(torch_cuda, g, y, view_begin=v0), want_b, _mass(y, batch), g["pixel"],
+                               "BP " + what)
+
+
+# Ledger #23: outputs that see only support-edge tails.  Each
+# output is a sum of weights times inputs, |dy_j| <= max|dW| sum_k |c_k|, and
+# the FP32 weight's absolute error is bounded relative to the LARGEST weight,
+# not to the weight itself: |dW| <= DELTA_W W_max with W_max = h^2 max M <=
+# h^2 / A <= sqrt(2) h (A = max|zeta| >= h / sqrt 2; the magnified model's
+# h^2 m / A obeys the same bound since m / |grad P| = 1), DELTA_W = 1e-6 (twice
+# the pinned 5e-7 of tests/test_weight_form.py).  So when max|y| < 1e4
+# eps_abs, eps_abs = DELTA_W sqrt(2) h sum|inputs| per slice, the 1e-4
+# max-normalised bar would demand more than FP32 weights can give, and the
+# bar is the derived absolute bound itself.  Everywhere else the bar of
+# test_gpu_parity.py applies unchanged.
+DELTA_W = 1e-6
+
+
+def _mass(x, batch):
+    """sum of |inputs| per slice, the largest slice's"""
+    x = np.abs(np.asarray(x, dtype=np.float64))
+    return float(x.reshape(batch, -1).sum(axis=1).max()) if batch > 1 else float(x.sum())
+
+
+def _assert_parity_or_tail(got, want, mass, h, what):
+    eps_abs = DELTA_W * np.sqrt(2.0) * h * mass
+    if np.abs(want).max() < 1e4 * eps_abs:
+        err = np.abs(np.asarray(got, np.float64) - want).max()
+        assert err <= eps_abs, f"{what}: tail case, max|dy| {err:.3e} > eps_abs {eps_abs:.3e}"
+    else:
+        _assert_parity(got, want, what)
 

@@ -1,0 +1,126 @@
+"""Narrow bins (tau / h down to 0.01): the CUDA path against
+the FP64 oracle at the parity bar, for every scanner kind and weight model.
+
+The weight's ramps are tau' + min|zeta| wide (Eq. 14); on views
+where a pixel edge runs along the ray min|zeta| -> 0, so an FP32 position
+error turns into a relative weight error ~1e-7 h / tau'.  Below
+cbp_narrow_ratio 0.02 the library switches to its precise mode (FP64
+positions and knots, smallest width innermost); these tests pin whichever
+path the library picks at tau/h = 0.01, 0.02, 0.05 (tau'/h 0.004 - 0.05), on full scans (8 views:
+the four axis-aligned views where min|zeta| = 0 at the central bin, and the
+diagonals) and on view ranges, plus the two draws of tools/fuzz_wide.py that
+exposed the FP32 limit (seeds 997 and 2009), and the precise mode forced on
+at the configs' normal widths."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1907_10526_b200 as cbp
+import workloads as W
+
+from tests.test_gpu_parity import _assert_parity, _bp, _fp, torch_cuda  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+
+def _narrow(kind, model, tau_h, n=40, n_views=8):
+    h = 1.0
+    R = n * h / np.sqrt(2.0)
+    if kind == cbp.PARALLEL:
+        pitch = h
+        n_det = int(2 * R / pitch) + 3
+        sid = sdd = 0.0
+    else:
+        sid, sdd, pitch = 100.0, 200.0, 2.0  # magnification 2: a pixel covers ~1 bin
+        n_det = int(2 * sdd * np.tan(np.arcsin(R / sid)) / pitch) + 3
+    return dict(n=n, pixel=h, n_views=n_views, n_det=n_det, det_pitch=pitch, det_width=tau_h * h,
+                sid=sid, sdd=sdd, kind=kind, model=model)
+
+
+CASES = [(k, m, t) for k in (cbp.FAN_FLAT, cbp.PARALLEL, cbp.FAN_ARC) for m in (cbp.MODEL_CNSF, cbp.MODEL_MAG)
+         for t in (0.01, 0.02, 0.05)]
+
+
+@pytest.mark.parametrize("kind,model,tau_h", CASES)
+def test_narrow_bins_parity(torch_cuda, kind, model, tau_h):
+    g = _narrow(kind, model, tau_h)
+    assert cbp.validate(g) == cbp.CBP_OK, g
+    assert cbp.precise_mode(g) == (1 if cbp.narrow_ratio(g) < 0.02 else 0)
+    what = f"kind {kind} model {model} tau/h {tau_h}"
+    img = W.random_image(g["n"], 41)
+    _assert_parity(_fp(torch_cuda, g, img), O.forward(g, img), "FP " + what)
+    y = W.random_sino(g["n_views"], g["n_det"], 42)
+    _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), "BP " + what)
+
+
+@pytest.mark.parametrize("kind", [cbp.FAN_FLAT, cbp.PARALLEL, cbp.FAN_ARC])
+def test_narrow_bins_view_range_and_batch(torch_cuda, kind):
+    # 12 views (0 and 90 degrees among them), views 2..8, an odd grid, a batch of 2
+    g = _narrow(kind, cbp.MODEL_CNSF, 0.01, n=37, n_views=12)
+    imgs = W.random_image(g["n"], 43, batch=2)
+    _assert_parity(_fp(torch_cuda, g, imgs, view_begin=2, view_count=7),
+                   O.forward(g, imgs, view_begin=2, view_count=7), f"FP range kind {kind}")
+    y = W.random_sino(7, g["n_det"], 44, batch=2)
+    _assert_parity(_bp(torch_cuda, g, y, view_begin=2), O.back(g, y, view_begin=2), f"BP range kind {kind}")
+
+
+def test_narrow_bins_shards_sum_to_full(torch_cuda):
+    # orbit and dihedral shards fall back to view blocks in the precise mode
+    torch = torch_cuda
+    g = _narrow(cbp.FAN_FLAT, cbp.MODEL_CNSF, 0.02, n=40, n_views=16)
+    img = torch.from_numpy(W.random_image(g["n"], 45)).cuda()
+    full = cbp.forward(g, img)
+    sino = torch.zeros_like(full)
+    for b0, nb in ((0, 1), (1, 2)):  # base views [0, 2] of n_views/8 + 1 = 3
+        cbp.forward_dihedral(g, img, b0, nb, sino=sino)
+    torch.cuda.synchronize()
+    want = O.forward(g, img.cpu().numpy())
+    _assert_parity(sino.cpu().numpy(), want, "FP dihedral shards")
+    _assert_parity(full.cpu().numpy(), want, "FP full")
+    y = torch.from_numpy(W.random_sino(g["n_views"], g["n_det"], 46)).cuda()
+    acc = cbp.back_dihedral(g, y, 0, 1)
+    cbp.back_dihedral(g, y, 1, 2, image=acc, accumulate=True)
+    _assert_parity(acc.cpu().numpy(), O.back(g, y.cpu().numpy()), "BP dihedral shards")
+    orb = cbp.forward_orbit(g, img, 1, 2)
+    rows = [1, 2, 5, 6, 9, 10, 13, 14]  # b + q n_views/4 for b in 1..2
+    _assert_parity(orb.reshape(8, -1).cpu().numpy(), want[rows], "FP orbit shard")
+
+
+# tools/fuzz_wide.py draws that exceeded the bar before the precise mode:
+# seed 997: flat detector, tau/h 0.014, a half-turn view (BP max-normalised 1.6e-4);
+# seed 2009: arc, one 1.49 mm pixel, a source 1.14 mm away, tau/h 0.009 (FP relL2 1.06e-5)
+FUZZ_WIDE = {
+    997: (dict(n=61, pixel=2.2618980132052817, n_views=2, n_det=669, det_pitch=1.503718837780938,
+               det_width=0.032364225680945026, sid=1220.1712432987902, sdd=4649.11752281311, kind=0, model=0),
+          4, 1, 1),
+    2009: (dict(n=1, pixel=1.4937332023018055, n_views=4, n_det=19, det_pitch=0.6050390134164245,
+                det_width=0.013130810019606656, sid=1.1440913447056926, sdd=3.644005974487285, kind=2, model=0),
+           1, 2, 2),
+}
+
+
+@pytest.mark.parametrize("seed", sorted(FUZZ_WIDE))
+def test_fuzz_wide_regressions(torch_cuda, seed):
+    g, batch, v0, nv = FUZZ_WIDE[seed]
+    assert cbp.validate(g) == cbp.CBP_OK
+    n = g["n"]
+    imgs = W.random_image(n, seed, batch=batch) if batch > 1 else W.random_image(n, seed)
+    y = W.random_sino(nv, g["n_det"], seed + 7, batch=batch) if batch > 1 else W.random_sino(nv, g["n_det"], seed + 7)
+    _assert_parity(_fp(torch_cuda, g, imgs, view_begin=v0, view_count=nv),
+                   O.forward(g, imgs, view_begin=v0, view_count=nv), f"FP fuzz_wide {seed}")
+    _assert_parity(_bp(torch_cuda, g, y, view_begin=v0), O.back(g, y, view_begin=v0), f"BP fuzz_wide {seed}")
+
+
+@pytest.mark.parametrize("kind,model", [(k, m) for k in (0, 1, 2) for m in (0, 1)])
+def test_precise_mode_forced_at_normal_widths(torch_cuda, monkeypatch, kind, model):
+    # the precise path is a full projector in its own right: config-1 widths
+    g = dict(W.geometry("1"), kind=kind, model=model)
+    if kind == cbp.PARALLEL:
+        g.update(sid=0.0, sdd=0.0, det_pitch=1.0, det_width=1.0, n_det=96)
+    monkeypatch.setenv("CBP_PRECISE", "1")
+    assert cbp.precise_mode(g) == 1
+    img = W.shepp_logan(g["n"])
+    _assert_parity(_fp(torch_cuda, g, img), O.forward(g, img), f"FP precise kind {kind} model {model}")
+    y = W.random_sino(g["n_views"], g["n_det"], 47)
+    _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), f"BP precise kind {kind} model {model}")
+    assert cbp.adjoint_check(g, seed=3) <= 1e-5

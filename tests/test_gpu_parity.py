@@ -95,29 +95,63 @@ def test_adjoint_config1(torch_cuda):
 
 
 # ---------------------------------------------- full sizes (sampled oracle)
-@pytest.mark.parametrize("cfg,stride", [("2", 45), ("3", 180), ("5", 719)])
-def test_forward_full_size_sampled_views(torch_cuda, cfg, stride):
+def _frame_views(n_views, bases):
+    """the views of base views `bases` under the 8 frames of the dihedral
+    symmetry: every octant of the scan, each frame of the
+    symmetric kernels' output"""
+    N = n_views
+    return sorted({((N - b if m else b) + q * (N // 4)) % N for b in bases for m in (0, 1) for q in range(4)})
+
+
+# base views per config: the octant's ends (v = 0, N/8, the axis and diagonal
+# views), its first view and interior ones -> 32-40 views over the 8 frames
+FRAME_BASES = {"2": (0, 1, 37, 61, 90), "3": (0, 1, 71, 133, 180), "5": (0, 1, 97, 211, 359, 360)}
+
+
+@pytest.mark.parametrize("cfg", ["2", "3", "5"])
+def test_forward_full_size_sampled_views(torch_cuda, cfg):
     g = W.geometry(cfg)
     img = W.shepp_logan(g["n"])
     y = _fp(torch_cuda, g, img)  # all views, the launch bench.py times
-    for v in range(0, g["n_views"], stride):
+    views = _frame_views(g["n_views"], FRAME_BASES[cfg])
+    assert len(views) >= 32
+    for v in views:
         _assert_parity(y[v], O.forward(g, img, view_begin=v, view_count=1)[0], f"FP cfg{cfg} v{v}")
     img_r = W.random_image(g["n"], 2)
     y = _fp(torch_cuda, g, img_r)
-    for v in range(7, g["n_views"], stride * 2):
+    for v in views[::3]:
         _assert_parity(y[v], O.forward(g, img_r, view_begin=v, view_count=1)[0],
                        f"FP cfg{cfg} rand v{v}")
 
 
-@pytest.mark.parametrize("cfg,npix", [("2", 96), ("3", 24), ("5", 8)])
-def test_back_full_size_sampled_pixels(torch_cuda, cfg, npix):
+def _bp_sample_pixels(n, nrand, seed=11):
+    """BP check pixels: corners and edge midpoints of 32 x 32 tiles (the BP's
+    tile anchors and ragged borders), both diagonals (the dihedral frames'
+    fixed lines), the image corners, and random pixels"""
+    rng = np.random.default_rng(seed)
+    T = 32
+    tiles = (n + T - 1) // T
+    pts = set()
+    for t in rng.choice(tiles * tiles, size=min(tiles * tiles, 16), replace=False):
+        r0, c0 = (t // tiles) * T, (t % tiles) * T
+        r1, c1 = min(r0 + T, n) - 1, min(c0 + T, n) - 1
+        rm, cm = (r0 + r1) // 2, (c0 + c1) // 2
+        pts |= {(r0, c0), (r0, c1), (r1, c0), (r1, c1), (r0, cm), (r1, cm), (rm, c0), (rm, c1)}
+    d = np.linspace(0, n - 1, 128).astype(int)
+    pts |= {(int(i), int(i)) for i in d} | {(int(i), int(n - 1 - i)) for i in d}
+    pts |= {(0, 0), (0, n - 1), (n - 1, 0), (n - 1, n - 1), (n // 2, n // 2)}
+    pts |= {(int(r), int(c)) for r, c in rng.integers(0, n, (nrand, 2))}
+    pts = sorted(pts)
+    return np.array([p[0] for p in pts]), np.array([p[1] for p in pts])
+
+
+@pytest.mark.parametrize("cfg,nrand", [("2", 96), ("3", 128), ("5", 128)])
+def test_back_full_size_sampled_pixels(torch_cuda, cfg, nrand):
     g = W.geometry(cfg)
     y = W.random_sino(g["n_views"], g["n_det"], 103)
     c = _bp(torch_cuda, g, y)
-    rng = np.random.default_rng(11)
-    n = g["n"]
-    rows = np.concatenate([[0, n - 1, n // 2, 0], rng.integers(0, n, npix)])
-    cols = np.concatenate([[0, n - 1, n // 2, n - 1], rng.integers(0, n, npix)])
+    rows, cols = _bp_sample_pixels(g["n"], nrand)
+    assert len(rows) >= (512 if cfg == "5" else 256)
     ref = O.back_pixels(g, y, rows, cols)
     _assert_parity(c[rows, cols], ref, f"BP cfg{cfg} sampled")
     # invariant at any size: BP is nonnegative for a nonnegative sinogram

@@ -96,3 +96,57 @@ def test_outside_support_residue_is_rounding_level():
         s = (A + B + C) / 2
         x = np.sign(rng.uniform(-1, 1)) * rng.uniform(s, s + 3 * A)
         assert abs(clamp_form(x, A, B, C, np.float32)) <= 4e-7 * (s + 3 * A) / (A * B)
+
+
+def precise_form(x, A, B, Cz):
+    """The kernels' precise mode (cbp_common.cuh cnsf_prec) in
+    numpy: s' = x and A in FP64; b = max(tau', C), c = min(tau', C) (the
+    smallest width innermost); the four knot arguments formed in FP64 and
+    rounded once to FP32; everything else FP32.  Returns M."""
+    f32 = np.float32
+    B, Cz = f32(B), f32(Cz)
+    b, c = max(B, Cz), min(B, Cz)
+    D = float(x) + 0.5 * (float(A) + float(f32(b - c)))
+    k = [f32(D), f32(D - float(b)), f32(D - A), f32((D - A) - float(b))]
+    with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
+        ic = f32(1) / c if c > 0 else f32(np.inf)
+        t = [f32(0) if np.isnan(u) else f32(min(max(u, f32(0)), f32(1)))
+             for u in (f32(kk * ic + f32(1)) for kk in k)]
+    T = f32(f32(f32(t[0] * t[0]) - f32(t[1] * t[1])) - f32(f32(t[2] * t[2]) - f32(t[3] * t[3])))
+    trap = max(f32(0), min(k[0], min(f32(A), b), -k[3]))
+    num = f32(trap + f32(f32(0.5) * c) * T)
+    return float(num / b) / A
+
+
+def _near_knot_cases(rng, n, brel):
+    """x within a ramp width of one of the 8 knots +-A/2 +-B/2 +-C/2 (where a
+    position error matters), C from 0 to A."""
+    for _ in range(n):
+        A = rng.uniform(0.7, 1.0)
+        C = A * rng.choice([0.0, 1e-3, 1e-2, 0.1, 0.5, 1.0]) * rng.uniform(0, 1)
+        B = A * brel * rng.uniform(0.5, 1.0)
+        knots = [sa * A / 2 + sb * B / 2 + sc * C / 2 for sa in (-1, 1) for sb in (-1, 1) for sc in (-1, 1)]
+        x = rng.choice(knots) + rng.uniform(-1, 1) * 0.5 * max(B, C)
+        yield x, A, B, C
+
+
+def test_precise_form_holds_for_narrow_bins():
+    # <= 2e-7 of the peak from tau'/A = 3 down to 1e-4 (cbp_validate's floor)
+    rng = np.random.default_rng(11)
+    for brel in (3.0, 0.3, 1e-2, 1e-3, 1e-4):
+        worst = 0.0
+        for x, A, B, C in _near_knot_cases(rng, 1500, brel):
+            ref = O.box_spline([A, B, C], x) if C >= 1e-6 * A else O.box_spline([A, B], x)
+            worst = max(worst, abs(precise_form(x, A, B, C) - ref) * A)
+        assert worst <= 2.5e-7, (brel, worst)
+
+
+def test_fp32_position_limits_the_standard_form():
+    # the reason for the precise mode: the standard form fed an FP32 s' (one
+    # rounding, the best an FP32 position can do) errs ~1e-7 A / tau' near knots
+    rng = np.random.default_rng(12)
+    worst = 0.0
+    for x, A, B, C in _near_knot_cases(rng, 1500, 1e-2):
+        ref = O.box_spline([A, B, C], x) if C >= 1e-6 * A else O.box_spline([A, B], x)
+        worst = max(worst, abs(clamp_form(np.float32(x), A, B, C, np.float32) - ref) * A)
+    assert worst > 5e-6

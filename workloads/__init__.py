@@ -72,8 +72,20 @@ FIG7 = dict(n=128, pixel=1.0, n_views=360, n_det=409, det_pitch=1.0, det_width=0
             sdd=400.0)
 
 
+# Extra bench workloads for the general (non-symmetric) path and the paper's
+# own timing shapes: config 2's geometry with 721 views (no
+# 4- or 8-fold view symmetry: the direct kernels), and P:512-515's all-ones
+# shapes at 256, 512 and 1024 mm.
+EXTRA: dict[str, dict] = {
+    "2v721": _fan(512, 721, 1024),
+    "p256": dict(PAPER_TIMING[256]),
+    "p512": dict(PAPER_TIMING[512]),
+    "p1024": dict(PAPER_TIMING[1024]),
+}
+
+
 def geometry(name: str) -> dict:
-    return dict(CONFIGS[name])
+    return dict(CONFIGS[name] if name in CONFIGS else EXTRA[name])
 
 
 # ---------------------------------------------------------------------------
