@@ -491,8 +491,8 @@ def main():
 
         def e2e_sino_step():  # the same pair with the sinogram through host memory too
             hs = h_sino.view(nv, ns) if orbit else h_sino
-            cbp.forward(g, h_img, hs, view_begin=sh.begin if args.views else 0)
-            cbp.back(g, hs, h_out, view_begin=sh.begin if args.views else 0)
+            cbp.forward(g, h_img, hs, view_begin=sh.begin, view_count=sh.count)
+            cbp.back(g, hs, h_out, view_begin=sh.begin)
 
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         unpiped = None

@@ -750,8 +750,15 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     const int vpg = (nv + G - 1) / G;
     const size_t plane = (size_t)g.n * g.n;
     float* part = nullptr;
-    const bool mc = accumulate == CBP_ACC_MULTIMEM;  // always through the reduce kernel
-    if (G > 1 || sym || mc) {
+    // CBP_ACC_MULTIMEM: by default the BP's epilogue adds every finished tile
+    // (each frame, each view group) into the multicast image itself, so the
+    // switch's reduction overlaps the tiles still computing (G x frames more
+    // multicast traffic than one add of the reduced image); CBP_MC_REDUCE=1
+    // sums the planes locally first and adds once from cbp_reduce_kernel
+    static const bool mc_reduce = getenv("CBP_MC_REDUCE") != nullptr;
+    const bool mc_fused = accumulate == CBP_ACC_MULTIMEM && !mc_reduce;
+    const bool mc = accumulate == CBP_ACC_MULTIMEM && mc_reduce;  // through the reduce kernel
+    if (!mc_fused && (G > 1 || sym || mc)) {
         int rc = scratch_alloc((void**)&part, sizeof(float) * plane * batch * G * (sym ? images : 1), stream);
         if (rc != CBP_OK) return rc;
     }
@@ -771,7 +778,8 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     P.g = to_dev(g);
     P.t = t;
     P.sino = sino;
-    P.out = (G > 1 || sym || mc) ? part : img;
+    P.out = mc_fused ? img : ((G > 1 || sym || mc) ? part : img);
+    P.mc_fused = mc_fused ? 1 : 0;
     P.sym_stride = symmode == 4 ? nv : 0;
     P.sym_mode = symmode;
     P.images = sym ? images : 1;
@@ -780,7 +788,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     P.groups = (G > 1 || sym || mc) ? G : 1;
     P.views_per_group = vpg;
     P.batch = batch;
-    P.accumulate = (G == 1 && !sym && !mc && accumulate) ? 1 : 0;
+    P.accumulate = (G == 1 && !sym && !mc && !mc_fused && accumulate) ? 1 : 0;
     dim3 grid(tiles, tiles, G * SG);
 #ifdef CBP_DEBUG_CHECKS
     fprintf(stderr, "launch_bp S=%d G=%d vpg=%d grid=%d,%d,%d smem=%zu\n", S, G, vpg, grid.x, grid.y,
@@ -792,7 +800,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     fprintf(stderr, "bp kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
 #endif
     if (hdrs_owned) cudaFreeAsync(hdrs_owned, stream);
-    if (sym || G > 1 || mc) {
+    if (!mc_fused && (sym || G > 1 || mc)) {
         // symmetric: the G x S frame planes are already in output orientation
         const size_t count = sym ? plane : plane * batch;
         const int planes = sym ? G * batch : G;

@@ -57,6 +57,12 @@ struct BPParams {
     // [images][groups][8] out)
     int sym_mode;
     int images;
+    // 1: the view-sharded all-reduce fused into the epilogue (CBP_ACC_MULTIMEM):
+    // `out` is a multicast image address and every CTA adds its finished tile of
+    // every frame / view group with multimem.red (no partial planes, no reduce
+    // kernel): the NVSwitch sums the tiles of all CTAs and ranks while the
+    // remaining tiles still compute
+    int mc_fused;
 };
 
 constexpr int BP_TILE = 32;       // pixels per tile side
@@ -794,7 +800,8 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
         // symmetric frames: plane (sg groups + grp) frames + q; batch: (grp batch + b)
         const size_t pi = fsym ? ((size_t)sg * P.groups + grp) * P.batch + q
                                : (P.groups > 1 ? (size_t)grp * P.batch + b : (size_t)b);
-        float* out = P.out + pi * plane;
+        // fused multicast reduction: every frame of every view group adds into the image
+        float* out = P.mc_fused ? P.out + (fsym ? (size_t)sg : (size_t)b) * plane : P.out + pi * plane;
         const int4 e0 = ep[q][0], e1 = ep[q][1];
         const int OR = e0.x, OC = e0.y, oh = e0.z, ow = e0.w, s0 = e1.x, sc = e1.y, sr = e1.z;
         const bp_acc_t<S>* a = acc_s + q * BP_TILE * LD;
@@ -805,7 +812,11 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                 const int si = s0 + r * sr + c * sc;
                 const float4 v = make_float4((float)a[si], (float)a[si + sc], (float)a[si + 2 * sc],
                                              (float)a[si + 3 * sc]);
-                *reinterpret_cast<float4*>(out + (size_t)(OR + r) * n + OC + c) = v;
+                float4* o = reinterpret_cast<float4*>(out + (size_t)(OR + r) * n + OC + c);
+                if (P.mc_fused)
+                    mc_red_add4(o, v);
+                else
+                    *o = v;
             }
         } else {
             for (int i = tid; i < BP_TILE * BP_TILE; i += BP_THREADS) {
@@ -813,7 +824,10 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                 if (r < oh && c < ow) {
                     float* o = out + (size_t)(OR + r) * n + OC + c;
                     const float v = (float)a[s0 + r * sr + c * sc];
-                    *o = acc_out ? *o + v : v;
+                    if (P.mc_fused)
+                        mc_red_add(o, v);
+                    else
+                        *o = acc_out ? *o + v : v;
                 }
             }
         }

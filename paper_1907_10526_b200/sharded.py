@@ -109,11 +109,40 @@ def forward_sharded(geom, image, group=None, forward: Callable = _cbp.forward,
     return forward(geom, image, view_begin=sh.begin, view_count=sh.count, stream=stream), sh
 
 
+class MulticastImage:
+    """The image buffer of the fused reduction (CBP_ACC_MULTIMEM): one n x n
+    FP32 buffer per rank in torch symmetric memory, bound to an NVLink
+    multicast object.  The BP adds every finished tile into all ranks' copies
+    through ``multicast_ptr`` (the NVSwitch sums them), so no NCCL call follows
+    the BP.  Raises RuntimeError where the system has no multicast support
+    (e.g. a single GPU, or no NVSwitch)."""
+
+    def __init__(self, n: int, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        group = group or dist.group.WORLD
+        self.buf = symm_mem.empty((n, n), dtype=torch.float32, device=device)
+        self.hdl = symm_mem.rendezvous(self.buf, group)
+        self.mc = int(self.hdl.multicast_ptr) if self.hdl.has_multicast_support() else 0
+        if not self.mc:
+            raise RuntimeError("no NVLink multicast support for this group")
+
+    def barrier(self):
+        self.hdl.barrier(channel=0)
+
+
 def back_sharded(geom, sino_local, shard: Shard, image=None, group=None, dst: Optional[int] = None,
                  back: Callable = _cbp.back, back_orbit: Callable = _cbp.back_orbit,
-                 back_dihedral: Callable = _cbp.back_dihedral, stream=None):
+                 back_dihedral: Callable = _cbp.back_dihedral, stream=None,
+                 multimem: Optional[MulticastImage] = None):
     """c = sum_g A_g^T y_g: back-projects this rank's views, then sums the
-    partial images over the group (all_reduce, or reduce to `dst`)."""
+    partial images over the group (all_reduce, or reduce to `dst`).  With
+    `multimem` the sum is fused into the BP instead (CBP_ACC_MULTIMEM: every
+    rank's BP adds its tiles into all ranks' ``multimem.buf`` through the
+    multicast address; barriers before and after) and ``multimem.buf`` is
+    returned."""
     import contextlib
 
     import torch
@@ -123,10 +152,18 @@ def back_sharded(geom, sino_local, shard: Shard, image=None, group=None, dst: Op
     # torch's current stream: a different `stream` would let it read the
     # partial image before the BP has written it)
     on_bp_stream = contextlib.nullcontext()
-    if stream is not None and isinstance(image if image is not None else sino_local, torch.Tensor) and \
-            (image if image is not None else sino_local).is_cuda:
+    ref = image if image is not None else sino_local
+    if stream is not None and isinstance(ref, torch.Tensor) and ref.is_cuda:
         s = stream if isinstance(stream, torch.cuda.Stream) else torch.cuda.ExternalStream(int(stream))
         on_bp_stream = torch.cuda.stream(s)
+    if multimem is not None:
+        with on_bp_stream:
+            multimem.buf.zero_()
+            multimem.barrier()  # every copy is zero before any rank adds
+            if shard.count > 0:
+                _cbp.back_multimem(geom, sino_local, multimem.mc, shard=shard, stream=stream)
+            multimem.barrier()  # every rank's adds have landed
+        return multimem.buf
     if shard.count > 0:
         if shard.mode == "orbit":
             image = back_orbit(geom, sino_local, shard.begin, image=image, stream=stream)

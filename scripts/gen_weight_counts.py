@@ -37,12 +37,12 @@ def per_view_counts(g, dihedral):
 def main(cfgs):
     data = json.load(open(OUT)) if os.path.exists(OUT) else {}
     data["_comment"] = ("nonzero (view, pixel, bin) weights per view, counted by "
-                        "oracle.count_weights (scripts/gen_weight_counts.py; configs 3 and 5: "
-                        "base views of the 8-fold symmetry, expanded over their orbits)")
+                        "oracle.count_weights (scripts/gen_weight_counts.py; configs 3, 5 and the "
+                        "paper shapes p*: base views of the 8-fold symmetry, expanded over their orbits)")
     for c in cfgs:
         g = W.geometry(c)
         t = time.time()
-        per_view = per_view_counts(g, dihedral=c in ("3", "5"))
+        per_view = per_view_counts(g, dihedral=c not in ("1", "2") and g["n_views"] % 8 == 0)
         data[c] = dict(geometry=g, per_view=per_view, total=sum(per_view),
                        per_view_pixel=sum(per_view) / (g["n"] ** 2 * g["n_views"]))
         print(c, sum(per_view), data[c]["per_view_pixel"], f"{time.time() - t:.1f}s", flush=True)
