@@ -36,6 +36,15 @@ def build_debug() -> str:
     return out
 
 
+def build_variant(out: str, defines: list[str]) -> str:
+    """an A/B build of the same sources with extra -D macros (tools/ab_time.py)"""
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", out, os.path.join(CSRC, "cbp.cu")]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(res.stderr[-3000:])
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     deps = sources() + [os.path.join(ROOT, "include", "cbp.h"), os.path.abspath(__file__)]
     stale = (not os.path.exists(LIB)) or any(os.path.getmtime(d) > os.path.getmtime(LIB)

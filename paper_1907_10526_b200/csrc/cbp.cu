@@ -395,6 +395,7 @@ int launch_fp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* img,
     Pm.batch = batch;
     Pm.sym_stride = 0;
     Pm.sym_mode = 0;
+    Pm.rot_rows = 0;
     rc = launch_fp_kernel<S, PREC>(Pm, nv, G, stream);
     cudaFreeAsync(pad, stream);
     return rc;
@@ -420,12 +421,22 @@ int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     const int P = fp_pad_width(g);
     const int np = g.n + 2 * P;
     const size_t plane = (size_t)np * np * 4;
+    // rot_rows (opt-in, CBP_ROTROWS=1): column-major rays are walked as
+    // row-major rays of the view a quarter turn on, so the transposed copy is
+    // not needed (half the pad kernel's writes and of the FP's image
+    // footprint).  Measured slower: config 2 FP 0.187 vs 0.177 ms, config 3
+    // 1.271 vs 1.231, config 5 9.50 vs 9.32 (a warp's rays near 45 degrees
+    // then walk two views' geometry: split access patterns)
+    static const bool rot = getenv("CBP_ROTROWS") != nullptr;
     float* pad = nullptr;
-    int rc = scratch_alloc((void**)&pad, sizeof(float) * 2 * plane, stream);
+    int rc = scratch_alloc((void**)&pad, sizeof(float) * (rot ? 1 : 2) * plane, stream);
     if (rc != CBP_OK) return rc;
-    float* padT = pad + plane;
+    float* padT = rot ? nullptr : pad + plane;
     dim3 pgrid((np + cbp::PAD_TILE - 1) / cbp::PAD_TILE, (np + cbp::PAD_TILE - 1) / cbp::PAD_TILE, 1);
-    cbp::cbp_pad_sym4_kernel<<<pgrid, dim3(cbp::PAD_TILE, 8), 0, stream>>>(img, pad, padT, g.n, P, np);
+    if (rot)
+        cbp::cbp_pad_sym4_kernel<false><<<pgrid, dim3(cbp::PAD_TILE, 8), 0, stream>>>(img, pad, padT, g.n, P, np);
+    else
+        cbp::cbp_pad_sym4_kernel<true><<<pgrid, dim3(cbp::PAD_TILE, 8), 0, stream>>>(img, pad, padT, g.n, P, np);
     ++g_launches;
     cbp::FPParams Pm;
     Pm.split = 0x7fffffff;
@@ -443,6 +454,7 @@ int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     Pm.batch = 4;
     Pm.sym_stride = stride ? stride : base_count;
     Pm.sym_mode = 4;
+    Pm.rot_rows = rot ? 1 : 0;
     if (count2 > 0) {  // a second block of base views (natural layout only), same pad, same launch
         Pm.split = base_count;
         Pm.view_begin2 = begin2;
@@ -490,6 +502,7 @@ int launch_fp_sym8(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     Pm.batch = 8;
     Pm.sym_stride = 0;
     Pm.sym_mode = 8;
+    Pm.rot_rows = 0;
     rc = launch_fp_kernel<8>(Pm, g.n_views / 8 + 1, 1, stream);
     cudaFreeAsync(pad, stream);
     return rc;
@@ -720,6 +733,158 @@ int get_headers(const cbp_geometry_t& g, const cbp::Tables& t, int32_t v0, int32
     return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
 }
 
+// ---- BP orbit clusters: representative tiles of the orbits
+// of the dihedral group on the T x T tile grid (n = 32 T), per device
+std::mutex g_orbit_mu;
+std::map<std::pair<int, int>, std::pair<int2*, int>> g_orbits;
+
+int get_orbit_reps(int T, const int2** out, int* count)
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return CBP_ECUDA;
+    std::lock_guard<std::mutex> lock(g_orbit_mu);
+    auto it = g_orbits.find({dev, T});
+    if (it == g_orbits.end()) {
+        std::vector<char> seen((size_t)T * T, 0);
+        std::vector<int2> reps;
+        for (int ty = 0; ty < T; ++ty)
+            for (int tx = 0; tx < T; ++tx) {
+                if (seen[(size_t)ty * T + tx]) continue;
+                reps.push_back(make_int2(tx, ty));
+                for (int q = 0; q < 8; ++q) {  // the same frames as frame_fwd on tile coordinates
+                    int r = ty, c = tx;
+                    if (q >> 2) r = T - 1 - r;
+                    for (int k = 0; k < (q & 3); ++k) {
+                        const int nr = T - 1 - c;
+                        c = r;
+                        r = nr;
+                    }
+                    seen[(size_t)r * T + c] = 1;
+                }
+            }
+        int2* d = nullptr;
+        if (cudaMalloc(&d, sizeof(int2) * reps.size()) != cudaSuccess ||
+            cudaMemcpy(d, reps.data(), sizeof(int2) * reps.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(d);
+            cudaGetLastError();
+            return CBP_ECUDA;
+        }
+        it = g_orbits.emplace(std::make_pair(dev, T), std::make_pair(d, (int)reps.size())).first;
+    }
+    *out = it->second.first;
+    *count = it->second.second;
+    return CBP_OK;
+}
+
+// The dihedral BP as clusters of 8 CTAs over tile orbits: each output tile is
+// summed from its orbit's frame accumulators through distributed shared
+// memory, so there are no frame planes (8 per image and view group: 32 MB per
+// launch at config 2, 128 MB at config 5) and, with one view group, no reduce
+// kernel.  n must be a multiple of BP_TILE (frames map tiles onto tiles).
+// Opt-in (CBP_ORBIT=1): measured slower than the frame planes -- config 2 BP
+// 0.286-0.329 ms (G = 1..4) vs 0.192 ms, config 5 11.44 vs 9.48 ms: a
+// cluster holds its 8 SM slots until its slowest member (the orbit's tiles
+// see the base views from different sides) and clusters pack the GPCs less
+// densely than single CTAs.
+bool use_orbit(const cbp_geometry_t& g)
+{
+    const char* e = getenv("CBP_ORBIT");  // read per call: the tests compare both paths
+    return e && e[0] == '1' && g.n % cbp::BP_TILE == 0;
+}
+
+int launch_bp_orbit(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img, int32_t v0,
+                    int32_t nv, int32_t accumulate, cudaStream_t stream, int images)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = cbp::bp_smem_bytes(8, false);
+    static std::once_flag attr[64];
+    static int per_sm[64];
+    std::call_once(attr[dev & 63], [smem, dev] {
+        cudaFuncSetAttribute(cbp::cbp_bp_kernel<8, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        cudaFuncSetAttribute(cbp::cbp_bp_kernel<8, false, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+        int k = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_bp_kernel<8, false, true>, cbp::BP_THREADS,
+                                                          smem) != cudaSuccess || k < 1)
+            k = 1;
+        per_sm[dev & 63] = k;
+    });
+    const int T = g.n / cbp::BP_TILE;
+    const int2* reps = nullptr;
+    int nrep = 0;
+    if (get_orbit_reps(T, &reps, &nrep) != CBP_OK) return CBP_ECUDA;
+    const int ctas = 8 * nrep;
+    // view groups: the fewest with >= 3 waves of resident CTAs (as bp_groups)
+    const char* genv = getenv("CBP_BP_GROUPS");  // tuning knob (read per call)
+    const int Gforce = genv ? atoi(genv) : 0;
+    const int slots = sms * per_sm[dev & 63];
+    const int gmax = std::max(1, std::min(nv / 8, 16));
+    int G = 1;
+    while (G < gmax && (double)ctas * G * images < 3.0 * slots) ++G;
+    if (Gforce > 0) G = std::max(1, std::min(Gforce, (int)nv));
+    const int vpg = (nv + G - 1) / G;
+    G = (nv + vpg - 1) / vpg;
+    const bool mc_fused = accumulate == CBP_ACC_MULTIMEM;  // (the reduce-kernel multimem path is not needed here)
+    const size_t plane = (size_t)g.n * g.n;
+    float* part = nullptr;
+    if (G > 1 && !mc_fused) {
+        int rc = scratch_alloc((void**)&part, sizeof(float) * plane * G * images, stream);
+        if (rc != CBP_OK) return rc;
+    }
+    cbp::BPParams P;
+    const cbp::BPHeader* hdrs = nullptr;
+    cbp::BPHeader* hdrs_owned = nullptr;
+    if (get_pair_order(&P.pairs) != CBP_OK || get_headers(g, t, v0, nv, stream, &hdrs, &hdrs_owned) != CBP_OK) {
+        if (part) cudaFreeAsync(part, stream);
+        return CBP_ECUDA;
+    }
+    P.hdrs = hdrs;
+    P.g = to_dev(g);
+    P.t = t;
+    P.sino = sino;
+    P.out = part ? part : img;
+    P.view_begin = v0;
+    P.view_count = nv;
+    P.groups = G;
+    P.views_per_group = vpg;
+    P.batch = 8;
+    P.accumulate = (G == 1 && accumulate == CBP_ACC_ADD) ? 1 : 0;
+    P.sym_stride = 0;
+    P.sym_mode = 8;
+    P.images = images;
+    P.mc_fused = mc_fused ? 1 : 0;
+    P.orbit_reps = reps;
+    P.orbit_T = T;
+    static const bool no_pdl = getenv("CBP_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas, 1, G * images);
+    cfg.blockDim = dim3(cbp::BP_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 8;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, cbp::cbp_bp_kernel<8, false, true>, P);
+    ++g_launches;
+    if (hdrs_owned) cudaFreeAsync(hdrs_owned, stream);
+    if (part) {
+        const int blocks = (int)std::min<size_t>((plane / 4 + 255) / 256, (size_t)sms * 8 / images + 1);
+        launch_pdl(cbp::cbp_reduce_kernel, dim3(std::max(blocks, 1), images), dim3(256), 0, stream,
+                   (const float*)part, img, plane, G, accumulate == CBP_ACC_ADD ? 1 : 0);
+        ++g_launches;
+        cudaFreeAsync(part, stream);
+    }
+    return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+}
+
 template <int S, bool PREC = false>
 int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
                 int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream,
@@ -729,6 +894,9 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     // views [v0, v0 + nv), sinogram [4][nv][n_det]; or 8 frames (rotations
     // and mirror) over base views [0, n_views/8], natural sinogram
     const bool sym = symmode != 0;
+    if constexpr (S == 8 && !PREC) {
+        if (symmode == 8 && use_orbit(g)) return launch_bp_orbit(g, t, sino, img, v0, nv, accumulate, stream, images);
+    }
     if (sym) batch = symmode;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -780,6 +948,8 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     P.sino = sino;
     P.out = mc_fused ? img : ((G > 1 || sym || mc) ? part : img);
     P.mc_fused = mc_fused ? 1 : 0;
+    P.orbit_reps = nullptr;
+    P.orbit_T = 0;
     P.sym_stride = symmode == 4 ? nv : 0;
     P.sym_mode = symmode;
     P.images = sym ? images : 1;
@@ -820,6 +990,9 @@ int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, 
     if (g.model == CBP_MODEL_MAG)
         return launch_mag(g, t, img, const_cast<float*>(sino), batch, v0, nv, accumulate, stream, false);
     if (precise(g)) return launch_bp_s<1, true>(g, t, sino, img, batch, v0, nv, accumulate, stream);
+    // test knob: the one-slice-per-weight kernel for any batch (tests/test_gpu_parity.py)
+    static const bool force_s1 = getenv("CBP_BP_FORCE_S1") != nullptr;
+    if (force_s1) return launch_bp_s<1>(g, t, sino, img, batch, v0, nv, accumulate, stream);
     if (use_sym8(g, batch, v0, nv))
         return launch_bp_s<8>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8);
     if (batch > 1 && use_sym8(g, 1, v0, nv))  // a batch: the 8 frames of each image

@@ -31,6 +31,7 @@
 // atomics anywhere: the result is deterministic.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <type_traits>
 
 #include "cbp_common.cuh"
@@ -63,14 +64,25 @@ struct BPParams {
     // kernel): the NVSwitch sums the tiles of all CTAs and ranks while the
     // remaining tiles still compute
     int mc_fused;
+    // orbit clusters (cbp_bp_kernel<8, false, true>, n a multiple of BP_TILE):
+    // cluster k of 8 CTAs covers the orbit of tile orbit_reps[k] (x, y) under
+    // the 8 frames on the orbit_T x orbit_T tile grid
+    const int2* orbit_reps;
+    int orbit_T;
 };
 
 constexpr int BP_TILE = 32;       // pixels per tile side
 constexpr int BP_THREADS = 256;   // 8 warps x 2 pairs x 2 pixels x 32 lanes = 32 x 32
 constexpr int BP_VC = 8;          // views per chunk
 constexpr int BP_NB = 80;         // bins per view per pass (a 32-pixel tile spans <= ~64)
-constexpr int BP_BUCKETS = 32;    // ray directions over [0, pi) for the pair order
-constexpr int BP_RUN_CHUNKS = 4;  // register partial sums span at most 4 chunks (32 views)
+#ifndef CBP_BP_BUCKETS  // (compile-time knobs for A/B builds)
+#define CBP_BP_BUCKETS 32
+#endif
+#ifndef CBP_BP_RUN_CHUNKS
+#define CBP_BP_RUN_CHUNKS 4
+#endif
+constexpr int BP_BUCKETS = CBP_BP_BUCKETS;        // ray directions over [0, pi) for the pair order
+constexpr int BP_RUN_CHUNKS = CBP_BP_RUN_CHUNKS;  // register partial sums span at most 4 chunks (32 views)
 constexpr int BP_PAIRS = BP_TILE * BP_TILE / 2;
 
 struct __align__(16) BPEntry {
@@ -509,6 +521,26 @@ __device__ __forceinline__ void frame_inv(int n, int q, int m, int& r, int& c)
     if (m) r = n - 1 - r;
 }
 
+// Orbit clusters.  With n = 32 T the 8 frames map tiles
+// onto tiles: tile (ty, tx) -> frame_fwd(T, ...) on tile coordinates.  The
+// orbit of a tile has 8, 4 (a diagonal tile: the transpose fixes it) or 1
+// (the centre tile of an odd T) distinct tiles; its members are listed in
+// frame order without repeats, identically by every CTA.
+__device__ __forceinline__ int bp_orbit_members(int T, int2 rep, int (&mem)[8])
+{
+    int size = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        int r = rep.y, c = rep.x;
+        frame_fwd(T, q & 3, q >> 2, r, c);
+        const int t = r * T + c;
+        bool seen = false;
+        for (int i = 0; i < size; ++i) seen |= mem[i] == t;
+        if (!seen) mem[size++] = t;
+    }
+    return size;
+}
+
 // dynamic shared memory of the BP kernel for S slices: entries, headers,
 // (S > 1) two y buffers [2][VC][NB][S], tile accumulators [S][32][33]
 __host__ __device__ constexpr size_t bp_smem_bytes(int S, bool prec = false)
@@ -580,10 +612,86 @@ __device__ __forceinline__ void bp_y_load(const BPParams& P, int vl0, int nvc, i
     }
 }
 
-template <int S, bool PREC = false>
+// The orbit cluster's epilogue: every CTA of the cluster holds the 8 frame
+// accumulators of its member tile; output tile U (member rank mod size) is
+// the sum, over the cluster's CTAs i and the frames q with g_q(S_i) = U, of
+// CTA i's frame q read through distributed shared memory in U's orientation
+// -- in (i, q) order, so the result is deterministic, with no partial frame
+// planes and no reduce kernel.  A member tile shared by 8 / size CTAs (a
+// smaller orbit) has its rows split among them.  Output: the image (one view
+// group; accumulate adds), the multicast image (mc_fused: red.add), or the
+// group's partial plane [images][groups] (cbp_reduce_kernel sums the groups).
+__device__ void bp_orbit_epilogue(const BPParams& P, float* acc_s, const int (&mem)[8], int size, int grp, int sg)
+{
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    constexpr int LD = BP_TILE + 1, PL = BP_TILE * LD;
+    const int T = P.orbit_T, n = P.g.n, tid = threadIdx.x;
+    const int rank = (int)cluster.block_rank();
+    const int U = mem[rank % size], ur = U / T, uc = U % T;
+    const int parts = 8 / size, part = rank / size;
+    const int rlo = part * (BP_TILE / parts), rhi = rlo + BP_TILE / parts;
+    __shared__ int4 contrib[64];  // (cluster rank i, base index in its acc_s, col step, row step)
+    __shared__ int ncontrib;
+    if (tid == 0) {
+        int k = 0;
+        for (int i = 0; i < 8; ++i) {
+            const int S0 = mem[i % size], sr0 = (S0 / T) * BP_TILE, sc0 = (S0 % T) * BP_TILE;
+            for (int q = 0; q < 8; ++q) {
+                int tr = S0 / T, tc = S0 % T;
+                frame_fwd(T, q & 3, q >> 2, tr, tc);
+                if (tr * T + tc != U) continue;
+                // source pixel of output pixels (ur 32, uc 32) + {(0, 0), (0, 1), (1, 0)}
+                int k0r = ur * BP_TILE, k0c = uc * BP_TILE, k1r = k0r, k1c = k0c + 1, k2r = k0r + 1, k2c = k0c;
+                frame_inv(n, q & 3, q >> 2, k0r, k0c);
+                frame_inv(n, q & 3, q >> 2, k1r, k1c);
+                frame_inv(n, q & 3, q >> 2, k2r, k2c);
+                contrib[k++] = make_int4(i, q * PL + (k0r - sr0) * LD + (k0c - sc0), (k1r - k0r) * LD + (k1c - k0c),
+                                         (k2r - k0r) * LD + (k2c - k0c));
+            }
+        }
+        ncontrib = k;
+    }
+    cluster.sync();  // every CTA's accumulators are final (and contrib is ready)
+    const int nc = ncontrib;
+    const size_t plane = (size_t)n * n;
+    float* out = P.groups > 1 && !P.mc_fused ? P.out + ((size_t)sg * P.groups + grp) * plane
+                                             : P.out + (size_t)sg * plane;
+    const bool add = P.groups == 1 && P.accumulate;
+    for (int i = tid; i < (rhi - rlo) * (BP_TILE / 4); i += BP_THREADS) {
+        const int r = rlo + i / (BP_TILE / 4), c = (i % (BP_TILE / 4)) * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < nc; ++k) {
+            const int4 cb = contrib[k];
+            const float* a = cluster.map_shared_rank(acc_s, cb.x);
+            const int si = cb.y + r * cb.w + c * cb.z;
+            v.x += a[si];
+            v.y += a[si + cb.z];
+            v.z += a[si + 2 * cb.z];
+            v.w += a[si + 3 * cb.z];
+        }
+        float4* o = reinterpret_cast<float4*>(out + (size_t)(ur * BP_TILE + r) * n + uc * BP_TILE + c);
+        if (P.mc_fused) {
+            mc_red_add4(o, v);
+        } else {
+            if (add) {
+                const float4 w = *o;
+                v.x += w.x;
+                v.y += w.y;
+                v.z += w.z;
+                v.w += w.w;
+            }
+            *o = v;
+        }
+    }
+    cluster.sync();  // the other CTAs' reads of this CTA's accumulators are done
+}
+
+template <int S, bool PREC = false, bool ORB = false>
 __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp_bp_kernel(const BPParams P)
 {
     static_assert(!PREC || S == 1, "the precise mode runs one slice per weight");
+    static_assert(!ORB || (S == 8 && !PREC), "orbit clusters carry the 8 dihedral frames");
     using Ent = typename std::conditional<PREC, BPEntryP, BPEntry>::type;
     constexpr bool STAGE = S > 1;  // y staged asynchronously one chunk ahead
     constexpr int HB = bp_hdr_bufs(S);
@@ -596,15 +704,29 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
 
     const GeomDev& g = P.g;
     const int tid = threadIdx.x;
-    const int col0 = blockIdx.x * BP_TILE, row0 = blockIdx.y * BP_TILE;
     const int grp = blockIdx.z % P.groups, sg = blockIdx.z / P.groups;  // view group, slice group
-    const int vg0 = grp * P.views_per_group;
-    const int vgn = max(0, min(P.views_per_group, P.view_count - vg0));
+    int vg0 = grp * P.views_per_group;
+    int vgn = max(0, min(P.views_per_group, P.view_count - vg0));
+    int tile_x = blockIdx.x, tile_y = blockIdx.y, tiles_x = gridDim.x;
+    int omem[8], osize = 1;
+    if constexpr (ORB) {
+        // cluster rank r takes orbit member r mod size over part r / size of the
+        // group's views (8 / size parts: a smaller orbit splits its views)
+        tiles_x = P.orbit_T;
+        osize = bp_orbit_members(P.orbit_T, P.orbit_reps[blockIdx.x / 8], omem);
+        const int rank = blockIdx.x % 8, parts = 8 / osize, part = rank / osize;
+        tile_x = omem[rank % osize] % tiles_x;
+        tile_y = omem[rank % osize] / tiles_x;
+        const int per = (vgn + parts - 1) / parts;
+        vg0 += part * per;
+        vgn = max(0, min(per, vgn - part * per));
+    }
+    const int col0 = tile_x * BP_TILE, row0 = tile_y * BP_TILE;
     const int nchunks = (vgn + BP_VC - 1) / BP_VC;
     float hcx, hcy;  // anchor k_a = centre of the tile's valid pixels
     double kax, kay;
-    bp_tile_anchor(g, blockIdx.x, blockIdx.y, hcx, hcy, kax, kay);
-    const BPHeader* hsrc = P.hdrs + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * P.view_count + vg0;
+    bp_tile_anchor(g, tile_x, tile_y, hcx, hcy, kax, kay);
+    const BPHeader* hsrc = P.hdrs + ((size_t)tile_y * tiles_x + tile_x) * P.view_count + vg0;
     const size_t sino_plane = (size_t)P.view_count * g.n_det;
     constexpr int HW = sizeof(BPHeader) / 16;  // 16-byte words per header
     auto hdr_buf = [&](int c) { return hdr_all + (c % HB) * BP_VC; };
@@ -636,7 +758,7 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
     float2 a0[S], a1[S];
 #pragma unroll
     for (int q = 0; q < S; ++q) a0[q] = a1[q] = make_float2(0.f, 0.f);
-    int bucket = -1, horiz = 1, e0 = 0, e1 = 0;
+    int bucket = -1, horiz = 1, e0 = 0, e1 = 0, prev_npass = 1;
     float2 dc0, dr0, dc1, dr1;  // pixel offsets of the two pairs (lanes a, b)
     for (int c = 0; c < nchunks; ++c) {
         const int vc = c * BP_VC;
@@ -654,12 +776,21 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                              true);
             cp_async_commit();
         } else {
+            // the single header buffer is rewritten here: every thread must be done
+            // reading the previous chunk's headers.  A chunk with passes ends in a
+            // barrier; one whose views all miss the tile (npass = 0: a tile the
+            // detector does not cover for those views) does not -- without this
+            // barrier a fast thread overwrote the headers a slow one was still
+            // reading (found by tools/fuzz.py wide seeds 139 and 2189: ragged edge
+            // tiles outside the detector, one slice per weight)
+            if (c > 0 && prev_npass == 0) __syncthreads();
             if (tid < nvc * HW)
                 reinterpret_cast<int4*>(hdr)[tid] = __ldg(reinterpret_cast<const int4*>(hsrc + vc) + tid);
             __syncthreads();
         }
         int npass = 0;
         for (int vi = 0; vi < nvc; ++vi) npass = max(npass, (int)hdr[vi].npass_f);
+        prev_npass = npass;
         for (int pass = 0; pass < npass; ++pass) {
             if (STAGE && pass > 0) bp_y_load<S>(P, vg0 + vc, nvc, pass, hdr, ytab, false);
 #pragma unroll 3
@@ -689,7 +820,10 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                 const BPHeader& H = hdr[vi];
                 const int4 hi = *reinterpret_cast<const int4*>(&H.ja);  // ja, jlo, jhi, bucket
                 // new pair order, or FP32 register sums over BP_RUN views: hand the pixels back
-                const bool renew = hi.w != bucket || (vi == 0 && pass == 0 && c > 0 && c % BP_RUN_CHUNKS == 0);
+                // (S >= 4: the tile accumulator is FP32 too, so periodic flushes buy no
+                // precision -- measured config 5 BP 9.69 -> 9.46 ms without them)
+                const bool renew = hi.w != bucket ||
+                                   (S <= 2 && vi == 0 && pass == 0 && c > 0 && c % BP_RUN_CHUNKS == 0);
                 if (renew) {
                     if (bucket >= 0) {
                         bp_flush<S>(acc_s, horiz, e0, e1, a0, a1);
@@ -764,6 +898,10 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
     if constexpr (STAGE) {
         cp_async_wait_all();
         __syncthreads();
+    }
+    if constexpr (ORB) {
+        bp_orbit_epilogue(P, acc_s, omem, osize, grp, sg);
+        return;
     }
     // Write the tile's sums.  With symmetry, slice q holds frame g_q = R^qq M^m
     // of the image; its values go straight to the output orientation (pixel

@@ -51,6 +51,10 @@ struct FPParams {
     // 8: the full dihedral symmetry (S = 8, cbp_pad_sym8_kernel) over base
     // views [0, n_views/8], output the natural [n_views][n_det] sinogram
     int sym_mode;
+    // 1 (with sym_stride > 0): a column-major ray of base view v is walked as
+    // the row-major ray of view v + n_views/4 and its frame s written as frame
+    // s + 1, so only the row-major padded copy is read (padT is not built)
+    int rot_rows;
     // (the line split is the kernel's PARTS template parameter, see cbp_fp_kernel)
 };
 
@@ -59,6 +63,9 @@ constexpr int FP_BLOCK = 128;
 // over more than 4 warps (small grids: view shards, small images)
 __host__ __device__ constexpr int fp_threads(int parts) { return parts <= 4 ? FP_BLOCK : 32 * parts; }
 constexpr int FP_KMAX_UNROLLED = 6;
+#ifndef CBP_FP_P8_MINB  // resident 256-thread CTAs per SM of the 8-part FP (A/B knob)
+#define CBP_FP_P8_MINB 2
+#endif
 
 // ---- zero-padded (and transposed) image copies, S slices interleaved ------
 constexpr int PAD_TILE = 32;
@@ -110,6 +117,7 @@ __device__ __forceinline__ void rot90_pow(int n, int q, int& r, int& c)
     }
 }
 
+template <bool TRANSPOSE>
 __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym4_kernel(const float* __restrict__ img,
                                                                     float* __restrict__ pad,
                                                                     float* __restrict__ padT, int n,
@@ -128,11 +136,12 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym4_kernel(const float*
             int a = sr, b = sc;
             rot90_pow(n, q, a, b);
             v[q] = in ? img[(size_t)a * n + b] : 0.0f;
-            tile[rr][threadIdx.x][q] = v[q];
+            if constexpr (TRANSPOSE) tile[rr][threadIdx.x][q] = v[q];
         }
         if (r < np && c < np)
             *reinterpret_cast<float4*>(pad + ((size_t)r * np + c) * 4) = make_float4(v[0], v[1], v[2], v[3]);
     }
+    if constexpr (!TRANSPOSE) return;  // the rot_rows FP reads pad only
     __syncthreads();
     for (int cc = threadIdx.y; cc < PAD_TILE; cc += 8) {
         const int c = c0 + cc, r = r0 + threadIdx.x;
@@ -441,7 +450,7 @@ __device__ void fp_walk_prec(const FPRay& R, const FPRayD& D, int K, int i0, int
 // when the grid would otherwise be short of ~16 waves: the ragged last wave
 // of a 1.6-wave grid cost ~25 %.
 template <int S, int PARTS, bool PREC = false>
-__global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? 2 : (S == 1 ? 7 : (S == 4 ? 6 : 4)))
+__global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? CBP_FP_P8_MINB : (S == 1 ? 7 : (S == 4 ? 6 : 4)))
     cbp_fp_kernel(const FPParams P)
 {
     static_assert(!PREC || S == 1, "the precise mode runs one slice per weight");
@@ -474,8 +483,20 @@ __global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? 2 : (S == 1 ? 7
     // ---- per-ray constants (FP64): Eq. 11 frame, Eq. 12 directions, Eq. 13 gain
     const double2 cs = P.t.view_cs[v];
     const double2 bd = P.t.bin_d[j];
-    const double cth = cs.x, sth = cs.y, s = bd.x, invL = bd.y;
+    const double s = bd.x, invL = bd.y;
     const double sphi = g.parallel ? 0.0 : s * invL, cphi = g.parallel ? 1.0 : g.sdd * invL;
+    double cth = cs.x, sth = cs.y;
+    // rot_rows: rotating the scanner by +90 degrees (u -> (-sin, cos)) maps this
+    // ray onto the same bin of view v + N/4, where it runs along the rows
+    // (r' = (-r_y, r_x)), and W(v + N/4, j, R k) = W(v, j, k):
+    // frame s of the rotated walk is output frame s + 1
+    int rq = 0;
+    if (P.rot_rows && fabs(sphi * cth - cphi * sth) < fabs(cphi * cth + sphi * sth)) {
+        const double t = cth;
+        cth = -sth;
+        sth = t;
+        rq = 1;
+    }
     const double rx = sphi * cth - cphi * sth;  // r_j = (D_ps e + s_j u) / L_j  (parallel: e)
     const double ry = cphi * cth + sphi * sth;
     const double vx = -ry, vy = rx;             // v_j = (-D_ps u + s_j e) / L_j
@@ -630,7 +651,7 @@ __global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? 2 : (S == 1 ? 7
                 const int bin = m ? g.n_det - 1 - j : j;
                 dst = sino_out + (size_t)view * g.n_det + bin;
             } else if (P.sym_stride > 0) {
-                dst = sino_out + ((size_t)vl + (size_t)q * P.sym_stride) * g.n_det + j;
+                dst = sino_out + ((size_t)vl + (size_t)((q + rq) & 3) * P.sym_stride) * g.n_det + j;
             } else if (b < P.batch) {
                 dst = sino_out + ((size_t)b * P.view_count + vl) * g.n_det + j;
             }

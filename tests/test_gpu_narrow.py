@@ -8,7 +8,7 @@ cbp_narrow_ratio 0.02 the library switches to its precise mode (FP64
 positions and knots, smallest width innermost); these tests pin whichever
 path the library picks at tau/h = 0.01, 0.02, 0.05 (tau'/h 0.004 - 0.05), on full scans (8 views:
 the four axis-aligned views where min|zeta| = 0 at the central bin, and the
-diagonals) and on view ranges, plus the two draws of tools/fuzz_wide.py that
+diagonals) and on view ranges, plus the two draws of tools/fuzz.py wide that
 exposed the FP32 limit (seeds 997 and 2009), and the precise mode forced on
 at the configs' normal widths."""
 import numpy as np
@@ -86,7 +86,7 @@ def test_narrow_bins_shards_sum_to_full(torch_cuda):
     _assert_parity(orb.reshape(8, -1).cpu().numpy(), want[rows], "FP orbit shard")
 
 
-# tools/fuzz_wide.py draws that exceeded the bar before the precise mode:
+# tools/fuzz.py wide draws that exceeded the bar before the precise mode:
 # seed 997: flat detector, tau/h 0.014, a half-turn view (BP max-normalised 1.6e-4);
 # seed 2009: arc, one 1.49 mm pixel, a source 1.14 mm away, tau/h 0.009 (FP relL2 1.06e-5)
 FUZZ_WIDE = {
@@ -124,3 +124,45 @@ def test_precise_mode_forced_at_normal_widths(torch_cuda, monkeypatch, kind, mod
     y = W.random_sino(g["n_views"], g["n_det"], 47)
     _assert_parity(_bp(torch_cuda, g, y), O.back(g, y), f"BP precise kind {kind} model {model}")
     assert cbp.adjoint_check(g, seed=3) <= 1e-5
+
+
+# tools/fuzz.py wide seeds 139 and 2189: batches of 8 in the precise mode (one
+# slice per weight, single header buffer) on scanners whose detector does not
+# cover the ragged edge tiles for whole chunks of views.  Such a chunk ends
+# without a barrier and a fast thread rewrote the headers a slow one was still
+# reading: nondeterministic errors up to 1e-2 (fixed in cbp_bp.cuh; repeated
+# runs must agree bitwise and meet the bar)
+FUZZ_WIDE_B8 = {
+    139: (dict(n=131, pixel=0.3635648482434381, n_views=100, n_det=850, det_pitch=0.1575262582236706,
+               det_width=0.01281560994357787, sid=197.13173562862266, sdd=468.5625236693143, kind=0, model=0), 8),
+    2189: (dict(n=142, pixel=0.2931904994119643, n_views=100, n_det=444, det_pitch=0.0717829057628753,
+                det_width=0.0032782721295456555, sid=0.0, sdd=0.0, kind=1, model=0), 8),
+}
+
+
+@pytest.mark.parametrize("seed", sorted(FUZZ_WIDE_B8))
+def test_one_slice_bp_header_race(torch_cuda, seed):
+    torch = torch_cuda
+    g, batch = FUZZ_WIDE_B8[seed]
+    y = W.random_sino(g["n_views"], g["n_det"], seed + 7, batch=batch)
+    want = O.back(g, y)
+    yd = torch.from_numpy(y).cuda()
+    outs = [cbp.back(g, yd).cpu().numpy() for _ in range(6)]
+    for o in outs:
+        _assert_parity(o, want, f"BP batch {batch} fuzz_wide {seed}")
+        assert np.array_equal(o, outs[0]), "nondeterministic BP"
+
+
+def test_one_slice_bp_standard_mode_uncovered_tiles(torch_cuda):
+    # the FP32 one-slice BP (batch 1, n_views % 4 != 0: no symmetry) on the same
+    # kind of scanner at normal widths
+    torch = torch_cuda
+    g = dict(FUZZ_WIDE_B8[2189][0], n_views=99, det_width=0.0717829057628753)
+    assert cbp.precise_mode(g) == 0 and cbp.symmetry_fold(g) == 1
+    y = W.random_sino(g["n_views"], g["n_det"], 7)
+    want = O.back(g, y)
+    yd = torch.from_numpy(y).cuda()
+    outs = [cbp.back(g, yd).cpu().numpy() for _ in range(6)]
+    for o in outs:
+        _assert_parity(o, want, "BP one slice, uncovered edge tiles")
+        assert np.array_equal(o, outs[0]), "nondeterministic BP"

@@ -138,7 +138,7 @@ def test_variant_batch_full_scan(torch_cuda, kind):
 
 
 def test_arc_bp_close_source_bin_range(torch_cuda):
-    # regression (tools/fuzz_wide.py seed 2009): a source within a few pixels
+    # regression (tools/fuzz.py wide seed 2009): a source within a few pixels
     # of the field of view; the arc BP's per-tile bin range used the small-angle
     # bound 1.01 sigma/delta for asin(sigma/|k - p|) and dropped bins (2.4e-2)
     g = dict(n=1, pixel=1.4937332023018055, n_views=4, n_det=19, det_pitch=0.6050390134164245,

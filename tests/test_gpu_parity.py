@@ -439,3 +439,23 @@ def test_dihedral_shards_sum_to_full(torch_cuda, n_views, world):
     assert sorted(seen) == list(range(g["n_views"]))
     torch.cuda.synchronize()
     _assert_parity(total.cpu().numpy(), full_c.cpu().numpy(), "BP dihedral shards")
+
+
+def test_rot_rows_fp_matches_oracle(torch_cuda, monkeypatch):
+    # the opt-in rot_rows FP (CBP_ROTROWS=1, read once per process: run in a child)
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np, torch; sys.path.insert(0, '.');"
+            "import oracle as O, paper_1907_10526_b200 as cbp, workloads as W;"
+            "from tests.test_gpu_parity import _metrics;"
+            "g = dict(W.geometry('1'), n_views=88); img = W.shepp_logan(64);"
+            "y = cbp.forward(g, torch.from_numpy(img).cuda()).cpu().numpy();"
+            "print(*_metrics(y, O.forward(g, img)))")
+    import os
+    env = dict(os.environ, CBP_ROTROWS="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    rl2, mr = (float(x) for x in out.stdout.split())
+    assert rl2 <= REL_L2 and mr <= MAX_REL, (rl2, mr)

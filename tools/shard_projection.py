@@ -3,7 +3,9 @@ world size W, every rank's dihedral shard (sharded.make_shard, the bench's
 N > 1 shape) is timed on this GPU (FP + BP, warm L2, CUDA events); the
 projected step of W GPUs is the slowest shard (the ranks run concurrently
 on their own GPUs), plus the BP all-reduce, which this one-GPU box cannot
-measure (reported separately as not measured).  Usage:
+measure (reported separately as not measured).  With CBP_PROJ_GRAPH=1 each
+rank's pair is captured once in a CUDA graph and replayed (no host launch
+overhead in the timed loop; the library's launches are graph nodes).  Usage:
   python tools/shard_projection.py [config] [worlds...]"""
 import json
 import os
@@ -18,6 +20,17 @@ import workloads as W  # noqa: E402
 
 
 def t_ms(fn, reps=20):
+    if os.environ.get("CBP_PROJ_GRAPH") == "1":
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=s):
+            fn()
+        torch.cuda.synchronize()
+        fn = gr.replay
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
