@@ -63,6 +63,9 @@ constexpr int FP_BLOCK = 128;
 // over more than 4 warps (small grids: view shards, small images)
 __host__ __device__ constexpr int fp_threads(int parts) { return parts <= 4 ? FP_BLOCK : 32 * parts; }
 constexpr int FP_KMAX_UNROLLED = 6;
+#ifndef CBP_FP_S4_MINB  // resident 128-thread CTAs per SM of the 4-slice FP (A/B knob)
+#define CBP_FP_S4_MINB 6
+#endif
 #ifndef CBP_FP_P8_MINB  // resident 256-thread CTAs per SM of the 8-part FP (A/B knob)
 #define CBP_FP_P8_MINB 2
 #endif
@@ -450,7 +453,7 @@ __device__ void fp_walk_prec(const FPRay& R, const FPRayD& D, int K, int i0, int
 // when the grid would otherwise be short of ~16 waves: the ragged last wave
 // of a 1.6-wave grid cost ~25 %.
 template <int S, int PARTS, bool PREC = false>
-__global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? CBP_FP_P8_MINB : (S == 1 ? 7 : (S == 4 ? 6 : 4)))
+__global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? CBP_FP_P8_MINB : (S == 1 ? 7 : (S == 4 ? CBP_FP_S4_MINB : 4)))
     cbp_fp_kernel(const FPParams P)
 {
     static_assert(!PREC || S == 1, "the precise mode runs one slice per weight");
