@@ -3,7 +3,12 @@ racecheck / synccheck): CNSF FP/BP on the direct, batched (S = 2, 4),
 4-fold and 8-fold symmetric paths, ragged grids, the parallel and arc
 kinds, the magnified-footprint model (plain and 4-fold), orbit and dihedral
 shards, the normal operator and its host pipeline, the FP64 reference pair,
-and the vector / TV kernels of the iterative loops."""
+the vector / TV kernels of the iterative loops, and (round 2) the precise
+mode for narrow bins (CNSF and magnified, every kind, batches), the
+one-slice BP over edge tiles the detector misses, the opt-in orbit-cluster
+BP and rot_rows FP.  Run under the debug build (libcbp_debug.so:
+CBP_DEBUG_CHECKS index checks and a sync + error check after each launch)
+since compute-sanitizer is closed on this pool."""
 import os
 import sys
 
@@ -59,6 +64,25 @@ for dihedral in (False, True):
 # normal operator, device and host pipeline
 cbp.normal(g1, img)
 cbp.normal_stream(g1, np.stack([W.random_image(64, i) for i in range(3)]))
+# round 2: the precise mode (narrow bins), every kind and model, batches
+for kind in (cbp.FAN_FLAT, cbp.PARALLEL, cbp.FAN_ARC):
+    for model in (0, 1):
+        gn = dict(n=40, pixel=1.0, n_views=8, n_det=45 if kind == cbp.PARALLEL else 54,
+                  det_pitch=1.0 if kind == cbp.PARALLEL else 2.0, det_width=0.01,
+                  sid=0.0 if kind == cbp.PARALLEL else 100.0, sdd=0.0 if kind == cbp.PARALLEL else 200.0,
+                  kind=kind, model=model)
+        assert cbp.precise_mode(gn) == 1
+        pair(gn)
+        pair(gn, batch=3)
+# the one-slice BP over edge tiles the detector does not cover, batch 8 (precise mode)
+gw = dict(n=142, pixel=0.2931904994119643, n_views=100, n_det=444, det_pitch=0.0717829057628753,
+          det_width=0.0032782721295456555, sid=0.0, sdd=0.0, kind=1, model=0)
+pair(gw, batch=8)
+# the opt-in orbit-cluster BP (n a multiple of 32; an odd tile grid) and rot_rows FP
+os.environ["CBP_ORBIT"] = "1"
+pair(dict(g1, n_views=88))
+pair(dict(g1, n=96, n_det=192, n_views=48))
+os.environ.pop("CBP_ORBIT")
 # reference projector
 gs = dict(g1, n=16, n_views=6, n_det=40)
 yr = cbp.ref_forward(gs, torch.from_numpy(W.random_image(16, 3)).cuda())
