@@ -474,8 +474,9 @@ bool use_sym8(const cbp_geometry_t& g, int32_t batch, int32_t v0, int32_t nv)
 }
 
 int launch_fp_sym8(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, float* sino,
-                   cudaStream_t stream)
+                   cudaStream_t stream, int32_t base_begin = 0, int32_t base_count = -1)
 {
+    if (base_count < 0) base_count = g.n_views / 8 + 1 - base_begin;
     const int P = fp_pad_width(g);
     const int np = g.n + 2 * P;
     const size_t plane = (size_t)np * np * 8;
@@ -497,13 +498,13 @@ int launch_fp_sym8(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     Pm.np = np;
     Pm.P = P;
     Pm.sino = sino;
-    Pm.view_begin = 0;
-    Pm.view_count = g.n_views / 8 + 1;
+    Pm.view_begin = base_begin;
+    Pm.view_count = base_count;
     Pm.batch = 8;
     Pm.sym_stride = 0;
     Pm.sym_mode = 8;
     Pm.rot_rows = 0;
-    rc = launch_fp_kernel<8>(Pm, g.n_views / 8 + 1, 1, stream);
+    rc = launch_fp_kernel<8>(Pm, base_count, 1, stream);
     cudaFreeAsync(pad, stream);
     return rc;
 }
@@ -1390,6 +1391,8 @@ int cbp_forward_dihedral(const cbp_geometry_t* g, const float* image, float* sin
     // the 4 rotations of the base block, then those of its mirror images
     // N/4 - v (v = 0 and v = N/8 are their own mirror orbits)
     // one pad and one launch for both blocks (the grid of a small shard is far short of a wave)
+    // (one 8-frame launch over the base block instead, launch_fp_sym8(..., base_begin,
+    // base_count): measured slower at every shard size)
     const int lo = std::max(base_begin, 1), hi = std::min(base_begin + base_count, e);  // [lo, hi)
     return launch_fp_sym4(*g, t, image, sino, base_begin, base_count, stream, q, q - hi + 1, hi > lo ? hi - lo : 0);
 }
