@@ -334,6 +334,15 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    def _graph_call(fn, a, b, st):
+        nonlocal stream
+        saved = stream
+        stream = st
+        try:
+            fn(a, b)
+        finally:
+            stream = saved
+
     def fwd(image, y):
         if orbit:
             cbp.forward_orbit(g, image, sh.begin, sh.count, sino=y, stream=stream)
@@ -350,13 +359,28 @@ def main():
         else:
             cbp.back(g, y, image, view_begin=sh.begin, stream=stream)
 
+    # The timed step replays the FP and the BP as two CUDA graphs captured from
+    # the same library calls (the library's kernels, scratch allocations and
+    # programmatic-launch edges become graph nodes): the device timing then
+    # does not depend on how fast this Python loop enqueues -- with eager
+    # launches, host jitter (the clock sampler's driver queries, GC) left the
+    # GPU idle inside a few steps' BP interval (0.5-20 ms outliers; round 2).
+    # CBP_BENCH_EAGER=1 times eager launches instead.
+    graphs = None
+
     def step(ev=None):
         if ev:
             ev[0].record(stream)
-        fwd(img, sino)
+        if graphs:
+            graphs[0].replay()
+        else:
+            fwd(img, sino)
         if ev:
             ev[1].record(stream)
-        bwd(sino, out)
+        if graphs:
+            graphs[1].replay()
+        else:
+            bwd(sino, out)
         if ev:
             ev[2].record(stream)
         if world > 1 and not slice_shard:
@@ -368,6 +392,30 @@ def main():
         flush.zero_()
         step()
     torch.cuda.synchronize()
+    if os.environ.get("CBP_BENCH_EAGER") != "1":
+        try:
+            gfp, gbp = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(dev)
+            cap.wait_stream(stream)
+            with torch.cuda.stream(cap):
+                with torch.cuda.graph(gfp, stream=cap):
+                    _graph_call(fwd, img, sino, cap)
+                with torch.cuda.graph(gbp, stream=cap):
+                    _graph_call(bwd, sino, out, cap)
+            stream.wait_stream(cap)
+            torch.cuda.synchronize()
+            graphs = (gfp, gbp)
+            for _ in range(3):  # warm the graphs
+                flush.zero_()
+                step()
+            torch.cuda.synchronize()
+        except Exception as exc:  # noqa: BLE001 -- fall back to eager launches, say so in the line
+            graphs = None
+            graph_note = f"graph capture failed ({type(exc).__name__}: {str(exc)[:120]}); eager launches"
+        else:
+            graph_note = "FP and BP each replayed as a CUDA graph of the library calls"
+    else:
+        graph_note = "eager launches (CBP_BENCH_EAGER=1)"
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
@@ -421,7 +469,9 @@ def main():
         evals = units / folds[name] if units else None
         flops = evals * (FLOPS_PER_WEIGHT - 2) + units * 2 if units else None
         ach = flops / (ms * 1e-3) / 1e12 if flops else None
-        kernels[name] = {"ms": ms, "tflops": ach, "frac": ach / peak_tflops if ach else None,
+        per = fp_ms if name == "fp" else bp_ms
+        kernels[name] = {"ms": ms, "ms_median": statistics.median(per), "ms_min": min(per), "ms_max": max(per),
+                         "tflops": ach, "frac": ach / peak_tflops if ach else None,
                          "weights_per_launch": units, "weight_evaluations": evals,
                          "views_or_slices_per_evaluation": folds[name],
                          "effective_tflops_per_view_weight": units * FLOPS_PER_WEIGHT / (ms * 1e-3) / 1e12
@@ -578,6 +628,7 @@ def main():
             "config": bench_config(args, g, world, sh.mode if not slice_shard else "block", slice_shard),
             "roofline": roof,
             "kernels": kernels,
+            "timing": graph_note,
             "allreduce_ms": statistics.mean(ar_ms) if world > 1 else 0.0,
             "cpu_baseline": cpu,
             "e2e": e2e,
