@@ -280,7 +280,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1907_10526_b200 as cbp
-    from paper_1907_10526_b200.sharded import Shard, make_shard, view_shard
+    from paper_1907_10526_b200.sharded import MulticastImage, Shard, back_sharded, make_shard, view_shard
 
     assert args.warmup >= 3, "at least 3 warm-up steps"
     # CBP_BENCH_BACKEND=gloo (a logic check, not a measurement): the ranks may
@@ -366,7 +366,37 @@ def main():
     # launches, host jitter (the clock sampler's driver queries, GC) left the
     # GPU idle inside a few steps' BP interval (0.5-20 ms outliers; round 2).
     # CBP_BENCH_EAGER=1 times eager launches instead.
-    graphs = None
+    graphs, graph_kernels = None, (0, 0)
+    # N > 1, view shards: the BP's partial images are summed by the BP itself
+    # through an NVLink multicast image (CBP_ACC_MULTIMEM, sharded.MulticastImage)
+    # when the system has one and a first step agrees with the NCCL all-reduce;
+    # else (or CBP_BENCH_NCCL=1) by NCCL's all_reduce after the BP
+    mm, reduce_note = None, ("NCCL all_reduce after the BP" if world > 1 and not slice_shard else "none")
+    if world > 1 and not slice_shard and os.environ.get("CBP_BENCH_NCCL") != "1" and backend == "nccl":
+        why = ""
+        try:
+            mm = MulticastImage(n, device=dev)
+        except Exception as exc:  # noqa: BLE001
+            mm, why = None, str(exc)[:100]
+        # every rank agrees before any multicast barrier runs
+        ok = torch.tensor([1.0 if mm is not None else 0.0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 1.0:
+            fwd(img, sino)
+            bwd(sino, out)
+            dist.all_reduce(out)
+            ref = out.clone()
+            res = back_sharded(g, sino, sh, multimem=mm, stream=stream)
+            torch.cuda.synchronize()
+            err = float((res - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
+            ok.fill_(1.0 if err <= 1e-5 else 0.0)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            why = f"multicast BP disagreed with NCCL on some rank (here {err:.1e})"
+        if ok.item() == 1.0:
+            reduce_note = f"fused into the BP epilogue through NVLink multicast (checked against NCCL: {err:.1e})"
+        else:
+            mm = None
+            reduce_note = f"NCCL all_reduce after the BP ({why or 'multicast unavailable on some rank'})"
 
     def step(ev=None):
         if ev:
@@ -377,13 +407,15 @@ def main():
             fwd(img, sino)
         if ev:
             ev[1].record(stream)
-        if graphs:
+        if mm is not None:  # the BP adds into every rank's copy; zero + barriers before / after
+            back_sharded(g, sino, sh, multimem=mm, stream=stream)
+        elif graphs:
             graphs[1].replay()
         else:
             bwd(sino, out)
         if ev:
             ev[2].record(stream)
-        if world > 1 and not slice_shard:
+        if world > 1 and not slice_shard and mm is None:
             dist.all_reduce(out)
         if ev:
             ev[3].record(stream)
@@ -397,20 +429,24 @@ def main():
             gfp, gbp = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
             cap = torch.cuda.Stream(dev)
             cap.wait_stream(stream)
+            c0 = cbp.launch_count()
             with torch.cuda.stream(cap):
                 with torch.cuda.graph(gfp, stream=cap):
                     _graph_call(fwd, img, sino, cap)
+                c1 = cbp.launch_count()
                 with torch.cuda.graph(gbp, stream=cap):
                     _graph_call(bwd, sino, out, cap)
             stream.wait_stream(cap)
             torch.cuda.synchronize()
+            # the library's kernels captured in each graph: every replay launches them again
+            graph_kernels = (c1 - c0, cbp.launch_count() - c1)
             graphs = (gfp, gbp)
             for _ in range(3):  # warm the graphs
                 flush.zero_()
                 step()
             torch.cuda.synchronize()
         except Exception as exc:  # noqa: BLE001 -- fall back to eager launches, say so in the line
-            graphs = None
+            graphs, graph_kernels = None, (0, 0)
             graph_note = f"graph capture failed ({type(exc).__name__}: {str(exc)[:120]}); eager launches"
         else:
             graph_note = "FP and BP each replayed as a CUDA graph of the library calls"
@@ -429,7 +465,10 @@ def main():
         flush.zero_()  # L2 flush, outside the timed events
         step(evs[k])
     torch.cuda.synchronize()
+    # eager library calls count themselves; graph replays launch the captured kernels
     launches = cbp.launch_count() - launches0
+    if graphs:
+        launches += args.steps * (graph_kernels[0] + (graph_kernels[1] if mm is None else 0))
     if world > 1:
         dist.barrier()
     clk = clocks.stop() if clocks else None
@@ -533,10 +572,13 @@ def main():
             else:
                 d_img.copy_(h_img, non_blocking=True)  # H2D image
                 fwd(d_img, sino)
-                bwd(sino, d_out)
-                if world > 1 and not slice_shard:
-                    dist.all_reduce(d_out)
-                h_out.copy_(d_out)  # D2H image
+                if mm is not None:
+                    h_out.copy_(back_sharded(g, sino, sh, multimem=mm, stream=stream))  # D2H image
+                else:
+                    bwd(sino, d_out)
+                    if world > 1 and not slice_shard:
+                        dist.all_reduce(d_out)
+                    h_out.copy_(d_out)  # D2H image
                 torch.cuda.synchronize()
 
         def e2e_sino_step():  # the same pair with the sinogram through host memory too
@@ -595,7 +637,8 @@ def main():
                "path": f"cbp_normal_stream (A^T A) over {ke} distinct inputs in pinned host memory: the "
                        "library's copy/compute/copy pipeline (the sinogram stays on the device)" if piped
                else f"pinned H2D/D2H + {sh.mode} shards (cbp_forward_{sh.mode}/cbp_back_{sh.mode} or view "
-                    f"ranges)" + (" + NCCL all_reduce" if world > 1 and not slice_shard else ""),
+                    f"ranges)" + ((" + multicast BP" if mm is not None else " + NCCL all_reduce")
+                                   if world > 1 and not slice_shard else ""),
                "note": "a pipeline figure: steps follow each other without the L2 flush that separates the "
                        "device-timed steps of `value`, and PCIe copies overlap compute, so it can exceed "
                        "`value`" if piped else "synchronous steps"}
@@ -629,6 +672,7 @@ def main():
             "roofline": roof,
             "kernels": kernels,
             "timing": graph_note,
+            "bp_reduction": reduce_note,
             "allreduce_ms": statistics.mean(ar_ms) if world > 1 else 0.0,
             "cpu_baseline": cpu,
             "e2e": e2e,
