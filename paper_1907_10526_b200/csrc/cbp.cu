@@ -734,6 +734,80 @@ int get_headers(const cbp_geometry_t& g, const cbp::Tables& t, int32_t v0, int32
     return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
 }
 
+// ---- the persistent BP's plan (cbp_bp_plan_kernel): the
+// segments of an NB-CTA launch over (g, [v0, v0 + nv)).  Cached per device
+// next to the cached headers; recomputed per call (stream scratch) when the
+// headers are not cached.
+std::map<std::pair<HdrKey, int>, int*> g_plans;
+
+size_t plan_ints(int tiles, int NB) { return (size_t)(tiles + NB + 1) + (NB + 1) + (tiles + 1) + NB + (NB + 1); }
+
+int build_plan(const cbp::BPHeader* hdrs, int tiles, int nv, int NB, int* plan, cudaStream_t stream)
+{
+    int* cum = nullptr;
+    long long* pre = nullptr;
+    if (scratch_alloc((void**)&cum, sizeof(int) * (size_t)tiles * nv, stream) != CBP_OK) return CBP_ENOMEM;
+    if (scratch_alloc((void**)&pre, sizeof(long long) * (tiles + 1), stream) != CBP_OK) {
+        cudaFreeAsync(cum, stream);
+        return CBP_ENOMEM;
+    }
+    cbp::cbp_bp_plan_cost_kernel<<<tiles, 256, 0, stream>>>(hdrs, nv, cum, pre);
+    cbp::cbp_bp_plan_kernel<<<1, 1024, 0, stream>>>(cum, pre, tiles, nv, NB, plan);
+    g_launches += 2;
+    cudaFreeAsync(cum, stream);
+    cudaFreeAsync(pre, stream);
+    return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+}
+
+// *out: the plan; *owned: free it after use (stream-ordered)
+int get_plan(const cbp_geometry_t& g, int32_t v0, int32_t nv, int NB, const cbp::BPHeader* hdrs, bool hdrs_cached,
+             cudaStream_t stream, const int** out, int** owned)
+{
+    const int tiles1 = (g.n + cbp::BP_TILE - 1) / cbp::BP_TILE, tiles = tiles1 * tiles1;
+    const size_t bytes = sizeof(int) * plan_ints(tiles, NB);
+    *owned = nullptr;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return CBP_ECUDA;
+    if (hdrs_cached) {
+        HdrKey key;
+        std::memset(&key, 0, sizeof(key));
+        key.device = dev;
+        key.n = g.n;
+        key.n_views = g.n_views;
+        key.n_det = g.n_det;
+        key.kind = g.kind;
+        key.v0 = v0;
+        key.nv = nv;
+        key.pixel = g.pixel;
+        key.pitch = g.det_pitch;
+        key.tau = g.det_width;
+        key.sid = g.sid;
+        key.sdd = g.sdd;
+        std::lock_guard<std::mutex> lock(g_hdr_mu);
+        auto it = g_plans.find({key, NB});
+        if (it != g_plans.end()) {
+            *out = it->second;
+            return CBP_OK;
+        }
+        int* d = nullptr;
+        if (cudaMalloc(&d, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return CBP_ECUDA;
+        }
+        // shared across streams: finish building before publishing
+        if (build_plan(hdrs, tiles, nv, NB, d, stream) != CBP_OK || cudaStreamSynchronize(stream) != cudaSuccess) {
+            cudaFree(d);
+            return CBP_ECUDA;
+        }
+        g_plans.emplace(std::make_pair(key, NB), d);
+        *out = d;
+        return CBP_OK;
+    }
+    if (scratch_alloc((void**)owned, bytes, stream) != CBP_OK) return CBP_ENOMEM;
+    *out = *owned;
+    return build_plan(hdrs, tiles, nv, NB, *owned, stream);
+}
+
 // ---- BP orbit clusters: representative tiles of the orbits
 // of the dihedral group on the T x T tile grid (n = 32 T), per device
 std::mutex g_orbit_mu;
@@ -835,6 +909,7 @@ int launch_bp_orbit(const cbp_geometry_t& g, const cbp::Tables& t, const float* 
         if (rc != CBP_OK) return rc;
     }
     cbp::BPParams P;
+    std::memset(&P, 0, sizeof(P));
     const cbp::BPHeader* hdrs = nullptr;
     cbp::BPHeader* hdrs_owned = nullptr;
     if (get_pair_order(&P.pairs) != CBP_OK || get_headers(g, t, v0, nv, stream, &hdrs, &hdrs_owned) != CBP_OK) {
@@ -886,6 +961,132 @@ int launch_bp_orbit(const cbp_geometry_t& g, const cbp::Tables& t, const float* 
     return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
 }
 
+// CBP_BP_PROF=path (diagnostics, a -DCBP_BP_PROFILE build): the BP launches
+// record per-CTA start / end times, SMs and header features; each launch
+// appends "launch <ctas>" and one line per CTA to the file
+unsigned long long* bp_prof_begin(size_t ctas)
+{
+#ifndef CBP_BP_PROFILE
+    (void)ctas;
+    return nullptr;  // the timeline is compiled in only with -DCBP_BP_PROFILE (tools/bp_cta_prof.py)
+#endif
+    static const char* path = getenv("CBP_BP_PROF");
+    if (!path) return nullptr;
+    unsigned long long* d = nullptr;
+    if (cudaMalloc(&d, 64 * ctas) != cudaSuccess) return nullptr;
+    cudaMemset(d, 0, 64 * ctas);
+    return d;
+}
+void bp_prof_end(unsigned long long* d, size_t ctas, cudaStream_t stream)
+{
+    if (!d) return;
+    std::vector<unsigned long long> h(8 * ctas);
+    cudaStreamSynchronize(stream);
+    cudaMemcpy(h.data(), d, 64 * ctas, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    FILE* f = fopen(getenv("CBP_BP_PROF"), "a");
+    if (!f) return;
+    fprintf(f, "launch %zu\n", ctas);
+    for (size_t i = 0; i < ctas; ++i)
+        fprintf(f, "%llu %llu %llu %llu %llu %llu %llu\n", h[8 * i], h[8 * i + 1], h[8 * i + 2], h[8 * i + 3],
+                h[8 * i + 4], h[8 * i + 5], h[8 * i + 6]);
+    fclose(f);
+}
+
+// The persistent 8-frame BP: one wave of CTAs over cost-
+// balanced segments of the (tile, base view) pairs, compact per-segment
+// blocks, cbp_seg_reduce_kernel.  Opt-in (CBP_BP_SEG=1, read per call): it
+// does ~5 % less work than the view-group grid but a static split cannot
+// absorb the unequal progress of the two CTAs resident on an SM (measured:
+// 1.4 % faster at config 2, 7 % slower at configs 3 and 5).
+bool use_seg(const cbp_geometry_t& g, int32_t nv)
+{
+    const char* e = getenv("CBP_BP_SEG");
+    if (!e || e[0] != '1') return false;
+    const long long tiles = (g.n + cbp::BP_TILE - 1) / cbp::BP_TILE;
+    return tiles * tiles * (long long)nv < (1LL << 30);
+}
+
+// (accumulate: CBP_ACC_OVERWRITE or CBP_ACC_ADD; the multicast mode keeps the grid)
+int launch_bp_seg(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img, int32_t v0,
+                  int32_t nv, int32_t accumulate, cudaStream_t stream, int images)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = cbp::bp_smem_bytes(8, false);
+    static std::once_flag attr[64];
+    static int per_sm[64];
+    std::call_once(attr[dev & 63], [smem, dev] {
+        cudaFuncSetAttribute(cbp::cbp_bp_kernel<8, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        int k = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_bp_kernel<8, false, false, true>,
+                                                          cbp::BP_THREADS, smem) != cudaSuccess || k < 1)
+            k = 1;
+        per_sm[dev & 63] = k;
+    });
+    const char* nbenv = getenv("CBP_BP_SEG_CTAS");  // tuning knob (read per call)
+    const int NB = nbenv && atoi(nbenv) > 0 ? atoi(nbenv) : sms * per_sm[dev & 63];
+    const int tiles1 = (g.n + cbp::BP_TILE - 1) / cbp::BP_TILE, tiles = tiles1 * tiles1;
+    const cbp::BPHeader* hdrs = nullptr;
+    cbp::BPHeader* hdrs_owned = nullptr;
+    if (get_headers(g, t, v0, nv, stream, &hdrs, &hdrs_owned) != CBP_OK) return CBP_ECUDA;
+    const int* plan = nullptr;
+    int* plan_owned = nullptr;
+    int rc = get_plan(g, v0, nv, NB, hdrs, hdrs_owned == nullptr, stream, &plan, &plan_owned);
+    const int seg_max = tiles + NB;
+    float* blocks = nullptr;
+    if (rc == CBP_OK)
+        rc = scratch_alloc((void**)&blocks, sizeof(float) * images * seg_max * 8 * cbp::BP_TILE * cbp::BP_TILE, stream);
+    if (rc != CBP_OK) {
+        if (hdrs_owned) cudaFreeAsync(hdrs_owned, stream);
+        if (plan_owned) cudaFreeAsync(plan_owned, stream);
+        return rc;
+    }
+    cbp::BPParams P;
+    std::memset(&P, 0, sizeof(P));
+    if (get_pair_order(&P.pairs) != CBP_OK) return CBP_ECUDA;
+    P.g = to_dev(g);
+    P.t = t;
+    P.hdrs = hdrs;
+    P.sino = sino;
+    P.out = blocks;
+    P.sym_mode = 8;
+    P.images = images;
+    P.view_begin = v0;
+    P.view_count = nv;
+    P.groups = 1;
+    P.views_per_group = nv;
+    P.batch = 8;
+    P.seg_idx = plan;
+    P.cta_seg = plan + (tiles + NB + 1);
+    P.seg_max = seg_max;
+    P.prof = bp_prof_begin((size_t)NB * images);
+    launch_pdl(cbp::cbp_bp_kernel<8, false, false, true>, dim3(NB, 1, images), dim3(cbp::BP_THREADS), smem, stream,
+               P);
+    ++g_launches;
+    bp_prof_end(P.prof, (size_t)NB * images, stream);
+    if (hdrs_owned) cudaFreeAsync(hdrs_owned, stream);
+    {
+        const size_t plane = (size_t)g.n * g.n;
+        const int mode = accumulate ? 1 : 0;
+        const int* seg_first = P.cta_seg + NB + 1;
+        if (g.n % cbp::BP_TILE == 0) {
+            launch_pdl(cbp::cbp_seg_reduce_kernel<8>, dim3(tiles, images), dim3(256), 0, stream,
+                       (const float*)blocks, img, seg_first, g.n, seg_max, mode);
+        } else {
+            const int nblk = (int)std::min<size_t>((plane + 255) / 256, (size_t)sms * 8 / images + 1);
+            launch_pdl(cbp::cbp_seg_reduce_px_kernel<8>, dim3(std::max(nblk, 1), images), dim3(256), 0, stream,
+                       (const float*)blocks, img, seg_first, g.n, seg_max, mode);
+        }
+        ++g_launches;
+        cudaFreeAsync(blocks, stream);
+    }
+    if (plan_owned) cudaFreeAsync(plan_owned, stream);
+    return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+}
+
 template <int S, bool PREC = false>
 int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
                 int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream,
@@ -897,6 +1098,8 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     const bool sym = symmode != 0;
     if constexpr (S == 8 && !PREC) {
         if (symmode == 8 && use_orbit(g)) return launch_bp_orbit(g, t, sino, img, v0, nv, accumulate, stream, images);
+        if (symmode == 8 && accumulate != CBP_ACC_MULTIMEM && use_seg(g, nv))
+            return launch_bp_seg(g, t, sino, img, v0, nv, accumulate, stream, images);
     }
     if (sym) batch = symmode;
     int dev = 0, sms = 148;
@@ -932,6 +1135,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
         if (rc != CBP_OK) return rc;
     }
     cbp::BPParams P;
+    std::memset(&P, 0, sizeof(P));
     if (get_pair_order(&P.pairs) != CBP_OK) {
         if (part) cudaFreeAsync(part, stream);
         return CBP_ECUDA;
@@ -965,8 +1169,12 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     fprintf(stderr, "launch_bp S=%d G=%d vpg=%d grid=%d,%d,%d smem=%zu\n", S, G, vpg, grid.x, grid.y,
             grid.z, smem);
 #endif
+    P.seg_idx = P.cta_seg = nullptr;
+    P.seg_max = 0;
+    P.prof = bp_prof_begin((size_t)grid.x * grid.y * grid.z);
     launch_pdl(cbp::cbp_bp_kernel<S, PREC>, grid, dim3(cbp::BP_THREADS), smem, stream, P);
     ++g_launches;
+    bp_prof_end(P.prof, (size_t)grid.x * grid.y * grid.z, stream);
 #ifdef CBP_DEBUG_CHECKS
     fprintf(stderr, "bp kernel: %s\n", cudaGetErrorString(cudaStreamSynchronize(stream)));
 #endif

@@ -69,7 +69,34 @@ struct BPParams {
     // the 8 frames on the orbit_T x orbit_T tile grid
     const int2* orbit_reps;
     int orbit_T;
+    // persistent segments (cbp_bp_kernel<8, false, false, true>):
+    // the (tile, view) pairs of one image, tile-major, are cut into gridDim.x
+    // runs of equal estimated cost (cbp_bp_plan_kernel); CTA b walks segments
+    // cta_seg[b] .. cta_seg[b + 1] - 1 (a segment: one tile, views
+    // seg_idx[s] .. seg_idx[s + 1] - 1 of it, as tile * view_count + view) and
+    // writes each segment's S frame accumulators as a compact block
+    // out[image][seg][S][BP_TILE^2] (tile orientation) that cbp_seg_reduce_kernel
+    // maps onto the image
+    const int* seg_idx;
+    const int* cta_seg;
+    int seg_max;  // block slots per image (>= segments)
+    // CBP_BP_PROF (diagnostics, a -DCBP_BP_PROFILE build): per CTA start / end ns, SM,
+    // segments, header features
+    unsigned long long* prof;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+    return r;
+}
 
 constexpr int BP_TILE = 32;       // pixels per tile side
 constexpr int BP_THREADS = 256;   // 8 warps x 2 pairs x 2 pixels x 32 lanes = 32 x 32
@@ -687,8 +714,11 @@ __device__ void bp_orbit_epilogue(const BPParams& P, float* acc_s, const int (&m
     cluster.sync();  // the other CTAs' reads of this CTA's accumulators are done
 }
 
-template <int S, bool PREC = false, bool ORB = false>
-__global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp_bp_kernel(const BPParams P)
+// One CTA's work on one tile over views [vg0, vg0 + vgn) of the launch (view
+// group grp, slice group sg; seg: the segment of a persistent launch).
+template <int S, bool PREC, bool ORB, bool SEG>
+__device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_y, int tiles_x, int vg0, int vgn,
+                                        int grp, int sg, int seg, const int (&omem)[8], int osize)
 {
     static_assert(!PREC || S == 1, "the precise mode runs one slice per weight");
     static_assert(!ORB || (S == 8 && !PREC), "orbit clusters carry the 8 dihedral frames");
@@ -704,23 +734,6 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
 
     const GeomDev& g = P.g;
     const int tid = threadIdx.x;
-    const int grp = blockIdx.z % P.groups, sg = blockIdx.z / P.groups;  // view group, slice group
-    int vg0 = grp * P.views_per_group;
-    int vgn = max(0, min(P.views_per_group, P.view_count - vg0));
-    int tile_x = blockIdx.x, tile_y = blockIdx.y, tiles_x = gridDim.x;
-    int omem[8], osize = 1;
-    if constexpr (ORB) {
-        // cluster rank r takes orbit member r mod size over part r / size of the
-        // group's views (8 / size parts: a smaller orbit splits its views)
-        tiles_x = P.orbit_T;
-        osize = bp_orbit_members(P.orbit_T, P.orbit_reps[blockIdx.x / 8], omem);
-        const int rank = blockIdx.x % 8, parts = 8 / osize, part = rank / osize;
-        tile_x = omem[rank % osize] % tiles_x;
-        tile_y = omem[rank % osize] / tiles_x;
-        const int per = (vgn + parts - 1) / parts;
-        vg0 += part * per;
-        vgn = max(0, min(per, vgn - part * per));
-    }
     const int col0 = tile_x * BP_TILE, row0 = tile_y * BP_TILE;
     const int nchunks = (vgn + BP_VC - 1) / BP_VC;
     float hcx, hcy;  // anchor k_a = centre of the tile's valid pixels
@@ -738,8 +751,10 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
     };
 
     for (int i = tid; i < S * BP_TILE * (BP_TILE + 1); i += BP_THREADS) acc_s[i] = 0;
-    griddep_launch_dependents();  // the reduce may launch into this grid's tail
-    griddep_wait();               // the sinogram, headers and pool memory are ready
+    if constexpr (!SEG) {
+        griddep_launch_dependents();  // the reduce may launch into this grid's tail
+        griddep_wait();               // the sinogram, headers and pool memory are ready
+    }
 
     if constexpr (STAGE) {
         if (nchunks > 0) {
@@ -903,6 +918,7 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
         bp_orbit_epilogue(P, acc_s, omem, osize, grp, sg);
         return;
     }
+
     // Write the tile's sums.  With symmetry, slice q holds frame g_q = R^qq M^m
     // of the image; its values go straight to the output orientation (pixel
     // g_q(k)), so the partial planes are summed elementwise (cbp_reduce_kernel).
@@ -942,15 +958,23 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
         float* out = P.mc_fused ? P.out + (fsym ? (size_t)sg : (size_t)b) * plane : P.out + pi * plane;
         const int4 e0 = ep[q][0], e1 = ep[q][1];
         const int OR = e0.x, OC = e0.y, oh = e0.z, ow = e0.w, s0 = e1.x, sc = e1.y, sr = e1.z;
+        // the rectangle's origin and row pitch: the image, or (a persistent launch)
+        // the segment's compact block [q][oh][ow], also in output orientation
+        size_t pitch = n;
+        float* dst = out + (size_t)OR * n + OC;
+        if (SEG && !P.mc_fused) {
+            pitch = ow;
+            dst = P.out + (((size_t)sg * P.seg_max + seg) * S + q) * (BP_TILE * BP_TILE);
+        }
         const bp_acc_t<S>* a = acc_s + q * BP_TILE * LD;
-        const bool acc_out = P.groups == 1 && P.accumulate;
-        if (oh == BP_TILE && ow == BP_TILE && (n & 3) == 0 && !acc_out) {  // float4 stores
+        const bool acc_out = P.groups == 1 && P.accumulate && !SEG;
+        if (oh == BP_TILE && ow == BP_TILE && (pitch & 3) == 0 && !acc_out) {  // float4 stores
             for (int i = tid; i < BP_TILE * BP_TILE / 4; i += BP_THREADS) {
                 const int r = i / (BP_TILE / 4), c = (i % (BP_TILE / 4)) * 4;
                 const int si = s0 + r * sr + c * sc;
                 const float4 v = make_float4((float)a[si], (float)a[si + sc], (float)a[si + 2 * sc],
                                              (float)a[si + 3 * sc]);
-                float4* o = reinterpret_cast<float4*>(out + (size_t)(OR + r) * n + OC + c);
+                float4* o = reinterpret_cast<float4*>(dst + r * pitch + c);
                 if (P.mc_fused)
                     mc_red_add4(o, v);
                 else
@@ -960,7 +984,7 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
             for (int i = tid; i < BP_TILE * BP_TILE; i += BP_THREADS) {
                 const int r = i / BP_TILE, c = i % BP_TILE;
                 if (r < oh && c < ow) {
-                    float* o = out + (size_t)(OR + r) * n + OC + c;
+                    float* o = dst + r * pitch + c;
                     const float v = (float)a[s0 + r * sr + c * sc];
                     if (P.mc_fused)
                         mc_red_add(o, v);
@@ -969,6 +993,293 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
                 }
             }
         }
+    }
+}
+
+template <int S, bool PREC = false, bool ORB = false, bool SEG = false>
+__global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp_bp_kernel(const BPParams P)
+{
+    int omem[8], osize = 1;
+#ifdef CBP_BP_PROFILE
+    const unsigned long long t_start = P.prof ? globaltimer() : 0;
+    unsigned long long f_bins = 0, f_cov = 0, f_views = 0;  // the CTA's header features
+    auto prof_feat = [&](int tile, int v0, int len) {
+        if (P.prof && threadIdx.x == 0)
+            for (int v = v0; v < v0 + len; ++v) {
+                const BPHeader& H = P.hdrs[(size_t)tile * P.view_count + v];
+                ++f_views;
+                if (H.npass_f > 0.0f) {
+                    ++f_cov;
+                    f_bins += H.jhi - H.jlo + 1;
+                }
+            }
+    };
+    auto prof_end = [&](int segs) {
+        if (P.prof && threadIdx.x == 0) {
+            const size_t cta = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
+            unsigned long long* r = P.prof + 8 * cta;
+            r[0] = t_start;
+            r[1] = globaltimer();
+            r[2] = smid();
+            r[3] = segs;
+            r[4] = f_bins;
+            r[5] = f_cov;
+            r[6] = f_views;
+        }
+    };
+#else
+    auto prof_feat = [](int, int, int) {};
+    auto prof_end = [](int) {};
+#endif
+    if constexpr (SEG) {
+        static_assert(!ORB, "segments and orbit clusters are separate launch modes");
+        griddep_launch_dependents();  // the reduce may launch into this grid's tail
+        griddep_wait();               // the sinogram, headers, plan and pool memory are ready
+        const int tiles_x = (P.g.n + BP_TILE - 1) / BP_TILE;
+        const int s0 = P.cta_seg[blockIdx.x], s1 = P.cta_seg[blockIdx.x + 1];
+        for (int s = s0; s < s1; ++s) {
+            const int i0 = P.seg_idx[s], len = P.seg_idx[s + 1] - i0;
+            const int tile = i0 / P.view_count, v0 = i0 - tile * P.view_count;
+            if (s > s0) __syncthreads();  // the previous segment's epilogue is done with acc_s
+            prof_feat(tile, v0, len);
+            bp_body<S, PREC, ORB, SEG>(P, tile % tiles_x, tile / tiles_x, tiles_x, v0, len, 0, blockIdx.z, s, omem,
+                                       osize);
+        }
+        prof_end(s1 - s0);
+        return;
+    }
+    const int grp = blockIdx.z % P.groups, sg = blockIdx.z / P.groups;  // view group, slice group
+    int vg0 = grp * P.views_per_group;
+    int vgn = max(0, min(P.views_per_group, P.view_count - vg0));
+    int tile_x = blockIdx.x, tile_y = blockIdx.y, tiles_x = gridDim.x;
+    if constexpr (ORB) {
+        // cluster rank r takes orbit member r mod size over part r / size of the
+        // group's views (8 / size parts: a smaller orbit splits its views)
+        tiles_x = P.orbit_T;
+        osize = bp_orbit_members(P.orbit_T, P.orbit_reps[blockIdx.x / 8], omem);
+        const int rank = blockIdx.x % 8, parts = 8 / osize, part = rank / osize;
+        tile_x = omem[rank % osize] % tiles_x;
+        tile_y = omem[rank % osize] / tiles_x;
+        const int per = (vgn + parts - 1) / parts;
+        vg0 += part * per;
+        vgn = max(0, min(per, vgn - part * per));
+    }
+    if (!ORB) prof_feat(tile_y * tiles_x + tile_x, vg0, vgn);
+    bp_body<S, PREC, ORB, SEG>(P, tile_x, tile_y, tiles_x, vg0, vgn, grp, sg, 0, omem, osize);
+    prof_end(1);
+}
+
+// ---- the persistent BP's plan (per geometry and view range, cached with the
+// headers).  Estimated cost of tile t, view v: the bins of its range plus a
+// fixed per-view share (set-up, window, barriers), in bin units; a view that
+// misses the tile costs little.
+constexpr int BP_PLAN_VIEW = 12, BP_PLAN_MISS = 2;
+
+__device__ __forceinline__ int bp_plan_cost(const BPHeader& H)
+{
+    return H.npass_f > 0.0f ? H.jhi - H.jlo + 1 + BP_PLAN_VIEW : BP_PLAN_MISS;
+}
+
+// one CTA per tile: cum[t][v] = inclusive prefix of the tile's view costs,
+// tot[t] = the tile's total
+__global__ void __launch_bounds__(256) cbp_bp_plan_cost_kernel(const BPHeader* __restrict__ hdrs, int nv,
+                                                               int* __restrict__ cum, long long* __restrict__ tot)
+{
+    __shared__ int part[256];
+    __shared__ int carry;
+    const int t = blockIdx.x, tid = threadIdx.x;
+    if (tid == 0) carry = 0;
+    for (int v0 = 0; v0 < nv; v0 += 256) {
+        const int v = v0 + tid;
+        int c = v < nv ? bp_plan_cost(hdrs[(size_t)t * nv + v]) : 0;
+        part[tid] = c;
+        __syncthreads();
+        for (int off = 1; off < 256; off <<= 1) {  // Hillis-Steele inclusive scan
+            const int add = tid >= off ? part[tid - off] : 0;
+            __syncthreads();
+            part[tid] += add;
+            __syncthreads();
+        }
+        if (v < nv) cum[(size_t)t * nv + v] = carry + part[tid];
+        __syncthreads();
+        if (tid == 255) carry += part[255];
+        __syncthreads();
+    }
+    if (tid == 0) tot[t] = carry;
+}
+
+// one CTA: the segments of an NB-CTA persistent launch.  plan layout (ints):
+// seg_idx[tiles + NB + 1] | cta_seg[NB + 1] | seg_first[tiles + 1] | D[NB] | starts[NB + 1]
+// with pre[tiles + 1] (int64) the tiles' exclusive cost prefix.
+__global__ void __launch_bounds__(1024) cbp_bp_plan_kernel(const int* __restrict__ cum, long long* __restrict__ pre,
+                                                           int tiles, int nv, int NB, int* __restrict__ plan)
+{
+    int* seg_idx = plan;
+    int* cta_seg = seg_idx + tiles + NB + 1;
+    int* seg_first = cta_seg + NB + 1;
+    int* D = seg_first + tiles + 1;
+    int* starts = D + NB;
+    __shared__ long long ssum[1024];
+    __shared__ int sflag[1024];
+    __shared__ int nD;
+    const int tid = threadIdx.x;
+    // 1. exclusive prefix of the tile totals (pre holds the totals on entry)
+    const int per = (tiles + 1023) / 1024, a = min(tiles, tid * per), b = min(tiles, a + per);
+    long long s = 0;
+    for (int i = a; i < b; ++i) s += pre[i];
+    ssum[tid] = s;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        const long long add = tid >= off ? ssum[tid - off] : 0;
+        __syncthreads();
+        ssum[tid] += add;
+        __syncthreads();
+    }
+    long long run = ssum[tid] - s;
+    for (int i = a; i < b; ++i) {
+        const long long v = pre[i];
+        pre[i] = run;
+        run += v;
+    }
+    if (tid == 1023) pre[tiles] = ssum[1023];
+    __syncthreads();
+    const long long total = pre[tiles];
+    const int T = tiles * nv;
+    // 2. CTA b starts at the (tile, view) whose cost interval holds b total / NB
+    for (int bb = tid; bb < NB; bb += 1024) {
+        const long long target = (long long)bb * total / NB;
+        int lo = 0, hi = tiles - 1;  // last tile with pre[t] <= target
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pre[mid] <= target) lo = mid; else hi = mid - 1;
+        }
+        const long long local = target - pre[lo];
+        int vl = 0, vh = nv - 1;  // first view with cum > local
+        const int* c = cum + (size_t)lo * nv;
+        while (vl < vh) {
+            const int mid = (vl + vh) >> 1;
+            if (c[mid] > local) vh = mid; else vl = mid + 1;
+        }
+        starts[bb] = lo * nv + vl;
+    }
+    if (tid == 0) starts[NB] = T;
+    __syncthreads();
+    // 3. D = the distinct CTA starts inside a tile (tile starts are boundaries anyway)
+    if (tid == 0) {
+        int k = 0;
+        for (int bb = 0; bb < NB; ++bb) {
+            const int x = starts[bb];
+            if (x % nv != 0 && (k == 0 || D[k - 1] != x)) D[k++] = x;
+        }
+        nD = k;
+    }
+    (void)sflag;
+    __syncthreads();
+    const int nd = nD, nseg = tiles + nd;
+    auto below = [&](int x) {  // #{d in D : d < x}
+        int l = 0, h = nd;
+        while (l < h) {
+            const int m = (l + h) >> 1;
+            if (D[m] < x) l = m + 1; else h = m;
+        }
+        return l;
+    };
+    for (int t = tid; t < tiles; t += 1024) {
+        const int r = t + below(t * nv);
+        seg_idx[r] = t * nv;
+        seg_first[t] = r;
+    }
+    for (int i = tid; i < nd; i += 1024) seg_idx[(D[i] + nv - 1) / nv + i] = D[i];
+    for (int bb = tid; bb < NB; bb += 1024) {
+        const int x = starts[bb];
+        cta_seg[bb] = (x + nv - 1) / nv + below(x);
+    }
+    if (tid == 0) {
+        seg_idx[nseg] = T;
+        cta_seg[NB] = nseg;
+        seg_first[tiles] = nseg;
+    }
+}
+
+// out[image][p] (+)= sum over frames q (fixed order) and the segments of the
+// tile holding k = g_q^-1(p) (in order) of block[image][seg][q] at p: the
+// persistent BP's reduction, deterministic.  Blocks are in output orientation
+// (g_q of the tile's rectangle, row pitch = its width).  n a multiple of
+// BP_TILE (frames map tiles onto tiles): one CTA per output tile, float4 rows;
+// else one thread per pixel (cbp_seg_reduce_px_kernel).  S = 8: the dihedral
+// frames.  mode 1 adds to out, 2 adds through a multicast address.
+template <int S>
+__global__ void __launch_bounds__(256) cbp_seg_reduce_kernel(const float* __restrict__ blocks, float* __restrict__ out,
+                                                             const int* __restrict__ seg_first, int n, int seg_max,
+                                                             int accumulate)
+{
+    griddep_wait();  // the BP's blocks
+    constexpr int TT = BP_TILE * BP_TILE;
+    const int T = n / BP_TILE, U = blockIdx.x, ur = U / T, uc = U % T, tid = threadIdx.x;
+    __shared__ int2 segs[S];
+    if (tid < S) {
+        int tr = ur, tc = uc;  // the source tile of frame q on the T x T tile grid
+        if constexpr (S == 8) frame_inv(T, tid & 3, tid >> 2, tr, tc);
+        const int t = tr * T + tc;
+        segs[tid] = make_int2(__ldg(seg_first + t), __ldg(seg_first + t + 1));
+    }
+    __syncthreads();
+    blocks += (size_t)blockIdx.y * seg_max * S * TT;
+    out += (size_t)blockIdx.y * n * n;
+    const int r = tid / (BP_TILE / 4), c = (tid % (BP_TILE / 4)) * 4;  // 256 threads x 4 pixels
+    float4* o = reinterpret_cast<float4*>(out + (size_t)(ur * BP_TILE + r) * n + uc * BP_TILE + c);
+    float4 v = accumulate == 1 ? *o : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+        const int2 sr = segs[q];
+        for (int s = sr.x; s < sr.y; ++s) {
+            const float4 b = __ldg(reinterpret_cast<const float4*>(blocks + ((size_t)s * S + q) * TT) + tid);
+            v.x += b.x;
+            v.y += b.y;
+            v.z += b.z;
+            v.w += b.w;
+        }
+    }
+    if (accumulate == 2)
+        mc_red_add4(o, v);
+    else
+        *o = v;
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) cbp_seg_reduce_px_kernel(const float* __restrict__ blocks,
+                                                                float* __restrict__ out,
+                                                                const int* __restrict__ seg_first, int n,
+                                                                int seg_max, int accumulate)
+{
+    griddep_wait();  // the BP's blocks
+    constexpr int TT = BP_TILE * BP_TILE;
+    const int tiles_x = (n + BP_TILE - 1) / BP_TILE;
+    const size_t plane = (size_t)n * n;
+    blocks += (size_t)blockIdx.y * seg_max * S * TT;
+    out += (size_t)blockIdx.y * plane;
+    for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < plane; p += (size_t)gridDim.x * blockDim.x) {
+        const int r = (int)(p / n), c = (int)(p % n);
+        float v = accumulate == 1 ? out[p] : 0.0f;
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+            int kr = r, kc = c;
+            const int qq = S == 8 ? (q & 3) : 0, m = S == 8 ? (q >> 2) : 0;
+            frame_inv(n, qq, m, kr, kc);
+            const int tr = kr / BP_TILE, tc = kc / BP_TILE;
+            // g_q of the source tile's rectangle: origin and width (as the BP's epilogue)
+            const int row0 = tr * BP_TILE, col0 = tc * BP_TILE;
+            int ra = row0, ca = col0, rb = min(row0 + BP_TILE, n) - 1, cb = min(col0 + BP_TILE, n) - 1;
+            frame_fwd(n, qq, m, ra, ca);
+            frame_fwd(n, qq, m, rb, cb);
+            const int off = q * TT + (r - min(ra, rb)) * (abs(ca - cb) + 1) + (c - min(ca, cb));
+            const int t = tr * tiles_x + tc, s1 = __ldg(seg_first + t + 1);
+            for (int s = __ldg(seg_first + t); s < s1; ++s) v += __ldg(blocks + (size_t)s * S * TT + off);
+        }
+        if (accumulate == 2)
+            mc_red_add(out + p, v);
+        else
+            out[p] = v;
     }
 }
 
