@@ -33,7 +33,10 @@
  * workspace with cudaMemcpyAsync on `stream`, and the call then synchronises
  * `stream` before returning so the host result is ready.  The caller owns
  * every buffer; the library never retains a data pointer.  Per-geometry
- * tables (a few KB) are cached per device, guarded by a mutex.
+ * tables (a few KB) and the BP's per-(tile, view) headers (96 B each: up to
+ * 256 MB per geometry and view range, 1 GB in all; beyond that they are
+ * rebuilt per call in stream-ordered scratch) are cached per device until the
+ * process exits, guarded by a mutex.
  *
  * Streams: `stream` is a cudaStream_t (0 = legacy default stream).  With
  * device pointers all work is stream-ordered and asynchronous: execution

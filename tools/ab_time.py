@@ -1,6 +1,6 @@
 """A/B timing of library builds: for each libcbp*.so given, time the FP and
 BP of one config (warm L2, CUDA events, interleaved rounds so clock drift
-hits every build alike).  usage: python tools/ab_time.py CFG lib1.so lib2.so ..."""
+hits every build alike).  usage: [AB_BATCH=B] python tools/ab_time.py CFG lib1.so lib2.so ..."""
 import json
 import os
 import subprocess
@@ -14,6 +14,8 @@ sys.path.insert(0, %r)
 import paper_1907_10526_b200 as cbp, workloads as W
 g = dict(W.geometry(%r), model=int(os.environ.get("AB_MODEL", "0")))
 img = torch.from_numpy(W.shepp_logan(g["n"])).cuda()
+if int(os.environ.get("AB_BATCH", "1")) > 1:  # a batch of slices (e.g. config 4: 64)
+    img = img.expand(int(os.environ["AB_BATCH"]), -1, -1).contiguous()
 y = cbp.forward(g, img); c = cbp.back(g, y)
 def t(fn, reps=30):
     for _ in range(3): fn()
