@@ -454,8 +454,11 @@ __device__ __forceinline__ void bp_pair(const BPEntry* row, const float* yrow, i
 // per-tile accumulators: FP64 for S <= 2, FP32 for S >= 4 (shared-memory
 // budget; each term is already a partial over a run of views)
 // one loop for both of a lane's pixel pairs (see cbp_bp_kernel)
+#ifndef CBP_BP_UNION8  // A/B knob: 0 = two exact-window loops at S = 8 as well
+#define CBP_BP_UNION8 1
+#endif
 template <int S>
-constexpr bool BP_UNION = S == 8;
+constexpr bool BP_UNION = S == 8 && CBP_BP_UNION8;
 
 // two pixel pairs over the same entries [jl, jh] (one set of shared loads,
 // two independent weight chains)
