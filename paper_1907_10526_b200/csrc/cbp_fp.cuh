@@ -72,9 +72,13 @@ constexpr int FP_KMAX_UNROLLED = 6;
 
 // ---- zero-padded (and transposed) image copies, S slices interleaved ------
 constexpr int PAD_TILE = 32;
+#ifndef CBP_PAD_ROWS  // threads per tile column of the pad kernels (A/B knob)
+#define CBP_PAD_ROWS 8
+#endif
+constexpr int PAD_ROWS = CBP_PAD_ROWS;  // a CTA is PAD_TILE x PAD_ROWS threads
 
 template <int S>
-__global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_kernel(const float* __restrict__ img,
+__global__ void __launch_bounds__(PAD_TILE * PAD_ROWS) cbp_pad_kernel(const float* __restrict__ img,
                                                                float* __restrict__ pad,
                                                                float* __restrict__ padT, int n,
                                                                int P, int np, int batch)
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_kernel(const float* __re
     const int r0 = blockIdx.y * PAD_TILE, c0 = blockIdx.x * PAD_TILE;
     float* dst = pad + (size_t)grp * np * np * S;
     float* dstT = padT + (size_t)grp * np * np * S;
-    for (int rr = threadIdx.y; rr < PAD_TILE; rr += 8) {
+    for (int rr = threadIdx.y; rr < PAD_TILE; rr += PAD_ROWS) {
         const int r = r0 + rr, c = c0 + threadIdx.x;
         const int sr = r - P, sc = c - P;
         const bool in = sr >= 0 && sr < n && sc >= 0 && sc < n;
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_kernel(const float* __re
         }
     }
     __syncthreads();
-    for (int cc = threadIdx.y; cc < PAD_TILE; cc += 8) {
+    for (int cc = threadIdx.y; cc < PAD_TILE; cc += PAD_ROWS) {
         const int c = c0 + cc, r = r0 + threadIdx.x;
         if (r < np && c < np)
 #pragma unroll
@@ -121,7 +125,7 @@ __device__ __forceinline__ void rot90_pow(int n, int q, int& r, int& c)
 }
 
 template <bool TRANSPOSE>
-__global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym4_kernel(const float* __restrict__ img,
+__global__ void __launch_bounds__(PAD_TILE * PAD_ROWS) cbp_pad_sym4_kernel(const float* __restrict__ img,
                                                                     float* __restrict__ pad,
                                                                     float* __restrict__ padT, int n,
                                                                     int P, int np)
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym4_kernel(const float*
     griddep_launch_dependents();  // the FP may launch and set up its rays meanwhile
     __shared__ float tile[PAD_TILE][PAD_TILE + 1][4];
     const int r0 = blockIdx.y * PAD_TILE, c0 = blockIdx.x * PAD_TILE;
-    for (int rr = threadIdx.y; rr < PAD_TILE; rr += 8) {
+    for (int rr = threadIdx.y; rr < PAD_TILE; rr += PAD_ROWS) {
         const int r = r0 + rr, c = c0 + threadIdx.x;
         const int sr = r - P, sc = c - P;
         const bool in = sr >= 0 && sr < n && sc >= 0 && sc < n;
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym4_kernel(const float*
     }
     if constexpr (!TRANSPOSE) return;  // the rot_rows FP reads pad only
     __syncthreads();
-    for (int cc = threadIdx.y; cc < PAD_TILE; cc += 8) {
+    for (int cc = threadIdx.y; cc < PAD_TILE; cc += PAD_ROWS) {
         const int c = c0 + cc, r = r0 + threadIdx.x;
         if (r < np && c < np) {
             const float* t = tile[threadIdx.x][cc];
@@ -162,7 +166,7 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym4_kernel(const float*
 // so y[view_g(v)][bin_m(j)] = sum_k c[g k] W(v, j, k): slice 4m + q of the
 // padded copy holds c o (R^q M^m).  Base views v in [0, n_views/8]; for v = 0
 // and v = n_views/8 the mirrored frames repeat the rotated ones.
-__global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym8_kernel(const float* __restrict__ img,
+__global__ void __launch_bounds__(PAD_TILE * PAD_ROWS) cbp_pad_sym8_kernel(const float* __restrict__ img,
                                                                     float* __restrict__ pad,
                                                                     float* __restrict__ padT, int n,
                                                                     int P, int np)
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym8_kernel(const float*
     griddep_launch_dependents();  // the FP may launch and set up its rays meanwhile
     __shared__ float tile[PAD_TILE][PAD_TILE + 1][8];
     const int r0 = blockIdx.y * PAD_TILE, c0 = blockIdx.x * PAD_TILE;
-    for (int rr = threadIdx.y; rr < PAD_TILE; rr += 8) {
+    for (int rr = threadIdx.y; rr < PAD_TILE; rr += PAD_ROWS) {
         const int r = r0 + rr, c = c0 + threadIdx.x;
         const int sr = r - P, sc = c - P;
         const bool in = sr >= 0 && sr < n && sc >= 0 && sc < n;
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(PAD_TILE * 8) cbp_pad_sym8_kernel(const float*
         }
     }
     __syncthreads();
-    for (int cc = threadIdx.y; cc < PAD_TILE; cc += 8) {
+    for (int cc = threadIdx.y; cc < PAD_TILE; cc += PAD_ROWS) {
         const int c = c0 + cc, r = r0 + threadIdx.x;
         if (r < np && c < np) {
             const float* t = tile[threadIdx.x][cc];
