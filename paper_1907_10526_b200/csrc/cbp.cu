@@ -1047,7 +1047,12 @@ int launch_bp_seg(const cbp_geometry_t& g, const cbp::Tables& t, const float* si
     }
     cbp::BPParams P;
     std::memset(&P, 0, sizeof(P));
-    if (get_pair_order(&P.pairs) != CBP_OK) return CBP_ECUDA;
+    if (get_pair_order(&P.pairs) != CBP_OK) {
+        if (hdrs_owned) cudaFreeAsync(hdrs_owned, stream);
+        if (plan_owned) cudaFreeAsync(plan_owned, stream);
+        cudaFreeAsync(blocks, stream);
+        return CBP_ECUDA;
+    }
     P.g = to_dev(g);
     P.t = t;
     P.hdrs = hdrs;

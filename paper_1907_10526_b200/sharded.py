@@ -125,7 +125,11 @@ class MulticastImage:
         group = group or dist.group.WORLD
         self.buf = symm_mem.empty((n, n), dtype=torch.float32, device=device)
         self.hdl = symm_mem.rendezvous(self.buf, group)
-        self.mc = int(self.hdl.multicast_ptr) if self.hdl.has_multicast_support() else 0
+        # has_multicast_support is a static query (device type, index); the
+        # handle's multicast_ptr is 0 when the group got no multicast object
+        from torch._C._distributed_c10d import _SymmetricMemory
+        dev_ok = _SymmetricMemory.has_multicast_support(symm_mem.DeviceType.CUDA, self.buf.device.index)
+        self.mc = int(self.hdl.multicast_ptr) if dev_ok else 0
         if not self.mc:
             raise RuntimeError("no NVLink multicast support for this group")
 

@@ -30,3 +30,45 @@ def test_two_gpu_sharded_normal_operator():
         if "metrics" in x:
             rl2, mr = x["metrics"]
             assert rl2 <= REL_L2 and mr <= MAX_REL, x
+
+
+ONE_RANK = r'''
+import json, os, sys
+sys.path.insert(0, %r)
+import torch, torch.distributed as dist
+import numpy as np
+import oracle as O, paper_1907_10526_b200 as cbp, workloads as W
+from paper_1907_10526_b200 import sharded
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+g = dict(W.geometry("1"), n_views=88)
+try:
+    mm = sharded.MulticastImage(g["n"])
+except RuntimeError as e:  # the documented outcome without a multicast object
+    print(json.dumps({"multicast": False, "why": str(e)}))
+else:
+    y = W.random_sino(g["n_views"], g["n_det"], 61)
+    sh = sharded.make_shard(g["n_views"], 0, 1, dihedral=True)
+    got = sharded.back_sharded(g, torch.from_numpy(y).cuda(), sh, multimem=mm).cpu().numpy()
+    want = O.back(g, y)
+    err = float(np.abs(got - want).max() / np.abs(want).max())
+    print(json.dumps({"multicast": True, "maxrel": err}))
+dist.destroy_process_group()
+'''
+
+
+def test_multicast_image_on_one_rank():
+    """sharded.MulticastImage on a one-rank NCCL group: it either binds a
+    multicast address (then the fused BP matches the oracle) or raises the
+    documented RuntimeError -- never a TypeError / AttributeError from the
+    symmetric-memory API (round 2 called the static has_multicast_support
+    without arguments, so the fused path could never have been taken)."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29573")
+    res = subprocess.run([sys.executable, "-c", ONE_RANK % ROOT], cwd=ROOT, capture_output=True, text=True,
+                         timeout=600, env=env)
+    assert res.returncode == 0, res.stderr[-3000:]
+    out = [json.loads(x) for x in res.stdout.splitlines() if x.startswith("{")][-1]
+    if out["multicast"]:
+        assert out["maxrel"] <= MAX_REL, out
+    else:
+        assert "multicast" in out["why"], out
