@@ -371,7 +371,7 @@ def main():
     # through an NVLink multicast image (CBP_ACC_MULTIMEM, sharded.MulticastImage)
     # when the system has one and a first step agrees with the NCCL all-reduce;
     # else (or CBP_BENCH_NCCL=1) by NCCL's all_reduce after the BP
-    mm, reduce_note = None, ("NCCL all_reduce after the BP" if world > 1 and not slice_shard else "none")
+    mm, reduce_note = None, (f"{backend} all_reduce after the BP" if world > 1 and not slice_shard else "none")
     if world > 1 and not slice_shard and os.environ.get("CBP_BENCH_NCCL") != "1" and backend == "nccl":
         why = ""
         try:
