@@ -434,9 +434,9 @@ int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
     float* padT = rot ? nullptr : pad + plane;
     dim3 pgrid((np + cbp::PAD_TILE - 1) / cbp::PAD_TILE, (np + cbp::PAD_TILE - 1) / cbp::PAD_TILE, 1);
     if (rot)
-        cbp::cbp_pad_sym4_kernel<false><<<pgrid, dim3(cbp::PAD_TILE, cbp::PAD_ROWS), 0, stream>>>(img, pad, padT, g.n, P, np);
+        cbp::cbp_pad_sym4_kernel<false><<<pgrid, dim3(cbp::PAD_TILE, cbp::PAD4_ROWS), 0, stream>>>(img, pad, padT, g.n, P, np);
     else
-        cbp::cbp_pad_sym4_kernel<true><<<pgrid, dim3(cbp::PAD_TILE, cbp::PAD_ROWS), 0, stream>>>(img, pad, padT, g.n, P, np);
+        cbp::cbp_pad_sym4_kernel<true><<<pgrid, dim3(cbp::PAD_TILE, cbp::PAD4_ROWS), 0, stream>>>(img, pad, padT, g.n, P, np);
     ++g_launches;
     cbp::FPParams Pm;
     Pm.split = 0x7fffffff;

@@ -76,6 +76,9 @@ constexpr int PAD_TILE = 32;
 #define CBP_PAD_ROWS 8
 #endif
 constexpr int PAD_ROWS = CBP_PAD_ROWS;  // a CTA is PAD_TILE x PAD_ROWS threads
+// the 4-rotation pad: one row of each staged block per thread, 1024-thread CTAs
+// (measured at config 2: 5.6 / 6.4 / 8.5 us for 32 / 16 / 8 rows under ncu)
+constexpr int PAD4_ROWS = 32;
 
 template <int S>
 __global__ void __launch_bounds__(PAD_TILE * PAD_ROWS) cbp_pad_kernel(const float* __restrict__ img,
@@ -124,38 +127,55 @@ __device__ __forceinline__ void rot90_pow(int n, int q, int& r, int& c)
     }
 }
 
+// The 4 rotated copies: output pixel (R0 + i, C0 + t) of a 32 x 32 tile (image
+// coordinates, the padding offset removed) takes c o R^q, and R^q maps the
+// tile onto a 32 x 32 image block whose local index is a fixed permutation:
+//   q = 0: block (R0, C0),               value at [i][t]
+//   q = 1: block (n-32-C0, R0),          value at [31-t][i]
+//   q = 2: block (n-32-R0, n-32-C0),     value at [31-i][31-t]
+//   q = 3: block (C0, n-32-R0),          value at [t][31-i]
+// so the four blocks are staged with coalesced row loads (out-of-image
+// pixels load 0: the zero border) and gathered from shared memory for pad
+// (row-major) and padT (the transposed tile) without per-pixel rotation
+// arithmetic.  (Reading the rotated pixels straight from global memory walks
+// a column per warp for q = 1, 3: 17 sectors per request, L1-bound; and a
+// staged variant with per-pixel rotation maths was slower still.)
 template <bool TRANSPOSE>
-__global__ void __launch_bounds__(PAD_TILE * PAD_ROWS) cbp_pad_sym4_kernel(const float* __restrict__ img,
-                                                                    float* __restrict__ pad,
-                                                                    float* __restrict__ padT, int n,
-                                                                    int P, int np)
+__global__ void __launch_bounds__(PAD_TILE * PAD4_ROWS) cbp_pad_sym4_kernel(const float* __restrict__ img,
+                                                                          float* __restrict__ pad,
+                                                                          float* __restrict__ padT, int n,
+                                                                          int P, int np)
 {
     griddep_launch_dependents();  // the FP may launch and set up its rays meanwhile
-    __shared__ float tile[PAD_TILE][PAD_TILE + 1][4];
-    const int r0 = blockIdx.y * PAD_TILE, c0 = blockIdx.x * PAD_TILE;
-    for (int rr = threadIdx.y; rr < PAD_TILE; rr += PAD_ROWS) {
-        const int r = r0 + rr, c = c0 + threadIdx.x;
-        const int sr = r - P, sc = c - P;
-        const bool in = sr >= 0 && sr < n && sc >= 0 && sc < n;
-        float v[4];
+    __shared__ float S[4][PAD_TILE][PAD_TILE + 1];
+    const int r0 = blockIdx.y * PAD_TILE, c0 = blockIdx.x * PAD_TILE;  // padded coordinates
+    const int R0 = r0 - P, C0 = c0 - P, t = threadIdx.x;
+    const int ar[4] = {R0, n - PAD_TILE - C0, n - PAD_TILE - R0, C0};  // block origins (row, col)
+    const int ac[4] = {C0, R0, n - PAD_TILE - C0, n - PAD_TILE - R0};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            int a = sr, b = sc;
-            rot90_pow(n, q, a, b);
-            v[q] = in ? img[(size_t)a * n + b] : 0.0f;
-            if constexpr (TRANSPOSE) tile[rr][threadIdx.x][q] = v[q];
+    for (int q = 0; q < 4; ++q) {
+        const int b = ac[q] + t;
+        const bool bin = b >= 0 && b < n;
+#pragma unroll
+        for (int i = threadIdx.y; i < PAD_TILE; i += PAD4_ROWS) {
+            const int a = ar[q] + i;
+            S[q][i][t] = (bin && a >= 0 && a < n) ? __ldg(img + (size_t)a * n + b) : 0.0f;
         }
+    }
+    __syncthreads();
+    constexpr int L = PAD_TILE - 1;
+    for (int i = threadIdx.y; i < PAD_TILE; i += PAD4_ROWS) {
+        const int r = r0 + i, c = c0 + t;
         if (r < np && c < np)
-            *reinterpret_cast<float4*>(pad + ((size_t)r * np + c) * 4) = make_float4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<float4*>(pad + ((size_t)r * np + c) * 4) =
+                make_float4(S[0][i][t], S[1][L - t][i], S[2][L - i][L - t], S[3][t][L - i]);
     }
     if constexpr (!TRANSPOSE) return;  // the rot_rows FP reads pad only
-    __syncthreads();
-    for (int cc = threadIdx.y; cc < PAD_TILE; cc += PAD_ROWS) {
-        const int c = c0 + cc, r = r0 + threadIdx.x;
-        if (r < np && c < np) {
-            const float* t = tile[threadIdx.x][cc];
-            *reinterpret_cast<float4*>(padT + ((size_t)c * np + r) * 4) = make_float4(t[0], t[1], t[2], t[3]);
-        }
+    for (int i = threadIdx.y; i < PAD_TILE; i += PAD4_ROWS) {
+        const int r = r0 + t, c = c0 + i;  // pixel (r, c) of the tile, stored at padT[c][r]
+        if (r < np && c < np)
+            *reinterpret_cast<float4*>(padT + ((size_t)c * np + r) * 4) =
+                make_float4(S[0][t][i], S[1][L - i][t], S[2][L - t][L - i], S[3][i][L - t]);
     }
 }
 
