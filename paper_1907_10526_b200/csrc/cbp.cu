@@ -566,6 +566,7 @@ int launch_mag(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, 
     P.sino = nullptr;
     P.sino_in = nullptr;
     P.image_out = nullptr;
+    P.pad4 = nullptr;
     if (fp) {
         P.image = img;
         P.sino = sino;
@@ -575,10 +576,21 @@ int launch_mag(const cbp_geometry_t& g, const cbp::Tables& t, const float* img, 
             cbp::cbp_mag_fp_kernel<1, true><<<dim3(bins, nv, batch), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
         } else if (sym4) {
             P.view_count = g.n_views / 4;
-            if (warp_walk)
+            float* pad4 = nullptr;
+            if (warp_walk) {  // the 4 rotations interleaved per pixel (no border)
+                const dim3 pgrid((g.n + cbp::PAD_TILE - 1) / cbp::PAD_TILE, (g.n + cbp::PAD_TILE - 1) / cbp::PAD_TILE);
+                if (scratch_alloc((void**)&pad4, sizeof(float) * 4 * (size_t)g.n * g.n, stream) != CBP_OK)
+                    return CBP_ENOMEM;
+                cbp::cbp_pad_sym4_kernel<false><<<pgrid, dim3(cbp::PAD_TILE, cbp::PAD4_ROWS), 0, stream>>>(
+                    img, pad4, nullptr, g.n, 0, g.n);
+                ++g_launches;
+                P.pad4 = pad4;
                 cbp::cbp_mag_fpw_kernel<4><<<dim3(bins, g.n_views / 4, 1), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
-            else
-                cbp::cbp_mag_fp_kernel<4><<<dim3(bins, g.n_views / 4, 1), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
+                ++g_launches;
+                cudaFreeAsync(pad4, stream);
+                return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+            }
+            cbp::cbp_mag_fp_kernel<4><<<dim3(bins, g.n_views / 4, 1), cbp::MAG_FP_BLOCK, 0, stream>>>(P);
         } else {
             if (warp_walk)
                 cbp::cbp_mag_fpw_kernel<1><<<dim3(bins, nv, batch), cbp::MAG_FP_BLOCK, 0, stream>>>(P);

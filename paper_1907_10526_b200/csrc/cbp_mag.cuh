@@ -84,16 +84,16 @@ __device__ __forceinline__ MagFootprint mag_footprint(const GeomDev& g, double c
         const float r2 = __fmaf_rn(depf, depf, latf * latf);
         if (g.arc) {
             P = g.sdd * atan2(lat, dep);
-            f = __fdiv_rn(sdd, r2);
+            f = sdd * rcp_approx(r2);
             m = sdd * rsqrtf(r2);
         } else {
-            const float invf = __frcp_rn(depf);
+            const float invf = rcp_approx(depf);  // refined in FP64 below for P
             double r = (double)invf;
             r = __fma_rn(r, __fma_rn(-dep, r, 1.0), r);
             P = g.sdd * lat * r;
             f = sdd * invf * invf;
             const float Pf = (float)P;
-            m = __fdiv_rn(__fmaf_rn(Pf, Pf, sdd * sdd), sdd * sqrtf(r2));
+            m = __fmaf_rn(Pf, Pf, sdd * sdd) * rcp_approx(sdd * sqrtf(r2));
         }
         // grad P = f (dep e + lat u)
         gx = f * __fmaf_rn(depf, -suf, latf * cuf);
@@ -108,13 +108,13 @@ __device__ __forceinline__ MagFootprint mag_footprint(const GeomDev& g, double c
     MagFootprint fp;
     fp.P = P;
     fp.A = A;
-    fp.invC = __frcp_rn(C);  // C = 0 -> +inf: sat() eliminates the direction
+    fp.invC = rcp_approx(C);  // C = 0 -> +inf: sat() eliminates the direction
     fp.w1 = __fmaf_rn(-B, fp.invC, 1.0f);
     fp.zoff = 0.5f * (A - C) + 0.5f * B;
     fp.minAB = fminf(A, B);
     fp.hC = 0.5f * C;
     fp.sigma = 0.5f * (A + B + C);
-    fp.wscale = __fdiv_rn(h * h * m, A * B);
+    fp.wscale = h * h * m * rcp_approx(A * B);
     return fp;
 }
 
@@ -198,6 +198,10 @@ struct MagParams {
     int view_begin, view_count, batch, accumulate;
     int vg;            // BP: view groups per pixel (1, 2, 4)
     double sigma_max;  // upper bound of every pixel's support half-width
+    // FP over a full scan (F = 4): the image's 4 rotations interleaved per pixel,
+    // [n][n][4] (cbp_pad_sym4_kernel with no border): one coalesced float4 per
+    // staged pixel instead of 4 loads, two of them walking a column per warp
+    const float* pad4;
 };
 
 // The pixels k with P(k) > s' are those with G(k) = alpha lat(k) - beta dep(k) > 0
@@ -541,6 +545,17 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK, 5) cbp_mag_fpw_kernel(MagParams 
                 m.hC = fp.hC;
                 m.sigma = fp.sigma;
                 m.wscale = fp.wscale;
+                if constexpr (F == 4) {
+                    if (p.pad4) {
+                        const float4 v4 = __ldg(reinterpret_cast<const float4*>(p.pad4) + (size_t)row * n + col);
+                        m.val[0] = v4.x;
+                        m.val[1] = v4.y;
+                        m.val[2] = v4.z;
+                        m.val[3] = v4.w;
+                        st[t] = m;
+                        continue;
+                    }
+                }
 #pragma unroll
                 for (int q = 0; q < F; ++q) {
                     int rr = row, cc = col;
