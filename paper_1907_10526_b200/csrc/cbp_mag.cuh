@@ -36,6 +36,12 @@
 
 namespace cbp {
 
+#ifndef CBP_MAG_BRANCHLESS  // A/B knob: the FP walk's weight as a select (1) or an early-out (0)
+#define CBP_MAG_BRANCHLESS 1
+#endif
+#ifndef CBP_MAG_BP_BRANCHLESS  // the same for the BP's bin loop, 4 frames only (measured: config 2,
+#define CBP_MAG_BP_BRANCHLESS 1   // 4 frames, 0.528 -> 0.507 ms; config 3, 8 frames, 3.60 -> 4.38 ms)
+#endif
 constexpr int MAG_FP_BLOCK = 128;
 constexpr int MAG_BP_BLOCK = 128;
 
@@ -170,10 +176,15 @@ __device__ __forceinline__ float mag_weight_prec(const MagFootprint& fp, double 
 }
 
 // W at x = s - P(k) (exactly 0 outside the open support, ledger #15): the
-// scalar form of cnsf_num2 with B = tau
+// scalar form of cnsf_num2 with B = tau.  BRANCHLESS: the
+// support test selects the result instead of returning early (the FP's
+// lanes walk different candidate counts; a divergent early-out costs more
+// than the ~20 instructions it skips)
+template <bool BRANCHLESS = false>
 __device__ __forceinline__ float mag_weight_x(const MagFootprint& fp, float x, float B)
 {
-    if (!(fabsf(x) < fp.sigma)) return 0.0f;
+    const bool in = fabsf(x) < fp.sigma;
+    if (!BRANCHLESS && !in) return 0.0f;
     const float z11 = x + fp.zoff;
     const float z21 = z11 - fp.A;
     const float t11 = sat_fma(z11, fp.invC, 1.0f), t12 = sat_fma(z11, fp.invC, fp.w1);
@@ -183,7 +194,8 @@ __device__ __forceinline__ float mag_weight_x(const MagFootprint& fp, float x, f
     T = __fmaf_rn(-t21, t21, T);
     T = __fmaf_rn(t22, t22, T);
     const float trap = fmaxf(fmin3(z11, fp.minAB, B - z21), 0.0f);
-    return fp.wscale * __fmaf_rn(fp.hC, T, trap);
+    const float w = fp.wscale * __fmaf_rn(fp.hC, T, trap);
+    return BRANCHLESS ? (in ? w : 0.0f) : w;
 }
 
 __device__ __forceinline__ double mag_bin_s(const GeomDev& g, int j) { return ((double)j - g.cs) * g.pitch; }
@@ -533,6 +545,8 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK, 5) cbp_mag_fpw_kernel(MagParams 
             for (int t = lane; t < cnt; t += 32) {
                 const int i = base + t;
                 const int row = rows ? l : i, col = rows ? i : l;
+                float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);  // issued before the footprint maths
+                if (F == 4 && p.pad4) v4 = __ldg(reinterpret_cast<const float4*>(p.pad4) + (size_t)row * n + col);
                 const double kx = ((double)col - g.c0) * g.h, ky = (g.c0 - (double)row) * g.h;
                 const MagFootprint fp = mag_footprint(g, cu, su, kx, ky);
                 MagStaged<F> m;
@@ -547,7 +561,6 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK, 5) cbp_mag_fpw_kernel(MagParams 
                 m.wscale = fp.wscale;
                 if constexpr (F == 4) {
                     if (p.pad4) {
-                        const float4 v4 = __ldg(reinterpret_cast<const float4*>(p.pad4) + (size_t)row * n + col);
                         m.val[0] = v4.x;
                         m.val[1] = v4.y;
                         m.val[2] = v4.z;
@@ -582,7 +595,7 @@ __global__ void __launch_bounds__(MAG_FP_BLOCK, 5) cbp_mag_fpw_kernel(MagParams 
                     fp.hC = m.hC;
                     fp.sigma = m.sigma;
                     fp.wscale = m.wscale;
-                    const float wgt = mag_weight_x(fp, (float)(s[r] - fp.P), B);
+                    const float wgt = mag_weight_x<CBP_MAG_BRANCHLESS>(fp, (float)(s[r] - fp.P), B);
 #pragma unroll
                     for (int f = 0; f < F; ++f) acc[r][f] = __fmaf_rn(m.val[f], wgt, acc[r][f]);
                 }
@@ -683,7 +696,8 @@ __global__ void __launch_bounds__(MAG_BP_BLOCK) cbp_mag_bp_kernel(MagParams p)
         }
         double sj = mag_bin_s(g, ja);
         for (int j = ja; j <= jb; ++j, sj += g.pitch) {
-            const float wgt = PREC ? mag_weight_prec(fp, sj - fp.P, B) : mag_weight_x(fp, (float)(sj - fp.P), B);
+            const float wgt = PREC ? mag_weight_prec(fp, sj - fp.P, B)
+                                   : mag_weight_x<CBP_MAG_BP_BRANCHLESS && F == 4>(fp, (float)(sj - fp.P), B);
 #pragma unroll
             for (int q = 0; q < F; ++q) {
                 if (q < 4 || !diag) acc[q] = __fmaf_rn(__ldg(yq[q] + (q >= 4 ? -j : j)), wgt, acc[q]);
