@@ -721,12 +721,12 @@ int get_headers(const cbp_geometry_t& g, const cbp::Tables& t, int32_t v0, int32
             *out = it->second;
             return CBP_OK;
         }
-        if (bytes <= (256ull << 20) && g_hdr_bytes + bytes <= (1ull << 30)) {
-            cbp::BPHeader* d = nullptr;
-            if (cudaMalloc(&d, bytes) != cudaSuccess) {
-                cudaGetLastError();
-                return CBP_ECUDA;
-            }
+        cbp::BPHeader* d = nullptr;
+        if (bytes <= (256ull << 20) && g_hdr_bytes + bytes <= (1ull << 30) && cudaMalloc(&d, bytes) != cudaSuccess) {
+            cudaGetLastError();  // no room to cache them: build them per call below
+            d = nullptr;
+        }
+        if (d) {
             cbp::cbp_bp_header_kernel<<<grid, 128, 0, stream>>>(to_dev(g), t, v0, nv, tiles, d);
             ++g_launches;
             // shared across streams: finish building before publishing
@@ -804,17 +804,19 @@ int get_plan(const cbp_geometry_t& g, int32_t v0, int32_t nv, int NB, const cbp:
         }
         int* d = nullptr;
         if (cudaMalloc(&d, bytes) != cudaSuccess) {
-            cudaGetLastError();
-            return CBP_ECUDA;
+            cudaGetLastError();  // no room to cache it: build it per call below
+            d = nullptr;
         }
-        // shared across streams: finish building before publishing
-        if (build_plan(hdrs, tiles, nv, NB, d, stream) != CBP_OK || cudaStreamSynchronize(stream) != cudaSuccess) {
-            cudaFree(d);
-            return CBP_ECUDA;
+        if (d) {
+            // shared across streams: finish building before publishing
+            if (build_plan(hdrs, tiles, nv, NB, d, stream) != CBP_OK || cudaStreamSynchronize(stream) != cudaSuccess) {
+                cudaFree(d);
+                return CBP_ECUDA;
+            }
+            g_plans.emplace(std::make_pair(key, NB), d);
+            *out = d;
+            return CBP_OK;
         }
-        g_plans.emplace(std::make_pair(key, NB), d);
-        *out = d;
-        return CBP_OK;
     }
     if (scratch_alloc((void**)owned, bytes, stream) != CBP_OK) return CBP_ENOMEM;
     *out = *owned;
