@@ -1,4 +1,7 @@
-import os, sys
+"""ncu driver for one dihedral view shard (the W = 8 launch
+list): warm-up plus a few FP+BP pairs of rank 1's shard of a W-rank split.
+usage: python tools/shard_once.py [config] [world]"""
+import sys
 sys.path.insert(0, '.')
 import torch
 import paper_1907_10526_b200 as cbp
