@@ -1123,7 +1123,6 @@ __global__ void __launch_bounds__(1024) cbp_bp_plan_kernel(const int* __restrict
     int* D = seg_first + tiles + 1;
     int* starts = D + NB;
     __shared__ long long ssum[1024];
-    __shared__ int sflag[1024];
     __shared__ int nD;
     const int tid = threadIdx.x;
     // 1. exclusive prefix of the tile totals (pre holds the totals on entry)
@@ -1176,7 +1175,6 @@ __global__ void __launch_bounds__(1024) cbp_bp_plan_kernel(const int* __restrict
         }
         nD = k;
     }
-    (void)sflag;
     __syncthreads();
     const int nd = nD, nseg = tiles + nd;
     auto below = [&](int x) {  // #{d in D : d < x}
