@@ -6,7 +6,8 @@ shards, the normal operator and its host pipeline, the FP64 reference pair,
 the vector / TV kernels of the iterative loops, and (round 2) the precise
 mode for narrow bins (CNSF and magnified, every kind, batches), the
 one-slice BP over edge tiles the detector misses, the opt-in orbit-cluster
-BP and rot_rows FP.  Run under the debug build (libcbp_debug.so:
+BP and rot_rows FP, and (v53) the opt-in persistent BP, the staged
+4-rotation pad and the magnified model's pad-fed FP.  Run under the debug build (libcbp_debug.so:
 CBP_DEBUG_CHECKS index checks and a sync + error check after each launch)
 since compute-sanitizer is closed on this pool."""
 import os
@@ -83,6 +84,23 @@ os.environ["CBP_ORBIT"] = "1"
 pair(dict(g1, n_views=88))
 pair(dict(g1, n=96, n_det=192, n_views=48))
 os.environ.pop("CBP_ORBIT")
+# round 2 (v53): the opt-in persistent BP (both reductions: n a multiple of 32
+# and ragged; many and few CTAs; a batch; a dihedral shard), the staged
+# 4-rotation pad at a ragged size, the magnified model's 4-fold FP on its pad
+os.environ["CBP_BP_SEG"] = "1"
+pair(dict(g1, n_views=88))
+pair(dict(rag, n_views=32))
+pair(dict(g1, n_views=88), batch=3)
+os.environ["CBP_BP_SEG_CTAS"] = "5"
+pair(dict(g1, n=96, n_det=192, n_views=48))
+os.environ["CBP_BP_SEG_CTAS"] = "3000"
+pair(dict(g1, n_views=88))
+os.environ.pop("CBP_BP_SEG_CTAS")
+sh = sharded.make_shard(88, 1, 3, dihedral=True)
+cbp.back_dihedral(dict(g1, n_views=88), cbp.forward(dict(g1, n_views=88), img), sh.begin, sh.count)
+os.environ.pop("CBP_BP_SEG")
+pair(dict(n=70, pixel=0.9, n_views=92, n_det=150, det_pitch=1.1, det_width=1.0, sid=200.0, sdd=400.0))
+pair(dict(n=70, pixel=0.9, n_views=92, n_det=150, det_pitch=1.1, det_width=1.0, sid=200.0, sdd=400.0, model=1))
 # reference projector
 gs = dict(g1, n=16, n_views=6, n_det=40)
 yr = cbp.ref_forward(gs, torch.from_numpy(W.random_image(16, 3)).cuda())
