@@ -1204,7 +1204,8 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
         const size_t count = sym ? plane : plane * batch;
         const int planes = sym ? G * batch : G;
         const int outs = sym ? images : 1;  // symmetric batch: one reduction per image
-        const int blocks = (int)std::min<size_t>((count / 4 + 255) / 256, (size_t)sms * 8 / outs + 1);
+        const size_t lanes = planes >= 16 && planes % 32 == 0 ? count : count / 4;  // 4 lanes per float4 (quad)
+        const int blocks = (int)std::min<size_t>((lanes + 255) / 256, (size_t)sms * 8 / outs + 1);
         launch_pdl(cbp::cbp_reduce_kernel, dim3(std::max(blocks, 1), outs), dim3(256), 0, stream,
                    (const float*)part, img, count, planes, mc ? 2 : (accumulate ? 1 : 0));
         ++g_launches;

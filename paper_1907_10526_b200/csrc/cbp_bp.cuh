@@ -1290,6 +1290,9 @@ __global__ void __launch_bounds__(256) cbp_seg_reduce_px_kernel(const float* __r
 // out + y count).  mode 2: out is a multicast address and the sum is ADDED
 // to every rank's copy by multimem.red (the view-sharded all-reduce of row a7
 // fused into the BP's last kernel; order across ranks is the switch's).
+#ifndef CBP_REDUCE_QUAD  // A/B knob: four lanes per float4 when there are many planes
+#define CBP_REDUCE_QUAD 1
+#endif
 __global__ void cbp_reduce_kernel(const float* __restrict__ part, float* __restrict__ out,
                                   size_t count, int groups, int accumulate)
 {
@@ -1298,7 +1301,57 @@ __global__ void cbp_reduce_kernel(const float* __restrict__ part, float* __restr
     out += (size_t)blockIdx.y * count;
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     const size_t t0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    if (((count & 3) | (reinterpret_cast<uintptr_t>(part) & 15) | (reinterpret_cast<uintptr_t>(out) & 15)) == 0) {
+    const bool aligned =
+        ((count & 3) | (reinterpret_cast<uintptr_t>(part) & 15) | (reinterpret_cast<uintptr_t>(out) & 15)) == 0;
+    if (aligned && CBP_REDUCE_QUAD && groups >= 16 && groups % 32 == 0) {
+        // many planes: four lanes per float4, each summing a quarter of the
+        // planes (8 loads in flight), combined as (q0 + q1) + (q2 + q3) --
+        // a fixed order, so the result stays deterministic
+        const size_t c4 = count / 4, total = 4 * c4;
+        const float4* p4 = reinterpret_cast<const float4*>(part);
+        float4* o4 = reinterpret_cast<float4*>(out);
+        const int lane = threadIdx.x & 31, qq = lane & 3, per = groups / 4;
+        for (size_t t = t0 - lane; t < total; t += stride) {  // warp-uniform trip count
+            const size_t tt = t + lane, i = tt >> 2;
+            const bool ok = tt < total;
+            float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ok) {
+                for (int gi = qq * per; gi < (qq + 1) * per; gi += 8) {
+                    float4 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = __ldg(p4 + (size_t)(gi + u) * c4 + i);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        s.x += v[u].x;
+                        s.y += v[u].y;
+                        s.z += v[u].z;
+                        s.w += v[u].w;
+                    }
+                }
+            }
+            float4 o;  // (q0 + q1) + (q2 + q3) on lane q0 of the quad
+            o.x = s.x + __shfl_down_sync(0xffffffffu, s.x, 1);
+            o.y = s.y + __shfl_down_sync(0xffffffffu, s.y, 1);
+            o.z = s.z + __shfl_down_sync(0xffffffffu, s.z, 1);
+            o.w = s.w + __shfl_down_sync(0xffffffffu, s.w, 1);
+            o.x += __shfl_down_sync(0xffffffffu, o.x, 2);
+            o.y += __shfl_down_sync(0xffffffffu, o.y, 2);
+            o.z += __shfl_down_sync(0xffffffffu, o.z, 2);
+            o.w += __shfl_down_sync(0xffffffffu, o.w, 2);
+            if (ok && qq == 0) {
+                if (accumulate == 1) {
+                    const float4 a = o4[i];
+                    o = make_float4(a.x + o.x, a.y + o.y, a.z + o.z, a.w + o.w);
+                }
+                if (accumulate == 2)
+                    mc_red_add4(o4 + i, o);
+                else
+                    o4[i] = o;
+            }
+        }
+        return;
+    }
+    if (aligned) {
         const size_t c4 = count / 4;
         const float4* p4 = reinterpret_cast<const float4*>(part);
         float4* o4 = reinterpret_cast<float4*>(out);
