@@ -1184,6 +1184,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     P.views_per_group = vpg;
     P.batch = batch;
     P.accumulate = (G == 1 && !sym && !mc && !mc_fused && accumulate) ? 1 : 0;
+    P.hdr_ready = hdrs_owned == nullptr ? 1 : 0;  // cached: complete before this launch
     dim3 grid(tiles, tiles, G * SG);
 #ifdef CBP_DEBUG_CHECKS
     fprintf(stderr, "launch_bp S=%d G=%d vpg=%d grid=%d,%d,%d smem=%zu\n", S, G, vpg, grid.x, grid.y,

@@ -80,6 +80,10 @@ struct BPParams {
     const int* seg_idx;
     const int* cta_seg;
     int seg_max;  // block slots per image (>= segments)
+    // 1: the headers are the library's cached set (written by an earlier,
+    // completed call), so the staged BP reads them -- and builds chunk 0's
+    // geometry-only entries -- before waiting on the FP (programmatic launch)
+    int hdr_ready;
     // CBP_BP_PROF (diagnostics, a -DCBP_BP_PROFILE build): per CTA start / end ns, SM,
     // segments, header features
     unsigned long long* prof;
@@ -454,6 +458,9 @@ __device__ __forceinline__ void bp_pair(const BPEntry* row, const float* yrow, i
 // per-tile accumulators: FP64 for S <= 2, FP32 for S >= 4 (shared-memory
 // budget; each term is already a partial over a run of views)
 // one loop for both of a lane's pixel pairs (see cbp_bp_kernel)
+#ifndef CBP_BP_EARLY  // A/B knob: chunk 0's headers and entries before the wait on the FP
+#define CBP_BP_EARLY 1
+#endif
 #ifndef CBP_BP_UNION8  // A/B knob: 0 = two exact-window loops at S = 8 as well
 #define CBP_BP_UNION8 1
 #endif
@@ -753,7 +760,43 @@ __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_
             cp_async16(reinterpret_cast<int4*>(hdr_buf(c)) + tid, reinterpret_cast<const int4*>(hsrc + c * BP_VC) + tid);
     };
 
+    // the S entries of chunk views vc .. vc + nvc - 1, pass `pass`, into tab
+    auto build_entries = [&](const BPHeader* hdr, int vc, int nvc, int pass) {
+#pragma unroll 3
+        for (int e = tid; e < BP_VC * BP_NB; e += BP_THREADS) {
+            const int vi = e / BP_NB, jj = e % BP_NB;
+            if (vi < nvc) {
+                const BPHeader& H = hdr[vi];
+                const int j = H.jlo + pass * BP_NB + jj;
+                CBP_CHECK(j > H.jhi || (j >= 0 && j < g.n_det), "entry j=%d jlo=%d jhi=%d\n", j, H.jlo, H.jhi);
+                if (j <= H.jhi) {
+                    if constexpr (PREC) {
+                        const size_t yo = (size_t)(vg0 + vc + vi) * g.n_det + j;
+                        bp_build_entry_prec(g, P.t, H, j, __ldg(P.sino + (size_t)sg * sino_plane + yo),
+                                            tab[vi][jj]);
+                    } else if constexpr (S == 1) {
+                        const size_t yo = (size_t)(vg0 + vc + vi) * g.n_det + j;
+                        bp_build_entry(g, P.t, H, j, __ldg(P.sino + (size_t)sg * sino_plane + yo), tab[vi][jj]);
+                    } else {
+                        bp_build_entry(g, P.t, H, j, 1.0f, tab[vi][jj]);  // c.w = h^2 / A
+                    }
+                }
+            }
+        }
+    };
+
     for (int i = tid; i < S * BP_TILE * (BP_TILE + 1); i += BP_THREADS) acc_s[i] = 0;
+    // staged BP with cached headers: chunk 0's headers and entries (geometry
+    // only) before the wait on the FP, so they overlap its tail
+    const bool early = STAGE && !SEG && CBP_BP_EARLY && P.hdr_ready && nchunks > 0;
+    if (early) {
+        hdr_copy(0);
+        if (nchunks > 1) hdr_copy(1);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+        build_entries(hdr_buf(0), 0, min(BP_VC, vgn), 0);
+    }
     if constexpr (!SEG) {
         griddep_launch_dependents();  // the reduce may launch into this grid's tail
         griddep_wait();               // the sinogram, headers and pool memory are ready
@@ -761,11 +804,13 @@ __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_
 
     if constexpr (STAGE) {
         if (nchunks > 0) {
-            hdr_copy(0);
-            if (nchunks > 1) hdr_copy(1);
-            cp_async_commit();
-            cp_async_wait_all();
-            __syncthreads();
+            if (!early) {
+                hdr_copy(0);
+                if (nchunks > 1) hdr_copy(1);
+                cp_async_commit();
+                cp_async_wait_all();
+                __syncthreads();
+            }
             bp_y_load<S>(P, vg0, min(BP_VC, vgn), 0, hdr_buf(0), y_buf(0), true);
             cp_async_commit();
         }
@@ -811,28 +856,7 @@ __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_
         prev_npass = npass;
         for (int pass = 0; pass < npass; ++pass) {
             if (STAGE && pass > 0) bp_y_load<S>(P, vg0 + vc, nvc, pass, hdr, ytab, false);
-#pragma unroll 3
-            for (int e = tid; e < BP_VC * BP_NB; e += BP_THREADS) {
-                const int vi = e / BP_NB, jj = e % BP_NB;
-                if (vi < nvc) {
-                    const BPHeader& H = hdr[vi];
-                    const int j = H.jlo + pass * BP_NB + jj;
-                    CBP_CHECK(j > H.jhi || (j >= 0 && j < g.n_det), "entry j=%d jlo=%d jhi=%d\n", j, H.jlo, H.jhi);
-                    if (j <= H.jhi) {
-                        if constexpr (PREC) {
-                            const size_t yo = (size_t)(vg0 + vc + vi) * g.n_det + j;
-                            bp_build_entry_prec(g, P.t, H, j, __ldg(P.sino + (size_t)sg * sino_plane + yo),
-                                                tab[vi][jj]);
-                        } else if constexpr (S == 1) {
-                            const size_t yo = (size_t)(vg0 + vc + vi) * g.n_det + j;
-                            bp_build_entry(g, P.t, H, j, __ldg(P.sino + (size_t)sg * sino_plane + yo),
-                                           tab[vi][jj]);
-                        } else {
-                            bp_build_entry(g, P.t, H, j, 1.0f, tab[vi][jj]);  // c.w = h^2 / A
-                        }
-                    }
-                }
-            }
+            if (!(early && c == 0 && pass == 0)) build_entries(hdr, vc, nvc, pass);
             __syncthreads();
             for (int vi = 0; vi < nvc; ++vi) {
                 const BPHeader& H = hdr[vi];
