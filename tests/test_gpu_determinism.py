@@ -30,6 +30,8 @@ CASES = {
     "uncovered_tiles_batch8": (NARROW_DET, 8),
     "precise": (dict(G1, n_views=90, det_width=0.01), 3),
     "mag": (dict(G1, n_views=88, model=1), 1),
+    # config 2: 4 view groups x 8 frames = 32 planes, the reduce's four-lane path
+    "sym8_config2": (W.geometry("2"), 1),
 }
 
 
