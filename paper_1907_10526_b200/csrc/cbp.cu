@@ -1107,7 +1107,7 @@ int launch_bp_seg(const cbp_geometry_t& g, const cbp::Tables& t, const float* si
     return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
 }
 
-template <int S, bool PREC = false>
+template <int S, bool PREC = false, int W = 0>
 int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
                 int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream,
                 int symmode = 0, int images = 1)
@@ -1126,14 +1126,14 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int SG = sym ? images : (batch + S - 1) / S;
-    const size_t smem = cbp::bp_smem_bytes(S, PREC);
+    const size_t smem = cbp::bp_smem_bytes(S, PREC, W);
     static std::once_flag attr[64];
     static int per_sm[64];
     std::call_once(attr[dev & 63], [smem, dev] {
-        cudaFuncSetAttribute(cbp::cbp_bp_kernel<S, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(cbp::cbp_bp_kernel<S, PREC, false, false, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         int k = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_bp_kernel<S, PREC>, cbp::BP_THREADS,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_bp_kernel<S, PREC, false, false, W>, cbp::BP_THREADS,
                                                           smem) != cudaSuccess || k < 1)
             k = 1;
         per_sm[dev & 63] = k;
@@ -1193,7 +1193,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     P.seg_idx = P.cta_seg = nullptr;
     P.seg_max = 0;
     P.prof = bp_prof_begin((size_t)grid.x * grid.y * grid.z);
-    launch_pdl(cbp::cbp_bp_kernel<S, PREC>, grid, dim3(cbp::BP_THREADS), smem, stream, P);
+    launch_pdl(cbp::cbp_bp_kernel<S, PREC, false, false, W>, grid, dim3(cbp::BP_THREADS), smem, stream, P);
     ++g_launches;
     bp_prof_end(P.prof, (size_t)grid.x * grid.y * grid.z, stream);
 #ifdef CBP_DEBUG_CHECKS
@@ -1215,6 +1215,21 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
 }
 
+// the wide chunk shape of the 8-frame BP (cbp::BPShape<1>: 4 views x 128
+// bins) when a tile's projection is wide: its mean span in bins, 32 h m (4 /
+// pi) / pitch with the magnification m = D_ps / D_po at the centre (the mean
+// of |cos| + |sin| over directions is 4 / pi), above 68 -- config 2-5: 54
+// (default shape), the paper's timing shapes: 81 (wide; BP 0.194 -> 0.163 ms
+// at p512, 0.716 -> 0.567 at p1024; config 2 with the wide shape 0.187 ->
+// 0.203).  CBP_BP_WIDE=0 / 1 forces it (read per call).
+bool bp_wide(const cbp_geometry_t& g)
+{
+    const char* e = getenv("CBP_BP_WIDE");
+    if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
+    const double m = g.kind == CBP_PARALLEL ? 1.0 : g.sdd / g.sid;
+    return cbp::BP_TILE * g.pixel * m * (4.0 / M_PI) / g.det_pitch > 68.0;
+}
+
 int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
               int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream)
 {
@@ -1225,9 +1240,12 @@ int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, 
     static const bool force_s1 = getenv("CBP_BP_FORCE_S1") != nullptr;
     if (force_s1) return launch_bp_s<1>(g, t, sino, img, batch, v0, nv, accumulate, stream);
     if (use_sym8(g, batch, v0, nv))
-        return launch_bp_s<8>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8);
+        return bp_wide(g) ? launch_bp_s<8, false, 1>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8)
+                          : launch_bp_s<8>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8);
     if (batch > 1 && use_sym8(g, 1, v0, nv))  // a batch: the 8 frames of each image
-        return launch_bp_s<8>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8, batch);
+        return bp_wide(g) ? launch_bp_s<8, false, 1>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream,
+                                                     8, batch)
+                          : launch_bp_s<8>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8, batch);
     if (use_sym4(g, batch, v0, nv))
         return launch_bp_s<4>(g, t, sino, img, batch, 0, g.n_views / 4, accumulate, stream, 4);
     if (batch >= 4) return launch_bp_s<4>(g, t, sino, img, batch, v0, nv, accumulate, stream);
@@ -1639,7 +1657,8 @@ int cbp_back_dihedral(const cbp_geometry_t* g, const float* sino, float* image, 
     if (g->model == CBP_MODEL_MAG || precise(*g))
         return block_dihedral(*g, t, image, const_cast<float*>(sino), base_begin, base_count, accumulate, stream,
                               false);
-    return launch_bp_s<8>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 8);
+    return bp_wide(*g) ? launch_bp_s<8, false, 1>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 8)
+                       : launch_bp_s<8>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 8);
 }
 
 // ---- row f1: SART / CGLS building blocks ---------------------------------

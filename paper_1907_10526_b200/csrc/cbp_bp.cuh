@@ -104,8 +104,23 @@ __device__ __forceinline__ unsigned smid()
 
 constexpr int BP_TILE = 32;       // pixels per tile side
 constexpr int BP_THREADS = 256;   // 8 warps x 2 pairs x 2 pixels x 32 lanes = 32 x 32
-constexpr int BP_VC = 8;          // views per chunk
-constexpr int BP_NB = 80;         // bins per view per pass (a 32-pixel tile spans <= ~64)
+#ifndef CBP_BP_VC  // (compile-time knobs for A/B builds)
+#define CBP_BP_VC 8
+#endif
+#ifndef CBP_BP_NB
+#define CBP_BP_NB 80
+#endif
+constexpr int BP_VC = CBP_BP_VC;  // views per chunk
+constexpr int BP_NB = CBP_BP_NB;  // bins per view per pass (a 32-pixel tile spans <= ~64 at config 2)
+// the chunk shape of the staged BP: W = 0 the default (8 views x 80 bins);
+// W = 1 for wide projected tiles (4 views x 128 bins: the paper's timing
+// shapes, where a tile spans 64-90+ bins and 80-bin passes split views in
+// two) -- the same shared memory budget
+template <int W>
+struct BPShape {
+    static constexpr int VC = W ? 4 : BP_VC;
+    static constexpr int NB = W ? 128 : BP_NB;
+};
 #ifndef CBP_BP_BUCKETS  // (compile-time knobs for A/B builds)
 #define CBP_BP_BUCKETS 32
 #endif
@@ -386,7 +401,7 @@ __device__ __forceinline__ void bp_pair_prec(const BPEntryP* row, int jl, int jh
                                              float2& acc)
 {
     if (jh < jl) return;
-    CBP_CHECK(jl >= base && jh - base < BP_NB, "bp_pair_prec jl=%d jh=%d base=%d\n", jl, jh, base);
+    CBP_CHECK(jl >= base && jh - base < 128, "bp_pair_prec jl=%d jh=%d base=%d\n", jl, jh, base);
     const BPEntryP* e = row + (jl - base);
     for (int k = jl; k <= jh; ++k, ++e) {
         const double xa = e->xa, sc = e->sc, sr = e->sr, A = e->A;
@@ -424,7 +439,7 @@ __device__ __forceinline__ void bp_pair(const BPEntry* row, const float* yrow, i
                                         int base, float dc, float dr, float2 (&acc)[S])
 {
     if (jh < jl) return;
-    CBP_CHECK(jl >= base && jh - base < BP_NB, "bp_pair jl=%d jh=%d base=%d\n", jl, jh, base);
+    CBP_CHECK(jl >= base && jh - base < 128, "bp_pair jl=%d jh=%d base=%d\n", jl, jh, base);
     const int cnt = jh - jl + 1;
     const BPEntry* e = row + (jl - base);
     const float* ys = yrow + (jl - base) * S;
@@ -475,7 +490,7 @@ __device__ __forceinline__ void bp_pair2(const BPEntry* row, const float* yrow, 
                                          float2 (&a1)[S])
 {
     if (jh < jl) return;
-    CBP_CHECK(jl >= base && jh - base < BP_NB, "bp_pair2 jl=%d jh=%d base=%d\n", jl, jh, base);
+    CBP_CHECK(jl >= base && jh - base < 128, "bp_pair2 jl=%d jh=%d base=%d\n", jl, jh, base);
     const int cnt = jh - jl + 1;
     const BPEntry* e = row + (jl - base);
     const float* ys = yrow + (jl - base) * S;
@@ -580,10 +595,11 @@ __device__ __forceinline__ int bp_orbit_members(int T, int2 rep, int (&mem)[8])
 
 // dynamic shared memory of the BP kernel for S slices: entries, headers,
 // (S > 1) two y buffers [2][VC][NB][S], tile accumulators [S][32][33]
-__host__ __device__ constexpr size_t bp_smem_bytes(int S, bool prec = false)
+__host__ __device__ constexpr size_t bp_smem_bytes(int S, bool prec = false, int W = 0)
 {
-    return (prec ? sizeof(BPEntryP) : sizeof(BPEntry)) * BP_VC * BP_NB + sizeof(BPHeader) * BP_VC * bp_hdr_bufs(S) +
-           (S > 1 ? 2 * sizeof(float) * BP_VC * BP_NB * S : 0) +
+    return (prec ? sizeof(BPEntryP) : sizeof(BPEntry)) * (W ? BPShape<1>::VC * BPShape<1>::NB : BP_VC * BP_NB) +
+           sizeof(BPHeader) * (W ? BPShape<1>::VC : BP_VC) * bp_hdr_bufs(S) +
+           (S > 1 ? 2 * sizeof(float) * (W ? BPShape<1>::VC * BPShape<1>::NB : BP_VC * BP_NB) * S : 0) +
            (S >= 4 ? sizeof(float) : sizeof(double)) * S * BP_TILE * (BP_TILE + 1);
 }
 
@@ -605,10 +621,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // ybuf[VC][NB][S] -- asynchronously (cp.async, overlapping the previous
 // chunk's compute) or with plain loads (later passes of a wide bin range).
 // Four .. sixteen threads per (view, slice) walk its bins.
-template <int S>
+template <int S, int W = 0>
 __device__ __forceinline__ void bp_y_load(const BPParams& P, int vl0, int nvc, int pass,
                                           const BPHeader* H, float* ybuf, bool async)
 {
+    constexpr int BP_VC = BPShape<W>::VC, BP_NB = BPShape<W>::NB;
     const GeomDev& g = P.g;
     constexpr int TPC = BP_THREADS / (BP_VC * S);  // threads per (view, slice)
     static_assert(TPC >= 1 && BP_THREADS % (BP_VC * S) == 0, "BP_VC * S must divide the CTA");
@@ -726,10 +743,11 @@ __device__ void bp_orbit_epilogue(const BPParams& P, float* acc_s, const int (&m
 
 // One CTA's work on one tile over views [vg0, vg0 + vgn) of the launch (view
 // group grp, slice group sg; seg: the segment of a persistent launch).
-template <int S, bool PREC, bool ORB, bool SEG>
+template <int S, bool PREC, bool ORB, bool SEG, int W = 0>
 __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_y, int tiles_x, int vg0, int vgn,
                                         int grp, int sg, int seg, const int (&omem)[8], int osize)
 {
+    constexpr int BP_VC = BPShape<W>::VC, BP_NB = BPShape<W>::NB;  // the chunk shape
     static_assert(!PREC || S == 1, "the precise mode runs one slice per weight");
     static_assert(!ORB || (S == 8 && !PREC), "orbit clusters carry the 8 dihedral frames");
     using Ent = typename std::conditional<PREC, BPEntryP, BPEntry>::type;
@@ -740,7 +758,7 @@ __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_
     BPHeader* hdr_all = reinterpret_cast<BPHeader*>(smem + sizeof(Ent) * BP_VC * BP_NB);  // [HB][VC]
     float* ytab_all = reinterpret_cast<float*>(hdr_all + HB * BP_VC);  // [2][VC][NB][S] (S > 1)
     bp_acc_t<S>* acc_s = reinterpret_cast<bp_acc_t<S>*>(
-        smem + bp_smem_bytes(S, PREC) - sizeof(bp_acc_t<S>) * S * BP_TILE * (BP_TILE + 1));
+        smem + bp_smem_bytes(S, PREC, W) - sizeof(bp_acc_t<S>) * S * BP_TILE * (BP_TILE + 1));
 
     const GeomDev& g = P.g;
     const int tid = threadIdx.x;
@@ -811,7 +829,7 @@ __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_
                 cp_async_wait_all();
                 __syncthreads();
             }
-            bp_y_load<S>(P, vg0, min(BP_VC, vgn), 0, hdr_buf(0), y_buf(0), true);
+            bp_y_load<S, W>(P, vg0, min(BP_VC, vgn), 0, hdr_buf(0), y_buf(0), true);
             cp_async_commit();
         }
     }
@@ -835,7 +853,7 @@ __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_
             __syncthreads();
             if (c + 2 < nchunks) hdr_copy(c + 2);
             if (c + 1 < nchunks)
-                bp_y_load<S>(P, vg0 + vc + BP_VC, min(BP_VC, vgn - vc - BP_VC), 0, hdr_buf(c + 1), y_buf(c + 1),
+                bp_y_load<S, W>(P, vg0 + vc + BP_VC, min(BP_VC, vgn - vc - BP_VC), 0, hdr_buf(c + 1), y_buf(c + 1),
                              true);
             cp_async_commit();
         } else {
@@ -852,10 +870,12 @@ __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_
             __syncthreads();
         }
         int npass = 0;
-        for (int vi = 0; vi < nvc; ++vi) npass = max(npass, (int)hdr[vi].npass_f);
+        for (int vi = 0; vi < nvc; ++vi)  // passes of BP_NB bins (the header's npass_f is for the default shape)
+            npass = max(npass, W == 0 ? (int)hdr[vi].npass_f
+                                      : (hdr[vi].jhi >= hdr[vi].jlo ? (hdr[vi].jhi - hdr[vi].jlo) / BP_NB + 1 : 0));
         prev_npass = npass;
         for (int pass = 0; pass < npass; ++pass) {
-            if (STAGE && pass > 0) bp_y_load<S>(P, vg0 + vc, nvc, pass, hdr, ytab, false);
+            if (STAGE && pass > 0) bp_y_load<S, W>(P, vg0 + vc, nvc, pass, hdr, ytab, false);
             if (!(early && c == 0 && pass == 0)) build_entries(hdr, vc, nvc, pass);
             __syncthreads();
             for (int vi = 0; vi < nvc; ++vi) {
@@ -1023,7 +1043,7 @@ __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_
     }
 }
 
-template <int S, bool PREC = false, bool ORB = false, bool SEG = false>
+template <int S, bool PREC = false, bool ORB = false, bool SEG = false, int W = 0>
 __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp_bp_kernel(const BPParams P)
 {
     int omem[8], osize = 1;
@@ -1069,8 +1089,8 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
             const int tile = i0 / P.view_count, v0 = i0 - tile * P.view_count;
             if (s > s0) __syncthreads();  // the previous segment's epilogue is done with acc_s
             prof_feat(tile, v0, len);
-            bp_body<S, PREC, ORB, SEG>(P, tile % tiles_x, tile / tiles_x, tiles_x, v0, len, 0, blockIdx.z, s, omem,
-                                       osize);
+            bp_body<S, PREC, ORB, SEG, W>(P, tile % tiles_x, tile / tiles_x, tiles_x, v0, len, 0, blockIdx.z, s,
+                                          omem, osize);
         }
         prof_end(s1 - s0);
         return;
@@ -1092,7 +1112,7 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
         vgn = max(0, min(per, vgn - part * per));
     }
     if (!ORB) prof_feat(tile_y * tiles_x + tile_x, vg0, vgn);
-    bp_body<S, PREC, ORB, SEG>(P, tile_x, tile_y, tiles_x, vg0, vgn, grp, sg, 0, omem, osize);
+    bp_body<S, PREC, ORB, SEG, W>(P, tile_x, tile_y, tiles_x, vg0, vgn, grp, sg, 0, omem, osize);
     prof_end(1);
 }
 

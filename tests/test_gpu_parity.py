@@ -459,3 +459,28 @@ def test_rot_rows_fp_matches_oracle(torch_cuda, monkeypatch):
     assert out.returncode == 0, out.stderr[-2000:]
     rl2, mr = (float(x) for x in out.stdout.split())
     assert rl2 <= REL_L2 and mr <= MAX_REL, (rl2, mr)
+
+
+@pytest.mark.parametrize("wide", ["0", "1"])
+def test_bp_chunk_shapes(torch_cuda, monkeypatch, wide):
+    """The 8-frame BP's two chunk shapes (cbp::BPShape: 8 views x 80 bins, or
+    4 views x 128 bins chosen for wide projected tiles such as the paper's
+    timing shapes), each forced on a narrow and a wide geometry (CBP_BP_WIDE):
+    one image, a batch of images (per-image frames), and dihedral shards
+    summing to the full BP -- all against the oracle."""
+    torch = torch_cuda
+    from paper_1907_10526_b200 import sharded
+    monkeypatch.setenv("CBP_BP_WIDE", wide)
+    for g in (dict(W.geometry("1"), n_views=88), dict(W.PAPER_TIMING[64])):
+        y = W.random_sino(g["n_views"], g["n_det"], 121)
+        want = O.back(g, y)
+        _assert_parity(_bp(torch, g, y), want, f"BP shape {wide} n_views {g['n_views']}")
+        ys = W.random_sino(g["n_views"], g["n_det"], 122, batch=2)
+        _assert_parity(_bp(torch, g, ys), np.stack([O.back(g, ys[b]) for b in range(2)]),
+                       f"BP shape {wide} batch")
+        yt = torch.from_numpy(y).cuda()
+        total = torch.zeros((g["n"], g["n"]), device="cuda")
+        for r in range(3):
+            sh = sharded.make_shard(g["n_views"], r, 3, dihedral=True)
+            total += cbp.back_dihedral(g, yt, sh.begin, sh.count)
+        _assert_parity(total.cpu().numpy(), want, f"BP shape {wide} dihedral shards")
