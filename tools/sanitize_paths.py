@@ -101,6 +101,13 @@ cbp.back_dihedral(dict(g1, n_views=88), cbp.forward(dict(g1, n_views=88), img), 
 os.environ.pop("CBP_BP_SEG")
 pair(dict(n=70, pixel=0.9, n_views=92, n_det=150, det_pitch=1.1, det_width=1.0, sid=200.0, sdd=400.0))
 pair(dict(n=70, pixel=0.9, n_views=92, n_det=150, det_pitch=1.1, det_width=1.0, sid=200.0, sdd=400.0, model=1))
+# v56: the 8-frame BP's wide chunk shape (the paper's timing shape; forced on a narrow geometry, a batch)
+pair(dict(W.PAPER_TIMING[64]))
+os.environ["CBP_BP_WIDE"] = "1"
+pair(dict(g1, n_views=88))
+pair(dict(g1, n_views=88), batch=3)
+pair(dict(rag, n_views=32))
+os.environ.pop("CBP_BP_WIDE")
 # reference projector
 gs = dict(g1, n=16, n_views=6, n_det=40)
 yr = cbp.ref_forward(gs, torch.from_numpy(W.random_image(16, 3)).cuda())
