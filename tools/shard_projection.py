@@ -6,7 +6,7 @@ on their own GPUs), plus the BP all-reduce, which this one-GPU box cannot
 measure (reported separately as not measured).  With CBP_PROJ_GRAPH=1 each
 rank's pair is captured once in a CUDA graph and replayed (no host launch
 overhead in the timed loop; the library's launches are graph nodes).  Usage:
-  python tools/shard_projection.py [config] [worlds...]"""
+  [PROJ_DIHEDRAL=0] python tools/shard_projection.py [config] [worlds...]   (0: orbit shards)"""
 import json
 import os
 import sys
@@ -55,14 +55,21 @@ def main():
         cbp.back(g, y, image=out)
     torch.cuda.synchronize()
     base = None
+    dihedral = os.environ.get("PROJ_DIHEDRAL", "1") != "0"  # 0: orbit shards (4 rotations of a base block)
     for world in worlds:
         per_rank = []
         for r in range(world):
-            sh = sharded.make_shard(g["n_views"], r, world, dihedral=True)
+            sh = sharded.make_shard(g["n_views"], r, world, dihedral=dihedral)
             if sh.mode == "block":  # world 1: the library's own full-scan path
                 def pair():
                     cbp.forward(g, img, sino=y)
                     cbp.back(g, y, image=out)
+            elif sh.mode == "orbit":
+                yo = torch.zeros((4, sh.count, g["n_det"]), device="cuda")
+
+                def pair(sh=sh, yo=yo):
+                    cbp.forward_orbit(g, img, sh.begin, sh.count, sino=yo)
+                    cbp.back_orbit(g, yo, sh.begin, image=out)
             else:
                 def pair(sh=sh):
                     cbp.forward_dihedral(g, img, sh.begin, sh.count, sino=y)
@@ -71,7 +78,7 @@ def main():
         slowest = max(p["ms"] for p in per_rank)
         if world == 1:
             base = slowest
-        line = {"config": cfg, "world": world, "mode": sharded.make_shard(g["n_views"], 0, world, dihedral=True).mode,
+        line = {"config": cfg, "world": world, "mode": sharded.make_shard(g["n_views"], 0, world, dihedral=dihedral).mode,
                 "slowest_rank_ms": slowest, "mean_rank_ms": sum(p["ms"] for p in per_rank) / world,
                 "max_views": max(p["views"] for p in per_rank),
                 "projected_pairs_per_s_compute_only": 1e3 / slowest,
