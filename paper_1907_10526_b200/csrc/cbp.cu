@@ -981,16 +981,17 @@ int launch_bp_orbit(const cbp_geometry_t& g, const cbp::Tables& t, const float* 
 // appends "launch <ctas>" and one line per CTA to the file
 unsigned long long* bp_prof_begin(size_t ctas)
 {
-#ifndef CBP_BP_PROFILE
-    (void)ctas;
-    return nullptr;  // the timeline is compiled in only with -DCBP_BP_PROFILE (tools/bp_cta_prof.py)
-#endif
+#ifdef CBP_BP_PROFILE
     static const char* path = getenv("CBP_BP_PROF");
     if (!path) return nullptr;
     unsigned long long* d = nullptr;
     if (cudaMalloc(&d, 64 * ctas) != cudaSuccess) return nullptr;
     cudaMemset(d, 0, 64 * ctas);
     return d;
+#else
+    (void)ctas;
+    return nullptr;  // the timeline is compiled in only with -DCBP_BP_PROFILE (tools/bp_cta_prof.py)
+#endif
 }
 void bp_prof_end(unsigned long long* d, size_t ctas, cudaStream_t stream)
 {
