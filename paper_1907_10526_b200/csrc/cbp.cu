@@ -273,6 +273,22 @@ int scratch_alloc(void** p, size_t bytes, cudaStream_t stream)
 // per-line candidate count K = floor(2 sigma_q) + 1 any ray can have, with
 // sigma_q = (A + C + tau') / (2 A) <= 1 + tau'_max / (sqrt(2) h) and
 // tau'_max <= (tau / D_ps) (D_po + n h / sqrt(2))
+// tau' > 0 at every pixel of the padded grid for every ray, so the FP walk
+// needs no clamp before 1 / tau' (cbp_fp_kernel's CLAMP = false): tau' =
+// g_j (k - p).v_j with g_j > 0 and (k - p).v_j >= D_po D_ps / L_j - R_pad on
+// the flat detector (D_po cos(gamma_j) - R_pad on the arc; parallel beam:
+// tau' = tau), R_pad = sqrt(2) ((n - 1) / 2 + P) h the padded grid's corner
+bool fp_tau_positive(const cbp_geometry_t& g, int P)
+{
+    if (g.kind == CBP_PARALLEL) return true;
+    const double rpad = std::sqrt(2.0) * (0.5 * (g.n - 1) + P) * g.pixel;
+    const double smax = 0.5 * (g.n_det - 1) * g.det_pitch;
+    const double dmin = g.kind == CBP_FAN_ARC ? g.sid * std::cos(std::min(smax / g.sdd, 1.5))
+                                              : g.sid * g.sdd / std::sqrt(g.sdd * g.sdd + smax * smax);
+    static const bool always = getenv("CBP_FP_CLAMP") != nullptr;  // test knob: the clamped walk everywhere
+    return !always && dmin - rpad > 1e-6 * g.sid;
+}
+
 int fp_pad_width(const cbp_geometry_t& g)
 {
     const double gmax = g.kind == CBP_FAN_ARC ? 2.0 * std::tan(0.5 * g.det_width / g.sdd) : g.det_width / g.sdd;
@@ -317,7 +333,7 @@ bool precise(const cbp_geometry_t& g)
 // ~8 waves of resident CTAs (config 2: 1.6 waves -> parts 4, FP -17 %;
 // config 3: 6.5 waves -> parts 2; config 4 / 5: enough waves)
 template <int S, bool PREC = false>
-int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stream)
+int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stream, bool noclamp = false)
 {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -351,6 +367,20 @@ int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stre
     const int64_t tiles = ctas(parts) / ((int64_t)views * groups);
     if (tiles > 65535) return CBP_EINVAL;
     const dim3 grid(views, (unsigned)tiles, groups);
+    if constexpr (S == 4 && !PREC) {  // tau' > 0 over the padded grid: the walk without the clamp
+        if (noclamp) {
+            if (parts == 8)
+                launch_pdl(cbp::cbp_fp_kernel<S, 8, PREC, false>, grid, dim3(cbp::fp_threads(8)), 0, stream, Pm);
+            else if (parts == 4)
+                launch_pdl(cbp::cbp_fp_kernel<S, 4, PREC, false>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
+            else if (parts == 2)
+                launch_pdl(cbp::cbp_fp_kernel<S, 2, PREC, false>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
+            else
+                launch_pdl(cbp::cbp_fp_kernel<S, 1, PREC, false>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
+            ++g_launches;
+            return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+        }
+    }
     if (parts == 8)
         launch_pdl(cbp::cbp_fp_kernel<S, 8, PREC>, grid, dim3(cbp::fp_threads(8)), 0, stream, Pm);
     else if (parts == 4)
@@ -396,7 +426,7 @@ int launch_fp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* img,
     Pm.sym_stride = 0;
     Pm.sym_mode = 0;
     Pm.rot_rows = 0;
-    rc = launch_fp_kernel<S, PREC>(Pm, nv, G, stream);
+    rc = launch_fp_kernel<S, PREC>(Pm, nv, G, stream, fp_tau_positive(g, P));
     cudaFreeAsync(pad, stream);
     return rc;
 }
@@ -460,7 +490,7 @@ int launch_fp_sym4(const cbp_geometry_t& g, const cbp::Tables& t, const float* i
         Pm.view_begin2 = begin2;
         Pm.sino2 = sino + (size_t)begin2 * g.n_det;
     }
-    rc = launch_fp_kernel<4>(Pm, base_count + (count2 > 0 ? count2 : 0), 1, stream);
+    rc = launch_fp_kernel<4>(Pm, base_count + (count2 > 0 ? count2 : 0), 1, stream, fp_tau_positive(g, P));
     cudaFreeAsync(pad, stream);
     return rc;
 }

@@ -271,7 +271,10 @@ struct FPRay {
 // (u11 = z11/C + 1, u12 = u11 - tau'/C, u21 = u11 - A/C, u22 = u12 - A/C),
 // and the trapezoid bound r = A + tau' - z11 is affine in k too.
 // `out` holds the thread's S FP64 totals at stride NT (shared memory)
-template <int K, int MAB, int S, bool PRE, int NT>
+// CLAMP: keep 1 / tau' finite for candidates in the zero border behind a
+// close source (tau' <= 0 there); the host launches the CLAMP = false kernel
+// when tau' > 0 at every padded pixel of every ray (fp_tau_positive)
+template <int K, int MAB, int S, bool PRE, int NT, bool CLAMP = true>
 __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, int np, int P,
                                         double* out)
 {
@@ -363,7 +366,7 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
                 // tau' > 0 at every pixel a ray's support reaches; candidates in the zero
                 // border behind a close source can have tau' <= 0: keep 1/tau' finite
                 // (their image values are 0)
-                const float2 iB = rcp2(make_float2(fmaxf(B.x, 1e-30f), fmaxf(B.y, 1e-30f)));
+                const float2 iB = CLAMP ? rcp2(make_float2(fmaxf(B.x, 1e-30f), fmaxf(B.y, 1e-30f))) : rcp2(B);
                 if constexpr (S == 1) {
                     const float2 cw = __fmul2_rn(make_float2(ca[0], cb[0]), iB);
                     acc[0] = __ffma2_rn(cw, num, acc[0]);
@@ -390,13 +393,13 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
     }
 }
 
-template <int K, int S, bool PRE, int NT>
+template <int K, int S, bool PRE, int NT, bool CLAMP = true>
 __device__ __forceinline__ void fp_walk_k(const FPRay& R, int mab, int i0, int i1, int n, int np,
                                           int P, double* out)
 {
-    if (mab == 1) fp_walk<K, 1, S, PRE, NT>(R, i0, i1, n, np, P, out);
-    else if (mab == 2) fp_walk<K, 2, S, PRE, NT>(R, i0, i1, n, np, P, out);
-    else fp_walk<K, 0, S, PRE, NT>(R, i0, i1, n, np, P, out);
+    if (mab == 1) fp_walk<K, 1, S, PRE, NT, CLAMP>(R, i0, i1, n, np, P, out);
+    else if (mab == 2) fp_walk<K, 2, S, PRE, NT, CLAMP>(R, i0, i1, n, np, P, out);
+    else fp_walk<K, 0, S, PRE, NT, CLAMP>(R, i0, i1, n, np, P, out);
 }
 
 // generic K (wide bins relative to pixels): same arithmetic, runtime trip count
@@ -476,7 +479,7 @@ __device__ void fp_walk_prec(const FPRay& R, const FPRayD& D, int K, int i0, int
 // shared memory (deterministic).  A CTA covers 128 / PARTS bins.  PARTS > 1
 // when the grid would otherwise be short of ~16 waves: the ragged last wave
 // of a 1.6-wave grid cost ~25 %.
-template <int S, int PARTS, bool PREC = false>
+template <int S, int PARTS, bool PREC = false, bool CLAMP = true>
 __global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? CBP_FP_P8_MINB : (S == 1 ? 7 : (S == 4 ? CBP_FP_S4_MINB : 4)))
     cbp_fp_kernel(const FPParams P)
 {
@@ -642,12 +645,12 @@ __global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? CBP_FP_P8_MINB 
             fp_walk_prec<NT>(R, Dr, Kw, i0, i1, n, P.np, P.P, acc);
         } else {
           switch (Kw) {
-            case 1: fp_walk_k<1, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
-            case 2: fp_walk_k<2, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
-            case 3: fp_walk_k<3, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
-            case 4: fp_walk_k<4, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
-            case 5: fp_walk_k<5, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
-            case 6: fp_walk_k<6, S, (S <= 2 || (S == 4 && PARTS > 1)), NT>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 1: fp_walk_k<1, S, (S <= 2 || (S == 4 && PARTS > 1)), NT, CLAMP>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 2: fp_walk_k<2, S, (S <= 2 || (S == 4 && PARTS > 1)), NT, CLAMP>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 3: fp_walk_k<3, S, (S <= 2 || (S == 4 && PARTS > 1)), NT, CLAMP>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 4: fp_walk_k<4, S, (S <= 2 || (S == 4 && PARTS > 1)), NT, CLAMP>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 5: fp_walk_k<5, S, (S <= 2 || (S == 4 && PARTS > 1)), NT, CLAMP>(R, mab, i0, i1, n, P.np, P.P, acc); break;
+            case 6: fp_walk_k<6, S, (S <= 2 || (S == 4 && PARTS > 1)), NT, CLAMP>(R, mab, i0, i1, n, P.np, P.P, acc); break;
             default: fp_walk_generic<S, NT>(R, Kw, i0, i1, n, P.np, P.P, acc); break;
           }
         }
