@@ -367,7 +367,7 @@ int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stre
     const int64_t tiles = ctas(parts) / ((int64_t)views * groups);
     if (tiles > 65535) return CBP_EINVAL;
     const dim3 grid(views, (unsigned)tiles, groups);
-    if constexpr (S == 4 && !PREC) {  // tau' > 0 over the padded grid: the walk without the clamp
+    if constexpr ((S == 4 || S == 1) && !PREC) {  // tau' > 0 over the padded grid: the walk without the clamp
         if (noclamp) {
             if (parts == 8)
                 launch_pdl(cbp::cbp_fp_kernel<S, 8, PREC, false>, grid, dim3(cbp::fp_threads(8)), 0, stream, Pm);
