@@ -484,3 +484,33 @@ def test_bp_chunk_shapes(torch_cuda, monkeypatch, wide):
             sh = sharded.make_shard(g["n_views"], r, 3, dihedral=True)
             total += cbp.back_dihedral(g, yt, sh.begin, sh.count)
         _assert_parity(total.cpu().numpy(), want, f"BP shape {wide} dihedral shards")
+
+
+CLAMPED_FP = r'''
+import os, sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_1907_10526_b200 as cbp, workloads as W
+g = %r
+img = torch.from_numpy(W.random_image(g["n"], 77)).cuda()
+np.save(%r, cbp.forward(g, img).cpu().numpy())
+'''
+
+
+@pytest.mark.parametrize("cfg", ["1", "2", "2v721"])
+def test_fp_without_clamp_is_exact(torch_cuda, tmp_path, cfg):
+    """The FP walks without its tau' clamp where the host proves tau' > 0 over
+    the padded grid (fp_tau_positive); there the clamp (max(tau', 1e-30)) never
+    acts, so the two kernels must agree bit for bit.  The clamped one is forced
+    in a subprocess (CBP_FP_CLAMP is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    torch = torch_cuda
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    g = W.geometry(cfg)
+    out = str(tmp_path / "clamped.npy")
+    res = subprocess.run([sys.executable, "-c", CLAMPED_FP % (root, g, out)], env=dict(os.environ, CBP_FP_CLAMP="1"),
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    img = torch.from_numpy(W.random_image(g["n"], 77)).cuda()
+    assert np.array_equal(cbp.forward(g, img).cpu().numpy(), np.load(out))
