@@ -367,16 +367,28 @@ int launch_fp_kernel(cbp::FPParams& Pm, int views, int groups, cudaStream_t stre
     const int64_t tiles = ctas(parts) / ((int64_t)views * groups);
     if (tiles > 65535) return CBP_EINVAL;
     const dim3 grid(views, (unsigned)tiles, groups);
-    if constexpr ((S == 4 || S == 1) && !PREC) {  // tau' > 0 over the padded grid: the walk without the clamp
-        if (noclamp) {
+    if constexpr ((S == 4 || S == 1) && !PREC) {
+        if (Pm.g.parallel) {  // tau' = tau: constant over every walk (CLAMP = 2)
             if (parts == 8)
-                launch_pdl(cbp::cbp_fp_kernel<S, 8, PREC, false>, grid, dim3(cbp::fp_threads(8)), 0, stream, Pm);
+                launch_pdl(cbp::cbp_fp_kernel<S, 8, PREC, 2>, grid, dim3(cbp::fp_threads(8)), 0, stream, Pm);
             else if (parts == 4)
-                launch_pdl(cbp::cbp_fp_kernel<S, 4, PREC, false>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
+                launch_pdl(cbp::cbp_fp_kernel<S, 4, PREC, 2>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
             else if (parts == 2)
-                launch_pdl(cbp::cbp_fp_kernel<S, 2, PREC, false>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
+                launch_pdl(cbp::cbp_fp_kernel<S, 2, PREC, 2>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
             else
-                launch_pdl(cbp::cbp_fp_kernel<S, 1, PREC, false>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
+                launch_pdl(cbp::cbp_fp_kernel<S, 1, PREC, 2>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
+            ++g_launches;
+            return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
+        }
+        if (noclamp) {  // tau' > 0 over the padded grid: the walk without the clamp
+            if (parts == 8)
+                launch_pdl(cbp::cbp_fp_kernel<S, 8, PREC, 0>, grid, dim3(cbp::fp_threads(8)), 0, stream, Pm);
+            else if (parts == 4)
+                launch_pdl(cbp::cbp_fp_kernel<S, 4, PREC, 0>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
+            else if (parts == 2)
+                launch_pdl(cbp::cbp_fp_kernel<S, 2, PREC, 0>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
+            else
+                launch_pdl(cbp::cbp_fp_kernel<S, 1, PREC, 0>, grid, dim3(cbp::FP_BLOCK), 0, stream, Pm);
             ++g_launches;
             return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
         }

@@ -271,10 +271,11 @@ struct FPRay {
 // (u11 = z11/C + 1, u12 = u11 - tau'/C, u21 = u11 - A/C, u22 = u12 - A/C),
 // and the trapezoid bound r = A + tau' - z11 is affine in k too.
 // `out` holds the thread's S FP64 totals at stride NT (shared memory)
-// CLAMP: keep 1 / tau' finite for candidates in the zero border behind a
-// close source (tau' <= 0 there); the host launches the CLAMP = false kernel
-// when tau' > 0 at every padded pixel of every ray (fp_tau_positive)
-template <int K, int MAB, int S, bool PRE, int NT, bool CLAMP = true>
+// CLAMP = 1: keep 1 / tau' finite for candidates in the zero border behind a
+// close source (tau' <= 0 there); 0: the host proved tau' > 0 at every padded
+// pixel of every ray (fp_tau_positive); 2: parallel beam, tau' = tau for every
+// candidate (Eq. 9-10), so its update and reciprocal leave the loops
+template <int K, int MAB, int S, bool PRE, int NT, int CLAMP = 1>
 __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, int np, int P,
                                         double* out)
 {
@@ -284,6 +285,7 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
     const float* row = R.base + ((size_t)(i0 + P) * np + P) * S;  // line i0, column 0
     float2 fi = make_float2((float)i0, (float)i0 + 1.0f);
     const float2 AC = make_float2(-R.A * R.invC, -R.A * R.invC);
+    const float iBpar = CLAMP == 2 ? rcp_approx(R.Be0) : 0.0f;  // parallel beam: 1 / tau, once per ray
     const float dzC = R.dz * R.invC, dzC2 = dzC - R.tq * R.invC, dr = R.tq - R.dz;
     for (int i = i0; i <= i1;) {
         // S == 1: acc[0] = (line a, line b).  S >= 2: acc[q2] = slices (2 q2, 2 q2 + 1) of
@@ -309,8 +311,9 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
             const float* pb = row + ((size_t)np + qb) * S;
             row += 2 * (size_t)np * S;
             const float2 f = make_float2((float)fla, (float)flb);
-            float2 B0 = __ffma2_rn(f, make_float2(R.btq, R.btq),
-                                   __ffma2_rn(fi, make_float2(R.dB, R.dB), make_float2(R.Be0, R.Be0)));
+            float2 B0 = CLAMP == 2 ? make_float2(R.Be0, R.Be0)  // parallel beam: tau' = tau
+                                   : __ffma2_rn(f, make_float2(R.btq, R.btq),
+                                                __ffma2_rn(fi, make_float2(R.dB, R.dB), make_float2(R.Be0, R.Be0)));
             // (no clamp here: tau' is affine along the line, and the first candidate
             // may lie in the zero border behind a close source with tau' < 0 --
             // clamping it shifted every later candidate's tau'; only the
@@ -349,7 +352,7 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
                 const float2 kk = make_float2(kf, kf);
                 const float2 z11 = k ? __ffma2_rn(kk, make_float2(R.dz, R.dz), z0) : z0;
                 const float2 r = k ? __ffma2_rn(kk, make_float2(dr, dr), r0) : r0;
-                const float2 B = k ? __ffma2_rn(kk, make_float2(R.tq, R.tq), B0) : B0;
+                const float2 B = (k && CLAMP != 2) ? __ffma2_rn(kk, make_float2(R.tq, R.tq), B0) : B0;
                 const float2 t11 = make_float2(sat_fma(kf, dzC, u11.x), sat_fma(kf, dzC, u11.y));
                 const float2 t12 = make_float2(sat_fma(kf, dzC2, u12.x), sat_fma(kf, dzC2, u12.y));
                 const float2 t21 = make_float2(sat_fma(kf, dzC, u21.x), sat_fma(kf, dzC, u21.y));
@@ -366,7 +369,9 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
                 // tau' > 0 at every pixel a ray's support reaches; candidates in the zero
                 // border behind a close source can have tau' <= 0: keep 1/tau' finite
                 // (their image values are 0)
-                const float2 iB = CLAMP ? rcp2(make_float2(fmaxf(B.x, 1e-30f), fmaxf(B.y, 1e-30f))) : rcp2(B);
+                const float2 iB = CLAMP == 1   ? rcp2(make_float2(fmaxf(B.x, 1e-30f), fmaxf(B.y, 1e-30f)))
+                                  : CLAMP == 2 ? make_float2(iBpar, iBpar)
+                                               : rcp2(B);
                 if constexpr (S == 1) {
                     const float2 cw = __fmul2_rn(make_float2(ca[0], cb[0]), iB);
                     acc[0] = __ffma2_rn(cw, num, acc[0]);
@@ -393,7 +398,7 @@ __device__ __forceinline__ void fp_walk(const FPRay& R, int i0, int i1, int n, i
     }
 }
 
-template <int K, int S, bool PRE, int NT, bool CLAMP = true>
+template <int K, int S, bool PRE, int NT, int CLAMP = 1>
 __device__ __forceinline__ void fp_walk_k(const FPRay& R, int mab, int i0, int i1, int n, int np,
                                           int P, double* out)
 {
@@ -479,7 +484,7 @@ __device__ void fp_walk_prec(const FPRay& R, const FPRayD& D, int K, int i0, int
 // shared memory (deterministic).  A CTA covers 128 / PARTS bins.  PARTS > 1
 // when the grid would otherwise be short of ~16 waves: the ragged last wave
 // of a 1.6-wave grid cost ~25 %.
-template <int S, int PARTS, bool PREC = false, bool CLAMP = true>
+template <int S, int PARTS, bool PREC = false, int CLAMP = 1>
 __global__ void __launch_bounds__(fp_threads(PARTS), PARTS > 4 ? CBP_FP_P8_MINB : (S == 1 ? 7 : (S == 4 ? CBP_FP_S4_MINB : 4)))
     cbp_fp_kernel(const FPParams P)
 {
