@@ -1150,7 +1150,7 @@ int launch_bp_seg(const cbp_geometry_t& g, const cbp::Tables& t, const float* si
     return cudaGetLastError() == cudaSuccess ? CBP_OK : CBP_ECUDA;
 }
 
-template <int S, bool PREC = false, int W = 0>
+template <int S, bool PREC = false, int W = 0, bool PAR = false>
 int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
                 int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream,
                 int symmode = 0, int images = 1)
@@ -1173,10 +1173,10 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     static std::once_flag attr[64];
     static int per_sm[64];
     std::call_once(attr[dev & 63], [smem, dev] {
-        cudaFuncSetAttribute(cbp::cbp_bp_kernel<S, PREC, false, false, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(cbp::cbp_bp_kernel<S, PREC, false, false, W, PAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         int k = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_bp_kernel<S, PREC, false, false, W>, cbp::BP_THREADS,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, cbp::cbp_bp_kernel<S, PREC, false, false, W, PAR>, cbp::BP_THREADS,
                                                           smem) != cudaSuccess || k < 1)
             k = 1;
         per_sm[dev & 63] = k;
@@ -1236,7 +1236,7 @@ int launch_bp_s(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino
     P.seg_idx = P.cta_seg = nullptr;
     P.seg_max = 0;
     P.prof = bp_prof_begin((size_t)grid.x * grid.y * grid.z);
-    launch_pdl(cbp::cbp_bp_kernel<S, PREC, false, false, W>, grid, dim3(cbp::BP_THREADS), smem, stream, P);
+    launch_pdl(cbp::cbp_bp_kernel<S, PREC, false, false, W, PAR>, grid, dim3(cbp::BP_THREADS), smem, stream, P);
     ++g_launches;
     bp_prof_end(P.prof, (size_t)grid.x * grid.y * grid.z, stream);
 #ifdef CBP_DEBUG_CHECKS
@@ -1273,6 +1273,19 @@ bool bp_wide(const cbp_geometry_t& g)
     return cbp::BP_TILE * g.pixel * m * (4.0 / M_PI) / g.det_pitch > 68.0;
 }
 
+// the 8-frame BP over base views [v0, v0 + nv): the chunk shape (bp_wide)
+// and, in parallel beam, the weight with tau' = tau (PAR)
+int launch_bp_sym8(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img, int32_t batch,
+                   int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream, int images)
+{
+    const bool wide = bp_wide(g), par = g.kind == CBP_PARALLEL;
+    if (par)
+        return wide ? launch_bp_s<8, false, 1, true>(g, t, sino, img, batch, v0, nv, accumulate, stream, 8, images)
+                    : launch_bp_s<8, false, 0, true>(g, t, sino, img, batch, v0, nv, accumulate, stream, 8, images);
+    return wide ? launch_bp_s<8, false, 1>(g, t, sino, img, batch, v0, nv, accumulate, stream, 8, images)
+                : launch_bp_s<8>(g, t, sino, img, batch, v0, nv, accumulate, stream, 8, images);
+}
+
 int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, float* img,
               int32_t batch, int32_t v0, int32_t nv, int32_t accumulate, cudaStream_t stream)
 {
@@ -1283,16 +1296,15 @@ int launch_bp(const cbp_geometry_t& g, const cbp::Tables& t, const float* sino, 
     static const bool force_s1 = getenv("CBP_BP_FORCE_S1") != nullptr;
     if (force_s1) return launch_bp_s<1>(g, t, sino, img, batch, v0, nv, accumulate, stream);
     if (use_sym8(g, batch, v0, nv))
-        return bp_wide(g) ? launch_bp_s<8, false, 1>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8)
-                          : launch_bp_s<8>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8);
+        return launch_bp_sym8(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 1);
     if (batch > 1 && use_sym8(g, 1, v0, nv))  // a batch: the 8 frames of each image
-        return bp_wide(g) ? launch_bp_s<8, false, 1>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream,
-                                                     8, batch)
-                          : launch_bp_s<8>(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, 8, batch);
+        return launch_bp_sym8(g, t, sino, img, batch, 0, g.n_views / 8 + 1, accumulate, stream, batch);
     if (use_sym4(g, batch, v0, nv))
         return launch_bp_s<4>(g, t, sino, img, batch, 0, g.n_views / 4, accumulate, stream, 4);
     if (batch >= 4) return launch_bp_s<4>(g, t, sino, img, batch, v0, nv, accumulate, stream);
     if (batch >= 2) return launch_bp_s<2>(g, t, sino, img, batch, v0, nv, accumulate, stream);
+    if (g.kind == CBP_PARALLEL)  // tau' = tau: the weight's tau' terms leave the loop
+        return launch_bp_s<1, false, 0, true>(g, t, sino, img, batch, v0, nv, accumulate, stream);
     return launch_bp_s<1>(g, t, sino, img, batch, v0, nv, accumulate, stream);
 }
 
@@ -1700,8 +1712,7 @@ int cbp_back_dihedral(const cbp_geometry_t* g, const float* sino, float* image, 
     if (g->model == CBP_MODEL_MAG || precise(*g))
         return block_dihedral(*g, t, image, const_cast<float*>(sino), base_begin, base_count, accumulate, stream,
                               false);
-    return bp_wide(*g) ? launch_bp_s<8, false, 1>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 8)
-                       : launch_bp_s<8>(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 8);
+    return launch_bp_sym8(*g, t, sino, image, 1, base_begin, base_count, accumulate, stream, 1);
 }
 
 // ---- row f1: SART / CGLS building blocks ---------------------------------

@@ -336,6 +336,9 @@ __global__ void __launch_bounds__(128) cbp_bp_header_kernel(GeomDev g, Tables t,
 // pairs along x for ray directions within 45 degrees of the x axis
 __host__ __device__ inline bool bucket_horiz(int b) { return b < BP_BUCKETS / 4 || b >= 3 * BP_BUCKETS / 4; }
 
+// PAR (parallel beam, tau' = tau): b.x, b.y carry 1 - tau / C and 1 / tau in
+// place of the tau' slopes (zero there), for bp_weight<true>
+template <bool PAR = false>
 __device__ void bp_build_entry(const GeomDev& g, const Tables& t, const BPHeader& H, int j, float y,
                                BPEntry& E)
 {
@@ -360,6 +363,7 @@ __device__ void bp_build_entry(const GeomDev& g, const Tables& t, const BPHeader
     const bool horiz = bucket_horiz(H.bucket);
     E.b = make_float4(tx, ty, horiz ? zsx : zsy, horiz ? tx : ty);
     E.c = make_float4(A, 1.0f / C, 0.5f * C, y * (h * h / A));
+    if constexpr (PAR) E.b = make_float4(fmaf(-Ba, E.c.y, 1.0f), 1.0f / Ba, E.b.z, 0.0f);
 }
 
 // The precise mode (narrow bins, cbp_common.cuh cnsf_prec): s' at the anchor,
@@ -417,9 +421,18 @@ __device__ __forceinline__ void bp_pair_prec(const BPEntryP* row, int jl, int jh
 
 // one entry, one pixel pair (lane b = lane a + one pixel along the pair axis):
 // returns num / tau' for both pixels (the weight without the h^2/A factor)
+template <bool PAR = false>
 __device__ __forceinline__ float2 bp_weight(const BPEntry* e, float dc, float dr)
 {
     const float4 ea = e->a, eb = e->b, ec = e->c;
+    if constexpr (PAR) {  // parallel beam: tau' = tau (ea.w), w1 and 1 / tau from the entry
+        const float za = fmaf(dr, ea.z, fmaf(dc, ea.y, ea.x));
+        const float2 z11 = make_float2(za, za + eb.z);
+        const float2 B = make_float2(ea.w, ea.w);
+        const float2 z21 = __fadd2_rn(z11, make_float2(-ec.x, -ec.x));
+        const float2 num = cnsf_num2(z11, z21, B, make_float2(eb.x, eb.x), ec.x, ec.y, ec.z);
+        return __fmul2_rn(num, make_float2(eb.y, eb.y));
+    }
     const float za = fmaf(dr, ea.z, fmaf(dc, ea.y, ea.x));
     const float Ba = fmaf(dr, eb.y, fmaf(dc, eb.x, ea.w));
     const float2 z11 = make_float2(za, za + eb.z);
@@ -434,7 +447,7 @@ __device__ __forceinline__ float2 bp_weight(const BPEntry* e, float dc, float dr
 // formed outside the row: the trip count is an integer).  S == 1: the entry's
 // c.w is y h^2/A.  S > 1: c.w is h^2/A and the S raw y values of the entry
 // are yrow[entry * S + q] (staged from the sinogram by bp_y_load).
-template <int S>
+template <int S, bool PAR = false>
 __device__ __forceinline__ void bp_pair(const BPEntry* row, const float* yrow, int jl, int jh,
                                         int base, float dc, float dr, float2 (&acc)[S])
 {
@@ -445,12 +458,12 @@ __device__ __forceinline__ void bp_pair(const BPEntry* row, const float* yrow, i
     const float* ys = yrow + (jl - base) * S;
     for (int k = 0; k < cnt; ++k, ++e, ys += S) {
         if constexpr (S == 1) {
-            const float2 w = bp_weight(e, dc, dr);
+            const float2 w = bp_weight<PAR>(e, dc, dr);
             const float yw = e->c.w;
             acc[0] = __ffma2_rn(make_float2(yw, yw), w, acc[0]);
         } else {
             const float hA = e->c.w;
-            const float2 w = __fmul2_rn(bp_weight(e, dc, dr), make_float2(hA, hA));
+            const float2 w = __fmul2_rn(bp_weight<PAR>(e, dc, dr), make_float2(hA, hA));
             if constexpr (S == 2) {
                 const float2 y2 = *reinterpret_cast<const float2*>(ys);
                 acc[0] = __ffma2_rn(make_float2(y2.x, y2.x), w, acc[0]);
@@ -484,7 +497,7 @@ constexpr bool BP_UNION = S == 8 && CBP_BP_UNION8;
 
 // two pixel pairs over the same entries [jl, jh] (one set of shared loads,
 // two independent weight chains)
-template <int S>
+template <int S, bool PAR = false>
 __device__ __forceinline__ void bp_pair2(const BPEntry* row, const float* yrow, int jl, int jh, int base,
                                          float dc0, float dr0, float dc1, float dr1, float2 (&a0)[S],
                                          float2 (&a1)[S])
@@ -497,13 +510,13 @@ __device__ __forceinline__ void bp_pair2(const BPEntry* row, const float* yrow, 
     for (int k = 0; k < cnt; ++k, ++e, ys += S) {
         if constexpr (S == 1) {
             const float yw = e->c.w;
-            const float2 w0 = bp_weight(e, dc0, dr0), w1 = bp_weight(e, dc1, dr1);
+            const float2 w0 = bp_weight<PAR>(e, dc0, dr0), w1 = bp_weight<PAR>(e, dc1, dr1);
             a0[0] = __ffma2_rn(make_float2(yw, yw), w0, a0[0]);
             a1[0] = __ffma2_rn(make_float2(yw, yw), w1, a1[0]);
         } else {
             const float hA = e->c.w;
-            const float2 w0 = __fmul2_rn(bp_weight(e, dc0, dr0), make_float2(hA, hA));
-            const float2 w1 = __fmul2_rn(bp_weight(e, dc1, dr1), make_float2(hA, hA));
+            const float2 w0 = __fmul2_rn(bp_weight<PAR>(e, dc0, dr0), make_float2(hA, hA));
+            const float2 w1 = __fmul2_rn(bp_weight<PAR>(e, dc1, dr1), make_float2(hA, hA));
             if constexpr (S == 2) {
                 const float2 y2 = *reinterpret_cast<const float2*>(ys);
                 a0[0] = __ffma2_rn(make_float2(y2.x, y2.x), w0, a0[0]);
@@ -743,7 +756,7 @@ __device__ void bp_orbit_epilogue(const BPParams& P, float* acc_s, const int (&m
 
 // One CTA's work on one tile over views [vg0, vg0 + vgn) of the launch (view
 // group grp, slice group sg; seg: the segment of a persistent launch).
-template <int S, bool PREC, bool ORB, bool SEG, int W = 0>
+template <int S, bool PREC, bool ORB, bool SEG, int W = 0, bool PAR = false>
 __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_y, int tiles_x, int vg0, int vgn,
                                         int grp, int sg, int seg, const int (&omem)[8], int osize)
 {
@@ -794,9 +807,10 @@ __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_
                                             tab[vi][jj]);
                     } else if constexpr (S == 1) {
                         const size_t yo = (size_t)(vg0 + vc + vi) * g.n_det + j;
-                        bp_build_entry(g, P.t, H, j, __ldg(P.sino + (size_t)sg * sino_plane + yo), tab[vi][jj]);
+                        bp_build_entry<PAR>(g, P.t, H, j, __ldg(P.sino + (size_t)sg * sino_plane + yo),
+                                            tab[vi][jj]);
                     } else {
-                        bp_build_entry(g, P.t, H, j, 1.0f, tab[vi][jj]);  // c.w = h^2 / A
+                        bp_build_entry<PAR>(g, P.t, H, j, 1.0f, tab[vi][jj]);  // c.w = h^2 / A
                     }
                 }
             }
@@ -943,14 +957,14 @@ __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_
                         jl2 = min(jl2, jl);
                         jh2 = max(jh2, jh);
                     } else if (p == 0) {
-                        bp_pair<S>(row, yrow, jl, jh, base, dcp.x, drp.x, a0);
+                        bp_pair<S, PAR>(row, yrow, jl, jh, base, dcp.x, drp.x, a0);
                     } else {
-                        bp_pair<S>(row, yrow, jl, jh, base, dcp.x, drp.x, a1);
+                        bp_pair<S, PAR>(row, yrow, jl, jh, base, dcp.x, drp.x, a1);
                     }
                 }
                 // both pairs over the union (weights outside a pixel's support are exactly 0)
                 if constexpr (BP_UNION<S>)
-                    bp_pair2<S>(row, yrow, jl2, jh2, base, dc0.x, dr0.x, dc1.x, dr1.x, a0, a1);
+                    bp_pair2<S, PAR>(row, yrow, jl2, jh2, base, dc0.x, dr0.x, dc1.x, dr1.x, a0, a1);
             }
             // the next pass rebuilds tab (the next chunk's top barrier covers S > 1)
             if (!STAGE || pass + 1 < npass) __syncthreads();
@@ -1043,7 +1057,7 @@ __device__ __forceinline__ void bp_body(const BPParams& P, int tile_x, int tile_
     }
 }
 
-template <int S, bool PREC = false, bool ORB = false, bool SEG = false, int W = 0>
+template <int S, bool PREC = false, bool ORB = false, bool SEG = false, int W = 0, bool PAR = false>
 __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp_bp_kernel(const BPParams P)
 {
     int omem[8], osize = 1;
@@ -1112,7 +1126,7 @@ __global__ void __launch_bounds__(BP_THREADS, S == 1 ? 4 : (S == 4 ? 3 : 2)) cbp
         vgn = max(0, min(per, vgn - part * per));
     }
     if (!ORB) prof_feat(tile_y * tiles_x + tile_x, vg0, vgn);
-    bp_body<S, PREC, ORB, SEG, W>(P, tile_x, tile_y, tiles_x, vg0, vgn, grp, sg, 0, omem, osize);
+    bp_body<S, PREC, ORB, SEG, W, PAR>(P, tile_x, tile_y, tiles_x, vg0, vgn, grp, sg, 0, omem, osize);
     prof_end(1);
 }
 
